@@ -1,0 +1,180 @@
+/*
+ * invop_b200.h — C ABI of libinvop_b200.so, the B200 (sm_100a) implementation
+ * of the quantized inverse-operator apply of arXiv 1602.00001 (reference
+ * package `invop`).
+ *
+ * The reference binds its hot path through one Python-level seam,
+ *   invop._kernels.plan_apply(col_ptr, group_coeff, group_ptr, entry_rows,
+ *                             entry_signs, x, out) -> (mults, adds)
+ *   (/root/reference/pkg/src/invop/_kernels/_native.pyx:15-49, selected in
+ *    /root/reference/pkg/src/invop/_kernels/__init__.py:14-39)
+ * which takes HOST CSC group tables. That is the wrong granularity for a device
+ * layout (5 B/entry + 16 B/group of pointer-chasing), so this ABI moves the seam
+ * up to the plan level: a plan owns the quantized operator in a compressed
+ * device layout (narrow integer codes stored as byte planes), and every entry
+ * point below replaces one reference function, cited per declaration.
+ *
+ * Conventions
+ *  - Plain C types only: pointers, int64_t sizes, int status codes.
+ *  - Every function returns INVOP_OK (0) or a negative-free status code; the
+ *    message of the last failure on the calling thread is invop_last_error().
+ *  - "device" pointers are CUDA device memory of the current device; "host"
+ *    pointers are ordinary (preferably pinned) host memory.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    All device work is stream-ordered and asynchronous unless stated.
+ *  - Matrices are row-major; a plan holds rows [row0, row0+rows) of an n x n
+ *    operator (a row shard; row0 = 0 and rows = n for the whole operator).
+ *  - Vectors for multi-RHS calls are stored RHS-major: X[t*ldx + j] is entry j
+ *    of right-hand side t; Y[t*ldy + i] is output row (row0+i) of RHS t.
+ */
+#ifndef INVOP_B200_H
+#define INVOP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct invop_plan invop_plan;
+typedef struct invop_operator invop_operator;
+
+/* status codes (mirror the reference error hierarchy,
+   /root/reference/pkg/src/invop/errors.py:4-25) */
+enum {
+  INVOP_OK = 0,
+  INVOP_E_VALUE = 1,       /* ValueError: bad shape / argument            */
+  INVOP_E_OVERFLOW = 2,    /* MantissaOverflowError (quant.py:58-64)      */
+  INVOP_E_CAPACITY = 3,    /* CapacityError (grid.py:149-154)             */
+  INVOP_E_SINGULAR = 4,    /* SingularMatrixError (dense.py:54-60)        */
+  INVOP_E_CUDA = 5,        /* CUDA runtime failure                         */
+  INVOP_E_UNSUPPORTED = 6  /* valid request this build cannot serve      */
+};
+
+/* arithmetic of an apply */
+enum { INVOP_F32 = 0, INVOP_F64 = 1 };
+/* INVOP_MODE_ORDERED: fp64, each output row accumulates (mant*10^-m)*x_j in
+   ascending column order, zero mantissas skipped — bitwise equal to the
+   reference apply (applyplan.py:4-8, _native.pyx:32-46).
+   INVOP_MODE_FAST: fp32 grouped-sum apply, sum_j mant_ij*x_j accumulated in
+   fp32, multiplied by 10^-m once per row. */
+enum { INVOP_MODE_FAST = 0, INVOP_MODE_ORDERED = 1 };
+
+const char* invop_last_error(void);
+int invop_abi_version(void);
+
+/* A1 — quantize (reference: invop.quantize, quant.py:48-65).
+   entries: device fp64 [rows x cols] (leading dim ld). mant: device int64
+   [rows x cols] (leading dim ldm). Rounds half away from zero exactly like
+   numpy: copysign(floor(|e*10^d|+0.5), e*10^d). If any |mantissa| > 2^53 the
+   call returns INVOP_E_OVERFLOW and *bad_index = i*cols + j of the first
+   maximal offender (synchronous on failure check). */
+int invop_quantize(const double* entries, int64_t rows, int64_t cols, int64_t ld,
+                   int digits, int64_t* mant, int64_t ldm, int64_t* bad_index,
+                   void* stream);
+
+/* A4/A5 — build a plan (reference: invop.build_plan, applyplan.py:116-172)
+   from device int64 mantissas of rows [row0,row0+rows) of an n x n matrix.
+   Chooses the narrowest byte-plane code width that holds every mantissa. */
+int invop_plan_create(const int64_t* mant, int64_t rows, int64_t n, int64_t ldm,
+                      int64_t row0, int scale_digits, void* stream, invop_plan** out);
+
+/* Fused A1+A4: quantize device fp64 rows and encode them into a plan without
+   materialising int64 mantissas. Same overflow contract as invop_quantize. */
+int invop_plan_from_f64(const double* entries, int64_t rows, int64_t n, int64_t ld,
+                        int64_t row0, int digits, int64_t* bad_index, void* stream,
+                        invop_plan** out);
+
+/* Build a plan from the reference's CSC group tables (device arrays; the
+   layout of ApplyPlan, applyplan.py:42-98). Used for the drop-in of the
+   _kernels.plan_apply seam. */
+int invop_plan_from_csc(int64_t n, int scale_digits, const int64_t* col_ptr,
+                        const int64_t* group_abs_mantissa, const int64_t* group_ptr,
+                        const int32_t* entry_rows, const int8_t* entry_signs,
+                        int64_t groups, int64_t entries, void* stream, invop_plan** out);
+
+int invop_plan_destroy(invop_plan* plan);
+
+/* plan geometry and storage */
+int invop_plan_info(const invop_plan* plan, int64_t* n, int64_t* rows, int64_t* row0,
+                    int* scale_digits, int* code_bytes, int* is_signed,
+                    int64_t* device_bytes, int64_t* max_abs);
+
+/* A5/A9 — planned counters (reference: ApplyPlan.planned_multiplications /
+   planned_additions, applyplan.py:92-98; quant.sparsity_stats :73-82).
+   adds = number of nonzero mantissas; mults = sum over columns of the number
+   of distinct nonzero |mantissa| in that column (over the plan's rows).
+   Computed on device on first request and cached (synchronous). */
+int invop_plan_counts(invop_plan* plan, int64_t* mults, int64_t* adds, void* stream);
+/* per-column distinct counts (device int64[n]) and nonzeros (device int64[n]) */
+int invop_plan_column_stats(invop_plan* plan, int64_t* distinct, int64_t* nonzero,
+                            void* stream);
+
+/* A2/A3 — expand codes back to int64 mantissas (device [rows x n], ldm). */
+int invop_plan_decode(const invop_plan* plan, int64_t* mant, int64_t ldm, void* stream);
+
+/* A4 — the reference's CSC group tables, built on device from the codes.
+   Pass NULL outputs to query sizes: *groups and *entries are returned
+   (synchronous). Outputs are device arrays sized n+1, G, G, G+1, E, E. */
+int invop_plan_csc(invop_plan* plan, int64_t* col_ptr, int64_t* group_abs_mantissa,
+                   double* group_coeff, int64_t* group_ptr, int32_t* entry_rows,
+                   int8_t* entry_signs, int64_t* groups, int64_t* entries, void* stream);
+
+/* A6/A7 — apply (reference: invop.apply -> _kernels.plan_apply,
+   applyplan.py:175-191, _native.pyx:15-49).
+   x: device [nrhs x n] (ldx), y: device [nrhs x rows] (ldy), both of `dtype`.
+   mode INVOP_MODE_ORDERED requires dtype INVOP_F64.
+   y is overwritten (the reference zero-fills then accumulates, :181). */
+int invop_apply(const invop_plan* plan, const void* x, int64_t ldx, void* y, int64_t ldy,
+                int64_t nrhs, int dtype, int mode, void* stream);
+
+/* Same contract with HOST fp64 buffers x [nrhs x n], y [nrhs x rows]
+   (contiguous); the host<->device copies are part of the call (synchronous).
+   This is the end-to-end entry a reference-side binding calls. */
+int invop_apply_host(invop_plan* plan, const double* x, double* y, int64_t nrhs,
+                     int mode, void* stream);
+
+/* A8 — naive quantized apply of the reference (applyplan.py:194-209):
+   identical arithmetic to ORDERED mode; provided under its own name. */
+int invop_apply_naive(const invop_plan* plan, const double* x, double* y, int64_t nrhs,
+                      void* stream);
+
+/* A10/A11 — device construction of rows of L^-1 (setup; reference builds the
+   operator with grid.build_uniform/build_variable, grid.py:157-186, and
+   inverts it densely with dense.invert, dense.py:36-62).
+   The operator is a 5-point stencil on an nx x ny interior grid, unknown
+   p = r*nx + c (r slow): row p has diag[p] on the diagonal and -w_west[p],
+   -w_east[p], -w_south[p], -w_north[p] towards (r,c-1),(r,c+1),(r-1,c),(r+1,c);
+   couplings to outside the grid must be 0. Arrays are host fp64 [nx*ny]. */
+int invop_operator_create(int64_t nx, int64_t ny, const double* diag, const double* w_west,
+                          const double* w_east, const double* w_south,
+                          const double* w_north, void* stream, invop_operator** out);
+/* block-LU factorisation (sequential over grid lines, fp64, on device).
+   Returns INVOP_E_SINGULAR if a pivot falls below 1e-13*max|entry|. */
+int invop_operator_factor(invop_operator* op, void* stream);
+int invop_operator_destroy(invop_operator* op);
+/* rows [row0,row0+rows) of L^-1 by batched multi-RHS block solves, quantized
+   to `digits` and encoded straight into a plan (fp64 L^-1 never stored). */
+int invop_construct_rows(invop_operator* op, int64_t row0, int64_t rows, int digits,
+                         void* stream, invop_plan** out);
+/* rows [row0,row0+rows) of L^-1 in fp64 into device memory out[rows x N] (ld). */
+int invop_construct_rows_f64(invop_operator* op, int64_t row0, int64_t rows, double* out,
+                             int64_t ld, void* stream);
+
+/* A10 (generic) — inverse of an arbitrary dense fp64 matrix (device a[n x n]
+   -> device out[n x n]) by Gauss-Jordan with partial pivoting; returns
+   INVOP_E_SINGULAR if a pivot falls below `tol` (reference: dense.invert,
+   dense.py:36-62, tol = 1e-13*max|a|). Synchronous. */
+int invop_dense_invert(const double* a, int64_t n, double* out, double tol, void* stream);
+
+/* next (f2) — conventional dense multiply of the reference (_native.pyx:75-92,
+   dense.apply_dense dense.py:74-82): y_r = m[r,0]*x[0] + m[r,1]*x[1] + ...
+   accumulated left to right in fp64 without FMA (bitwise equal). Device
+   pointers, m is [rows x cols] with leading dimension ld. */
+int invop_dense_matvec(const double* m, int64_t rows, int64_t cols, int64_t ld,
+                       const double* x, double* y, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* INVOP_B200_H */

@@ -1,0 +1,162 @@
+// C ABI plumbing of libinvop_b200: errors, plan lifetime, apply entry points.
+#include "common.cuh"
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+namespace invop {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+  return INVOP_E_CUDA;
+}
+
+int num_sms() {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cached[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cached[dev] = v > 0 ? v : 1;
+  }
+  return cached[dev];
+}
+
+int ensure_scratch(void** ptr, size_t* have, size_t need) {
+  if (*have >= need && *ptr) return INVOP_OK;
+  if (*ptr) cudaFree(*ptr);
+  *ptr = nullptr;
+  *have = 0;
+  INVOP_CUDA(cudaMalloc(ptr, need > 0 ? need : 16));
+  *have = need;
+  return INVOP_OK;
+}
+
+}  // namespace invop
+
+using namespace invop;
+
+extern "C" const char* invop_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" int invop_abi_version(void) { return 1; }
+
+extern "C" int invop_plan_destroy(invop_plan* p) {
+  if (!p) return INVOP_OK;
+  for (int b = 0; b < INVOP_MAX_PLANES; ++b)
+    if (p->planes[b]) cudaFree(p->planes[b]);
+  if (p->partial) cudaFree(p->partial);
+  if (p->counters) cudaFree(p->counters);
+  if (p->dev_x) cudaFree(p->dev_x);
+  if (p->dev_y) cudaFree(p->dev_y);
+  if (p->host_pinned) cudaFreeHost(p->host_pinned);
+  delete p;
+  return INVOP_OK;
+}
+
+extern "C" int invop_plan_info(const invop_plan* p, int64_t* n, int64_t* rows, int64_t* row0,
+                               int* scale_digits, int* code_bytes, int* is_signed,
+                               int64_t* device_bytes, int64_t* max_abs) {
+  if (!p) return fail(INVOP_E_VALUE, "plan is NULL");
+  if (n) *n = p->n;
+  if (rows) *rows = p->rows;
+  if (row0) *row0 = p->row0;
+  if (scale_digits) *scale_digits = p->digits;
+  if (code_bytes) *code_bytes = p->P;
+  if (is_signed) *is_signed = p->is_signed;
+  if (device_bytes) *device_bytes = (int64_t)p->P * p->rows * p->ld;
+  if (max_abs) *max_abs = p->max_abs;
+  return INVOP_OK;
+}
+
+static bool aligned16(const void* ptr) { return ((uintptr_t)ptr & 15u) == 0; }
+
+extern "C" int invop_apply(const invop_plan* p, const void* x, int64_t ldx, void* y,
+                           int64_t ldy, int64_t nrhs, int dtype, int mode, void* stream) {
+  if (!p) return fail(INVOP_E_VALUE, "plan is NULL");
+  if (nrhs < 0) return fail(INVOP_E_VALUE, "nrhs < 0");
+  if (nrhs > 1 && (ldx < p->n || ldy < p->rows))
+    return fail(INVOP_E_VALUE, "leading dimensions too small");
+  if (nrhs == 0 || p->rows == 0) return INVOP_OK;
+  if ((!x && p->n > 0) || !y) return fail(INVOP_E_VALUE, "NULL vector");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (p->n == 0) {
+    // empty operator: rows == 0 handled above
+    return INVOP_OK;
+  }
+  if (mode == INVOP_MODE_ORDERED) {
+    if (dtype != INVOP_F64)
+      return fail(INVOP_E_VALUE, "ordered (bitwise) mode computes in fp64: dtype must be F64");
+    if (!aligned16(x) || (nrhs > 1 && (ldx & 1)))
+      return fail(INVOP_E_VALUE, "x must be 16-byte aligned with an even leading dimension");
+    return apply_ordered_launch(p, (const double*)x, nrhs > 1 ? ldx : p->n, (double*)y,
+                                nrhs > 1 ? ldy : p->rows, nrhs, s);
+  }
+  if (mode == INVOP_MODE_FAST) {
+    if (dtype != INVOP_F32) return fail(INVOP_E_VALUE, "fast mode computes in fp32: dtype F32");
+    return apply_fast_launch(p, (const float*)x, nrhs > 1 ? ldx : p->n, (float*)y,
+                             nrhs > 1 ? ldy : p->rows, nrhs, s);
+  }
+  return fail(INVOP_E_VALUE, "unknown mode");
+}
+
+__global__ void k_f64_to_f32(const double* __restrict__ a, float* __restrict__ b, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = (float)a[i];
+}
+__global__ void k_f32_to_f64(const float* __restrict__ a, double* __restrict__ b, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = (double)a[i];
+}
+
+extern "C" int invop_apply_host(invop_plan* p, const double* x, double* y, int64_t nrhs,
+                                int mode, void* stream) {
+  if (!p) return fail(INVOP_E_VALUE, "plan is NULL");
+  if (nrhs <= 0 || p->rows == 0) return INVOP_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  size_t xb = (size_t)nrhs * p->n * sizeof(double);
+  size_t yb = (size_t)nrhs * p->rows * sizeof(double);
+  // fp64 staging + fp32 copies for the fast path
+  int rc = ensure_scratch(&p->dev_x, &p->dev_x_bytes, xb + xb / 2 + 64);
+  if (rc) return rc;
+  rc = ensure_scratch(&p->dev_y, &p->dev_y_bytes, yb + yb / 2 + 64);
+  if (rc) return rc;
+  double* dx = (double*)p->dev_x;
+  double* dy = (double*)p->dev_y;
+  INVOP_CUDA(cudaMemcpyAsync(dx, x, xb, cudaMemcpyHostToDevice, s));
+  if (mode == INVOP_MODE_ORDERED) {
+    rc = invop_apply(p, dx, p->n, dy, p->rows, nrhs, INVOP_F64, mode, stream);
+    if (rc) return rc;
+  } else {
+    float* fx = (float*)((char*)p->dev_x + ((xb + 15) & ~(size_t)15));
+    float* fy = (float*)((char*)p->dev_y + ((yb + 15) & ~(size_t)15));
+    int64_t nx = nrhs * p->n, ny = nrhs * p->rows;
+    k_f64_to_f32<<<(unsigned)std::min<int64_t>(cdiv(nx, 256), 4096), 256, 0, s>>>(dx, fx, nx);
+    rc = invop_apply(p, fx, p->n, fy, p->rows, nrhs, INVOP_F32, mode, stream);
+    if (rc) return rc;
+    k_f32_to_f64<<<(unsigned)std::min<int64_t>(cdiv(ny, 256), 4096), 256, 0, s>>>(fy, dy, ny);
+  }
+  INVOP_CUDA(cudaMemcpyAsync(y, dy, yb, cudaMemcpyDeviceToHost, s));
+  INVOP_CUDA(cudaStreamSynchronize(s));
+  return INVOP_OK;
+}
+
+extern "C" int invop_apply_naive(const invop_plan* p, const double* x, double* y, int64_t nrhs,
+                                 void* stream) {
+  // apply_naive_quantized (applyplan.py:194-209) accumulates mant*scale*x_j per
+  // nonzero in ascending column order: the arithmetic of ORDERED mode.
+  if (!p) return fail(INVOP_E_VALUE, "plan is NULL");
+  return invop_apply(p, x, p->n, y, p->rows, nrhs, INVOP_F64, INVOP_MODE_ORDERED, stream);
+}

@@ -1,0 +1,518 @@
+// K2 — single/few-RHS apply of a quantized inverse operator (sm_100a).
+//
+// Reference: invop.apply -> _kernels.plan_apply
+//   /root/reference/pkg/src/invop/applyplan.py:175-191
+//   /root/reference/pkg/src/invop/_kernels/_native.pyx:15-49
+// The reference walks a CSC table of (column, |mantissa|) groups and scatters
+// +-(|v|*10^-m)*x_j into the rows. On B200 the same sum is read row-wise from
+// the compressed byte-plane layout (common.cuh) so the operator streams
+// through HBM exactly once with 128-bit coalesced loads:
+//
+//  * k2_fast (INVOP_MODE_FAST): y_i = 10^-m * sum_j v_ij x_j in fp32. The
+//    "multiply each shared value once" of the paper becomes: every integer
+//    mantissa is summed against x with one FMA, and the common factor 10^-m is
+//    applied once per row. Persistent CTAs (one per SM) own contiguous row
+//    ranges; each warp owns a fixed column piece whose x values live in
+//    registers for the whole launch, so the inner loop is LDG.128 -> PRMT ->
+//    FADD -> FFMA with no shared-memory traffic. Per-warp row partials are
+//    reduced across the column pieces once, at the end, in a fixed order
+//    (deterministic).
+//
+//  * k2_ordered (INVOP_MODE_ORDERED): the bitwise contract of the reference —
+//    each output row accumulates t=(v*10^-m)*x_j in ascending j, fp64, no FMA,
+//    zero mantissas skipped (applyplan.py:4-8). One thread per row; each warp
+//    runs its own cp.async pipeline that stages a 32-row x 128-column tile of
+//    every byte plane in XOR-swizzled shared memory so the per-thread row walk
+//    is conflict-free LDS.128.
+#include "common.cuh"
+#include <algorithm>
+
+namespace invop {
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ uint4 ldg_stream(const uint8_t* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t u4get(const uint4& v, int w) {
+  return w == 0 ? v.x : (w == 1 ? v.y : (w == 2 ? v.z : v.w));
+}
+
+constexpr uint32_t MAGIC = 0x4B000000u;  // 2^23 as fp32 bits
+constexpr float F2_23 = 8388608.0f;
+
+// 4 codes of 8-bit plane word `a` -> floats (exact)
+template <bool SIGNED>
+__device__ __forceinline__ void dec8(uint32_t a, float* f) {
+  if (SIGNED) a ^= 0x80808080u;
+  const float off = SIGNED ? (F2_23 + 128.0f) : F2_23;
+  f[0] = __int_as_float(__byte_perm(a, MAGIC, 0x7550)) - off;
+  f[1] = __int_as_float(__byte_perm(a, MAGIC, 0x7551)) - off;
+  f[2] = __int_as_float(__byte_perm(a, MAGIC, 0x7552)) - off;
+  f[3] = __int_as_float(__byte_perm(a, MAGIC, 0x7553)) - off;
+}
+// 4 codes of 16 bits from plane words a (low byte) and b (high byte) -> floats
+template <bool SIGNED>
+__device__ __forceinline__ void dec16(uint32_t a, uint32_t b, float* f) {
+  uint32_t t01 = __byte_perm(a, b, 0x5140);
+  uint32_t t23 = __byte_perm(a, b, 0x7362);
+  if (SIGNED) { t01 ^= 0x80008000u; t23 ^= 0x80008000u; }
+  const float off = SIGNED ? (F2_23 + 32768.0f) : F2_23;
+  f[0] = __int_as_float(__byte_perm(t01, MAGIC, 0x7410)) - off;
+  f[1] = __int_as_float(__byte_perm(t01, MAGIC, 0x7432)) - off;
+  f[2] = __int_as_float(__byte_perm(t23, MAGIC, 0x7410)) - off;
+  f[3] = __int_as_float(__byte_perm(t23, MAGIC, 0x7432)) - off;
+}
+
+// ------------------------------------------------------------------ k2_fast
+struct FastArgs {
+  const uint8_t* planes[4];
+  int64_t rows, n, ld;
+  float scale;
+  const float* x;
+  int64_t ldx;
+  float* y;
+  int64_t ldy;
+  int WC, WR;        // warp grid: WC column pieces x WR row lanes (WC*WR <= warps)
+  int Cp;            // 512-column steps per row
+  int nslabs;        // x register slabs
+  int64_t ngroups;   // cdiv(rows, R)
+  int slot_rows;     // rows of the per-CTA partial buffer
+};
+
+// P bytes, R rows per warp iteration, KR right-hand sides, SW max steps per
+// warp per slab (x registers = 16*SW*KR floats per lane).
+template <int P, bool SIGNED, int R, int KR, int SW>
+__global__ void __launch_bounds__(512, 1) k2_fast(FastArgs a) {
+  constexpr bool TWO = (P >= 3);  // lo16 + hi accumulators
+  extern __shared__ float slot[];  // [slot_rows][WC][KR]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t g_lo = (int64_t)blockIdx.x * a.ngroups / gridDim.x;
+  const int64_t g_hi = (int64_t)(blockIdx.x + 1) * a.ngroups / gridDim.x;
+  const int64_t row_lo = g_lo * R;
+  const int WC = a.WC, WR = a.WR;
+  const int wc = warp % WC, wr = warp / WC;
+  const bool active = warp < WC * WR;
+  const int steps_per_slab = WC * SW;
+
+  for (int slab = 0; slab < a.nslabs; ++slab) {
+    // ---- x piece of this warp into registers
+    float xr[SW][KR][16];
+    bool stepv[SW];
+    bool finite = true;
+#pragma unroll
+    for (int t = 0; t < SW; ++t) {
+      int st = slab * steps_per_slab + wc + t * WC;
+      stepv[t] = active && (wc + t * WC < steps_per_slab) && (st < a.Cp);
+      int64_t c0 = (int64_t)st * 512 + lane * 16;
+#pragma unroll
+      for (int k = 0; k < KR; ++k)
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          float v = 0.0f;
+          if (stepv[t] && c0 + q < a.n) v = a.x[k * a.ldx + c0 + q];
+          finite = finite && isfinite(v);
+          xr[t][k][q] = v;
+        }
+    }
+    const bool masked = __any_sync(0xffffffffu, !finite);
+
+    if (active) {
+      for (int64_t g = g_lo + wr; g < g_hi; g += WR) {
+        float acc[R][KR], acch[R][KR];
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int k = 0; k < KR; ++k) { acc[r][k] = 0.0f; acch[r][k] = 0.0f; }
+        int64_t rowb[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          int64_t rr = g * R + r;
+          rowb[r] = (rr < a.rows ? rr : a.rows - 1) * a.ld;
+        }
+        // issue every load of this row group first (memory-level parallelism)
+        uint4 cw[SW][R][P];
+#pragma unroll
+        for (int t = 0; t < SW; ++t) {
+          if (!stepv[t]) continue;  // warp-uniform
+          int64_t off = (int64_t)(slab * steps_per_slab + wc + t * WC) * 512 + lane * 16;
+#pragma unroll
+          for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int b = 0; b < P; ++b) cw[t][r][b] = ldg_stream(a.planes[b] + rowb[r] + off);
+        }
+#pragma unroll
+        for (int t = 0; t < SW; ++t) {
+          if (!stepv[t]) continue;
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+              float fl[4], fh[4];
+              if (P == 1) {
+                dec8<SIGNED>(u4get(cw[t][r][0], w), fl);
+              } else if (P == 2) {
+                dec16<SIGNED>(u4get(cw[t][r][0], w), u4get(cw[t][r][P > 1 ? 1 : 0], w), fl);
+              } else {
+                dec16<false>(u4get(cw[t][r][0], w), u4get(cw[t][r][P > 1 ? 1 : 0], w), fl);
+                if (P == 3) dec8<SIGNED>(u4get(cw[t][r][P > 2 ? 2 : 0], w), fh);
+                else dec16<SIGNED>(u4get(cw[t][r][P > 2 ? 2 : 0], w),
+                                   u4get(cw[t][r][P > 3 ? 3 : 0], w), fh);
+              }
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const int q = 4 * w + i;
+#pragma unroll
+                for (int k = 0; k < KR; ++k) {
+                  float xv = xr[t][k][q];
+                  if (masked) {
+                    // reference skips zero mantissas: 0*inf must not poison
+                    bool nz = TWO ? (fl[i] != 0.0f || fh[i] != 0.0f) : (fl[i] != 0.0f);
+                    if (!nz) continue;
+                  }
+                  acc[r][k] = fmaf(fl[i], xv, acc[r][k]);
+                  if (TWO) acch[r][k] = fmaf(fh[i], xv, acch[r][k]);
+                }
+              }
+            }
+          }
+        }
+        // warp reduction (butterfly) and partial store
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int k = 0; k < KR; ++k) {
+            float v = acc[r][k], h = acch[r][k];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              v += __shfl_xor_sync(0xffffffffu, v, o);
+              if (TWO) h += __shfl_xor_sync(0xffffffffu, h, o);
+            }
+            if (TWO) v = fmaf(h, 65536.0f, v);
+            if (lane == 0) {
+              int64_t lr = g * R + r - row_lo;
+              float* sp = &slot[(lr * WC + wc) * KR + k];
+              *sp = (slab == 0) ? v : (*sp + v);
+            }
+          }
+      }
+    }
+  }
+  __syncthreads();
+  // fixed-order reduction over the column pieces
+  int64_t nrows = min(g_hi * R, a.rows) - row_lo;
+  for (int64_t idx = threadIdx.x; idx < nrows * KR; idx += blockDim.x) {
+    int64_t lr = idx / KR;
+    int k = (int)(idx - lr * KR);
+    float s = 0.0f;
+    for (int c = 0; c < WC; ++c) s += slot[(lr * WC + c) * KR + k];
+    a.y[k * a.ldy + row_lo + lr] = s * a.scale;
+  }
+}
+
+template <int P, bool SIGNED, int R, int KR, int SW>
+static int launch_fast_t(FastArgs a, int grid, cudaStream_t s) {
+  size_t smem = (size_t)a.slot_rows * a.WC * KR * sizeof(float);
+  auto kern = k2_fast<P, SIGNED, R, KR, SW>;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  kern<<<grid, 512, smem, s>>>(a);
+  INVOP_CHECK_LAUNCH("k2_fast");
+  return INVOP_OK;
+}
+
+template <int P, bool SIGNED>
+static int launch_fast_p(FastArgs a, int KR, int grid, cudaStream_t s) {
+  // R and SW chosen so loads in flight (R*P*SW uint4) and x registers fit
+  // 128 registers/thread at 512 threads/SM.
+  switch (KR) {
+    case 1: return launch_fast_t<P, SIGNED, (P <= 2 ? 4 : 2), 1, 2>(a, grid, s);
+    case 2: return launch_fast_t<P, SIGNED, 2, 2, 1>(a, grid, s);
+    default: return launch_fast_t<P, SIGNED, 2, 4, 1>(a, grid, s);
+  }
+}
+
+static int fast_R(int P, int KR) { return KR == 1 ? (P <= 2 ? 4 : 2) : 2; }
+static int fast_SW(int KR) { return KR == 1 ? 2 : 1; }
+
+int apply_fast_launch(const invop_plan* p, const float* x, int64_t ldx, float* y, int64_t ldy,
+                      int64_t nrhs, cudaStream_t s) {
+  if (p->P > 4) return fail(INVOP_E_UNSUPPORTED, "fast mode needs codes of at most 4 bytes");
+  if (p->rows == 0 || nrhs == 0) return INVOP_OK;
+  const int warps = 16;
+  const int sms = num_sms();
+  int Cp = (int)(p->ld / 512);
+  for (int64_t k0 = 0; k0 < nrhs; ) {
+    int KR = nrhs - k0 >= 4 ? 4 : (nrhs - k0 >= 2 ? 2 : 1);
+    int R = fast_R(p->P, KR), SW = fast_SW(KR);
+    // warp grid: maximise useful column steps per warp
+    int bestWC = 1, bestWR = warps;
+    double best = -1.0;
+    for (int WC = 1; WC <= warps; ++WC) {
+      int WR = warps / WC;
+      int per = (int)cdiv(Cp, WC);            // steps per warp (all slabs)
+      int slabs = (int)cdiv(per, SW);
+      double eff = (double)Cp / ((double)WC * per) * (double)(WC * WR) / warps;
+      eff -= 0.01 * slabs;                     // prefer fewer slabs (x reloads)
+      if (eff > best + 1e-9) { best = eff; bestWC = WC; bestWR = WR; }
+    }
+    FastArgs a;
+    for (int b = 0; b < 4; ++b) a.planes[b] = p->planes[b < p->P ? b : 0];
+    a.rows = p->rows; a.n = p->n; a.ld = p->ld;
+    a.scale = (float)p->scale;
+    a.x = x + k0 * ldx; a.ldx = ldx;
+    a.y = y + k0 * ldy; a.ldy = ldy;
+    a.WC = bestWC; a.WR = bestWR; a.Cp = Cp;
+    a.nslabs = (int)cdiv(cdiv(Cp, bestWC), SW);
+    a.ngroups = cdiv(p->rows, R);
+    int grid = (int)std::min<int64_t>(sms, a.ngroups);
+    a.slot_rows = (int)(cdiv(a.ngroups, grid) * R);
+    size_t smem = (size_t)a.slot_rows * a.WC * KR * sizeof(float);
+    if (smem > 220 * 1024) {
+      // too many rows per CTA for the partial buffer: use more CTAs (they
+      // queue behind one another; still correct)
+      grid = (int)std::min<int64_t>(a.ngroups, cdiv((int64_t)a.ngroups * R * a.WC * KR * 4,
+                                                    200 * 1024));
+      a.slot_rows = (int)(cdiv(a.ngroups, grid) * R);
+    }
+    int rc;
+    switch (p->P * 2 + p->is_signed) {
+      case 2: rc = launch_fast_p<1, false>(a, KR, grid, s); break;
+      case 3: rc = launch_fast_p<1, true>(a, KR, grid, s); break;
+      case 4: rc = launch_fast_p<2, false>(a, KR, grid, s); break;
+      case 5: rc = launch_fast_p<2, true>(a, KR, grid, s); break;
+      case 6: rc = launch_fast_p<3, false>(a, KR, grid, s); break;
+      case 7: rc = launch_fast_p<3, true>(a, KR, grid, s); break;
+      case 8: rc = launch_fast_p<4, false>(a, KR, grid, s); break;
+      default: rc = launch_fast_p<4, true>(a, KR, grid, s); break;
+    }
+    if (rc) return rc;
+    k0 += KR;
+  }
+  return INVOP_OK;
+}
+
+// --------------------------------------------------------------- k2_ordered
+constexpr int ORD_TILE = 128;   // columns per stage
+constexpr int ORD_STAGES = 4;
+
+struct OrdArgs {
+  const uint8_t* planes[8];
+  int64_t rows, n, ld;
+  double scale;
+  const double* x;
+  int64_t ldx;
+  double* y;
+  int64_t ldy;
+};
+
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N));
+}
+
+template <int P, bool SIGNED>
+__device__ __forceinline__ double code_to_double(const uint8_t* bytes) {
+  if (P <= 4 && !SIGNED) {
+    uint32_t u = 0;
+#pragma unroll
+    for (int b = 0; b < P; ++b) u |= (uint32_t)bytes[b] << (8 * b);
+    // 2^52 + u, exact
+    return __dadd_rn(__hiloint2double(0x43300000, (int)u), -4503599627370496.0);
+  } else {
+    uint64_t u = 0;
+#pragma unroll
+    for (int b = 0; b < P; ++b) u |= (uint64_t)bytes[b] << (8 * b);
+    int64_t v;
+    if (SIGNED && P < 8) {
+      const int sh = 64 - 8 * P;
+      v = (int64_t)(u << sh) >> sh;
+    } else {
+      v = (int64_t)u;
+    }
+    return (double)v;  // exact for |v| <= 2^53 (quantize guarantees it)
+  }
+}
+
+// KR right-hand sides per pass
+template <int P, bool SIGNED, int KR>
+__global__ void __launch_bounds__(128) k2_ordered(OrdArgs a) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int CODE_BYTES = 32 * ORD_TILE;                 // per plane per stage
+  constexpr int X_BYTES = ORD_TILE * 8 * KR;                // per stage
+  constexpr int STAGE_BYTES = CODE_BYTES * P + X_BYTES;
+  unsigned char* wbase = sm + (size_t)warp * STAGE_BYTES * ORD_STAGES;
+  const uint32_t wbase_s = (uint32_t)__cvta_generic_to_shared(wbase);
+
+  const int64_t row0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * 32;
+  if (row0 >= a.rows) return;  // whole warp idle (warp-uniform)
+  const int64_t myrow = row0 + lane;
+  const int64_t ntiles = (a.n + ORD_TILE - 1) / ORD_TILE;
+
+  auto issue = [&](int64_t tile, int stage) {
+    if (tile < ntiles) {
+      const int64_t col0 = tile * ORD_TILE;
+      const uint32_t sb = wbase_s + stage * STAGE_BYTES;
+#pragma unroll
+      for (int b = 0; b < P; ++b) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          int cid = lane + 32 * i;         // 256 chunks = 32 rows x 8 chunks
+          int r = cid >> 3, c = cid & 7;
+          int64_t gr = row0 + r;
+          gr = gr < a.rows ? gr : a.rows - 1;
+          const uint8_t* src = a.planes[b] + gr * a.ld + col0 + c * 16;
+          uint32_t dst = sb + b * CODE_BYTES + r * 128 + ((c ^ (r & 7)) << 4);
+          cp_async16(dst, src);
+        }
+      }
+      // x tile: ORD_TILE doubles per rhs = 64 chunks of 16 B
+#pragma unroll
+      for (int k = 0; k < KR; ++k) {
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          int cid = lane + 32 * i;
+          int64_t col = col0 + cid * 2;
+          uint32_t dst = sb + P * CODE_BYTES + k * ORD_TILE * 8 + cid * 16;
+          if (col + 1 < a.n) {
+            cp_async16(dst, a.x + k * a.ldx + col);
+          } else {
+            // tail: scalar copy with zero fill (synchronous store)
+            double* d = reinterpret_cast<double*>(wbase + stage * STAGE_BYTES +
+                                                  P * CODE_BYTES + k * ORD_TILE * 8 + cid * 16);
+            d[0] = col < a.n ? a.x[k * a.ldx + col] : 0.0;
+            d[1] = 0.0;
+          }
+        }
+      }
+    }
+    cp_async_commit();
+  };
+
+#pragma unroll
+  for (int s = 0; s < ORD_STAGES - 1; ++s) issue(s, s);
+
+  double acc[KR];
+#pragma unroll
+  for (int k = 0; k < KR; ++k) acc[k] = 0.0;
+  const int sr = lane;  // my row inside the tile
+  for (int64_t t = 0; t < ntiles; ++t) {
+    issue(t + ORD_STAGES - 1, (int)((t + ORD_STAGES - 1) % ORD_STAGES));
+    cp_async_wait<ORD_STAGES - 1>();
+    __syncwarp();
+    const unsigned char* sb = wbase + (t % ORD_STAGES) * STAGE_BYTES;
+    const double* xs = reinterpret_cast<const double*>(sb + P * CODE_BYTES);
+    const int64_t col0 = t * ORD_TILE;
+    const int cend = (int)min((int64_t)ORD_TILE, a.n - col0);
+    bool fin = true;
+#pragma unroll
+    for (int k = 0; k < KR; ++k)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) fin = fin && isfinite(xs[k * ORD_TILE + lane * 4 + i]);
+    const bool masked = __any_sync(0xffffffffu, !fin);
+#pragma unroll 1
+    for (int c = 0; c < 8; ++c) {
+      if (c * 16 >= cend) break;
+      uint4 w[P];
+#pragma unroll
+      for (int b = 0; b < P; ++b)
+        w[b] = *reinterpret_cast<const uint4*>(sb + b * CODE_BYTES + sr * 128 +
+                                               ((c ^ (sr & 7)) << 4));
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        uint8_t bytes[P];
+#pragma unroll
+        for (int b = 0; b < P; ++b) bytes[b] = (uint8_t)(u4get(w[b], q >> 2) >> (8 * (q & 3)));
+        // For finite x, adding (0*10^-m)*x_j = +-0 leaves the accumulator
+        // bitwise unchanged (it starts at +0 and x+(-x) rounds to +0), so the
+        // reference's zero skip only matters when the tile holds inf/nan.
+        bool take = true;
+        if (masked) {
+          take = false;
+#pragma unroll
+          for (int b = 0; b < P; ++b) take |= bytes[b] != 0;
+        }
+        if (take) {
+          const double d = __dmul_rn(code_to_double<P, SIGNED>(bytes), a.scale);
+#pragma unroll
+          for (int k = 0; k < KR; ++k)
+            acc[k] = __dadd_rn(acc[k], __dmul_rn(d, xs[k * ORD_TILE + c * 16 + q]));
+        }
+      }
+    }
+    __syncwarp();
+  }
+  cp_async_wait<0>();
+  if (myrow < a.rows) {
+#pragma unroll
+    for (int k = 0; k < KR; ++k) a.y[k * a.ldy + myrow] = acc[k];
+  }
+}
+
+template <int P, bool SIGNED, int KR>
+static int launch_ord_t(OrdArgs a, cudaStream_t s) {
+  constexpr int STAGE_BYTES = 32 * ORD_TILE * P + ORD_TILE * 8 * KR;
+  size_t per_warp = (size_t)STAGE_BYTES * ORD_STAGES;
+  int wpb = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / per_warp));
+  size_t smem = per_warp * wpb;
+  auto kern = k2_ordered<P, SIGNED, KR>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int64_t warps = cdiv(a.rows, 32);
+  int64_t grid = cdiv(warps, wpb);
+  kern<<<(unsigned)grid, wpb * 32, smem, s>>>(a);
+  INVOP_CHECK_LAUNCH("k2_ordered");
+  return INVOP_OK;
+}
+
+template <int P, bool SIGNED>
+static int launch_ord_p(OrdArgs a, int KR, cudaStream_t s) {
+  if (KR >= 4 && P <= 4) return launch_ord_t<P, SIGNED, 4>(a, s);
+  if (KR >= 2) return launch_ord_t<P, SIGNED, 2>(a, s);
+  return launch_ord_t<P, SIGNED, 1>(a, s);
+}
+
+int apply_ordered_launch(const invop_plan* p, const double* x, int64_t ldx, double* y,
+                         int64_t ldy, int64_t nrhs, cudaStream_t s) {
+  if (p->rows == 0 || nrhs == 0) return INVOP_OK;
+  for (int64_t k0 = 0; k0 < nrhs;) {
+    int KR = nrhs - k0 >= 4 && p->P <= 4 ? 4 : (nrhs - k0 >= 2 ? 2 : 1);
+    OrdArgs a;
+    for (int b = 0; b < 8; ++b) a.planes[b] = p->planes[b < p->P ? b : 0];
+    a.rows = p->rows; a.n = p->n; a.ld = p->ld; a.scale = p->scale;
+    a.x = x + k0 * ldx; a.ldx = ldx;
+    a.y = y + k0 * ldy; a.ldy = ldy;
+    int rc;
+    switch (p->P * 2 + p->is_signed) {
+      case 2: rc = launch_ord_p<1, false>(a, KR, s); break;
+      case 3: rc = launch_ord_p<1, true>(a, KR, s); break;
+      case 4: rc = launch_ord_p<2, false>(a, KR, s); break;
+      case 5: rc = launch_ord_p<2, true>(a, KR, s); break;
+      case 6: rc = launch_ord_p<3, false>(a, KR, s); break;
+      case 7: rc = launch_ord_p<3, true>(a, KR, s); break;
+      case 8: rc = launch_ord_p<4, false>(a, KR, s); break;
+      case 9: rc = launch_ord_p<4, true>(a, KR, s); break;
+      case 10: rc = launch_ord_p<5, false>(a, KR, s); break;
+      case 11: rc = launch_ord_p<5, true>(a, KR, s); break;
+      case 12: rc = launch_ord_p<6, false>(a, KR, s); break;
+      case 13: rc = launch_ord_p<6, true>(a, KR, s); break;
+      case 14: rc = launch_ord_p<7, false>(a, KR, s); break;
+      case 15: rc = launch_ord_p<7, true>(a, KR, s); break;
+      case 16: rc = launch_ord_p<8, false>(a, KR, s); break;
+      default: rc = launch_ord_p<8, true>(a, KR, s); break;
+    }
+    if (rc) return rc;
+    k0 += KR;
+  }
+  return INVOP_OK;
+}
+
+}  // namespace invop

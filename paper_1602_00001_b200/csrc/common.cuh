@@ -1,0 +1,88 @@
+// Shared definitions for libinvop_b200 (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include "../../include/invop_b200.h"
+
+#define INVOP_MAX_PLANES 8
+
+// Compressed device layout of a quantized operator shard.
+//
+// A mantissa v (int64) of row i, column j is stored as P little-endian bytes,
+// byte b in plane b: planes[b][i*ld + j] = (v >> 8b) & 0xff. P is the smallest
+// width that holds every mantissa (two's complement when any mantissa < 0).
+// ld (bytes per plane row) is n rounded up to 128 so every row of every plane
+// starts 128-byte aligned; padding bytes are 0. Keeping bytes in separate
+// planes lets (a) the fp32 apply assemble 16-bit halves with PRMT and
+// (b) the tensor-core batched apply feed each plane straight to an 8-bit MMA.
+struct invop_plan {
+  int64_t n = 0, rows = 0, row0 = 0, ld = 0;
+  int digits = 0;
+  double scale = 1.0;  // 10.0 ** -digits, bit-identical to Python's value
+  int P = 1;
+  int is_signed = 0;
+  uint8_t* planes[INVOP_MAX_PLANES] = {nullptr};
+  int64_t min_val = 0, max_val = 0, max_abs = 0;
+  int64_t nnz = 0;     // planned additions (E)
+  int64_t mults = -1;  // planned multiplications (G), lazily computed
+  int device = 0;
+  // scratch owned by the plan (grown on demand)
+  float* partial = nullptr; size_t partial_bytes = 0;
+  int* counters = nullptr; size_t counters_n = 0;
+  void* dev_x = nullptr; size_t dev_x_bytes = 0;
+  void* dev_y = nullptr; size_t dev_y_bytes = 0;
+  double* host_pinned = nullptr; size_t host_pinned_bytes = 0;
+};
+
+struct invop_operator {
+  int64_t nx = 0, ny = 0, N = 0;
+  double* diag = nullptr;  // device [N]
+  double* ww = nullptr;    // device [N] west weights
+  double* we = nullptr;
+  double* ws = nullptr;
+  double* wn = nullptr;
+  double* dinv = nullptr;  // device [ny][nx][nx]: inverses of Schur blocks
+  double* qmat = nullptr;  // device [ny][nx][nx]: Dinv_k * diag(up_k)
+  double max_entry = 0.0;
+  int factored = 0;
+};
+
+namespace invop {
+
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define INVOP_CUDA(call)                                   \
+  do {                                                     \
+    cudaError_t _e = (call);                               \
+    if (_e != cudaSuccess) return ::invop::cuda_fail(_e, #call); \
+  } while (0)
+
+#define INVOP_CHECK_LAUNCH(what) INVOP_CUDA(cudaGetLastError())
+
+__host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+__host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+int num_sms();
+int ensure_scratch(void** ptr, size_t* have, size_t need);
+
+// encode.cu
+int encode_int64(invop_plan* p, const int64_t* mant, int64_t ldm, cudaStream_t s);
+int plan_alloc_planes(invop_plan* p, int P);
+int plan_finalize_width(invop_plan* p, int64_t mn, int64_t mx, int64_t nnz);
+// apply kernels
+int apply_fast_launch(const invop_plan* p, const float* x, int64_t ldx, float* y,
+                      int64_t ldy, int64_t nrhs, cudaStream_t s);
+int apply_ordered_launch(const invop_plan* p, const double* x, int64_t ldx, double* y,
+                         int64_t ldy, int64_t nrhs, cudaStream_t s);
+
+}  // namespace invop
+
+// exact powers of ten used by quantize (10.0 ** d for d in 0..22 is exact)
+__host__ __device__ inline double invop_pow10_exact(int d) {
+  double r = 1.0;
+  for (int i = 0; i < d; ++i) r *= 10.0;
+  return r;
+}

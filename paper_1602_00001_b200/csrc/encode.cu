@@ -1,0 +1,699 @@
+// K1 — quantize / encode / decode / plan statistics (sm_100a).
+//
+// Reference semantics:
+//   quantize          /root/reference/pkg/src/invop/quant.py:48-65
+//   sparsity_stats    /root/reference/pkg/src/invop/quant.py:73-82
+//   build_plan tables /root/reference/pkg/src/invop/applyplan.py:116-172
+// All of this is setup work (once per operator); it is bandwidth-bound and
+// kept simple: grid-stride loops with 8-byte loads, block reductions, one
+// atomic per block.
+#include "common.cuh"
+#include <algorithm>
+#include <vector>
+#include <cstring>
+
+namespace invop {
+
+// ---------------------------------------------------------------- helpers
+__device__ __forceinline__ int64_t warp_min64(int64_t v) {
+  for (int o = 16; o > 0; o >>= 1) v = min(v, (int64_t)__shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ int64_t warp_max64(int64_t v) {
+  for (int o = 16; o > 0; o >>= 1) v = max(v, (int64_t)__shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ int64_t warp_sum64(int64_t v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// stats[0]=min, stats[1]=max, stats[2]=nnz  (block-reduced, one atomic each)
+__device__ void block_stats_commit(int64_t mn, int64_t mx, int64_t nz, long long* stats) {
+  __shared__ int64_t s_mn[32], s_mx[32], s_nz[32];
+  mn = warp_min64(mn); mx = warp_max64(mx); nz = warp_sum64(nz);
+  int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) { s_mn[w] = mn; s_mx[w] = mx; s_nz[w] = nz; }
+  __syncthreads();
+  if (w == 0) {
+    int nw = blockDim.x >> 5;
+    mn = l < nw ? s_mn[l] : INT64_MAX;
+    mx = l < nw ? s_mx[l] : INT64_MIN;
+    nz = l < nw ? s_nz[l] : 0;
+    mn = warp_min64(mn); mx = warp_max64(mx); nz = warp_sum64(nz);
+    if (l == 0) {
+      atomicMin(&stats[0], (long long)mn);
+      atomicMax(&stats[1], (long long)mx);
+      atomicAdd((unsigned long long*)&stats[2], (unsigned long long)nz);
+    }
+  }
+}
+
+struct Planes {
+  uint8_t* p[INVOP_MAX_PLANES];
+};
+
+__device__ __forceinline__ int64_t load_code(const Planes& pl, int P, int is_signed,
+                                             int64_t off) {
+  uint64_t u = 0;
+  for (int b = 0; b < P; ++b) u |= (uint64_t)pl.p[b][off] << (8 * b);
+  if (is_signed && P < 8) {
+    int sh = 64 - 8 * P;
+    return (int64_t)(u << sh) >> sh;
+  }
+  return (int64_t)u;
+}
+
+// ---------------------------------------------------------------- kernels
+__global__ void k_stats_int64(const int64_t* __restrict__ mant, int64_t rows, int64_t cols,
+                              int64_t ldm, long long* stats) {
+  int64_t mn = INT64_MAX, mx = INT64_MIN, nz = 0;
+  int64_t total = rows * cols;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = k / cols, j = k - i * cols;
+    int64_t v = mant[i * ldm + j];
+    mn = min(mn, v); mx = max(mx, v); nz += (v != 0);
+  }
+  block_stats_commit(mn, mx, nz, stats);
+}
+
+__global__ void k_encode_int64(const int64_t* __restrict__ mant, int64_t rows, int64_t cols,
+                               int64_t ldm, Planes pl, int P, int64_t ld) {
+  int64_t total = rows * ld;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = k / ld, j = k - i * ld;
+    uint64_t v = j < cols ? (uint64_t)mant[i * ldm + j] : 0;
+    for (int b = 0; b < P; ++b) pl.p[b][k] = (uint8_t)(v >> (8 * b));
+  }
+}
+
+__global__ void k_decode(Planes pl, int P, int is_signed, int64_t rows, int64_t cols,
+                         int64_t ld, int64_t* __restrict__ out, int64_t ldm) {
+  int64_t total = rows * cols;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = k / cols, j = k - i * cols;
+    out[i * ldm + j] = load_code(pl, P, is_signed, i * ld + j);
+  }
+}
+
+// numpy: scaled = e * 10.0**d ; mant = copysign(floor(|scaled| + 0.5), scaled)
+__device__ __forceinline__ double round_half_away(double e, double p10) {
+  double scaled = __dmul_rn(e, p10);
+  double m = floor(__dadd_rn(fabs(scaled), 0.5));
+  return copysign(m, scaled);
+}
+
+// pass 1 of quantize: max |mantissa| (as ordered uint64 bits of the double)
+__global__ void k_quant_maxabs(const double* __restrict__ e, int64_t rows, int64_t cols,
+                               int64_t ld, double p10, unsigned long long* maxbits) {
+  unsigned long long m = 0;
+  int64_t total = rows * cols;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = k / cols, j = k - i * cols;
+    double a = fabs(round_half_away(e[i * ld + j], p10));
+    unsigned long long b = (unsigned long long)__double_as_longlong(a);
+    m = b > m ? b : m;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long t = __shfl_xor_sync(0xffffffffu, m, o);
+    m = t > m ? t : m;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(maxbits, m);
+}
+
+__global__ void k_quant_first_index(const double* __restrict__ e, int64_t rows, int64_t cols,
+                                    int64_t ld, double p10, unsigned long long target,
+                                    unsigned long long* first) {
+  int64_t total = rows * cols;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = k / cols, j = k - i * cols;
+    double a = fabs(round_half_away(e[i * ld + j], p10));
+    if ((unsigned long long)__double_as_longlong(a) == target)
+      atomicMin(first, (unsigned long long)k);
+  }
+}
+
+__global__ void k_quant_write(const double* __restrict__ e, int64_t rows, int64_t cols,
+                              int64_t ld, double p10, int64_t* __restrict__ mant, int64_t ldm) {
+  int64_t total = rows * cols;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = k / cols, j = k - i * cols;
+    mant[i * ldm + j] = (int64_t)round_half_away(e[i * ld + j], p10);
+  }
+}
+
+// fused quantize -> stats (pass A) and quantize -> planes (pass B)
+__global__ void k_quant_stats(const double* __restrict__ e, int64_t rows, int64_t cols,
+                              int64_t ld, double p10, long long* stats) {
+  int64_t mn = INT64_MAX, mx = INT64_MIN, nz = 0;
+  int64_t total = rows * cols;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = k / cols, j = k - i * cols;
+    int64_t v = (int64_t)round_half_away(e[i * ld + j], p10);
+    mn = min(mn, v); mx = max(mx, v); nz += (v != 0);
+  }
+  block_stats_commit(mn, mx, nz, stats);
+}
+
+__global__ void k_quant_encode(const double* __restrict__ e, int64_t rows, int64_t cols,
+                               int64_t lde, double p10, Planes pl, int P, int64_t ld) {
+  int64_t total = rows * ld;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = k / ld, j = k - i * ld;
+    uint64_t v = j < cols ? (uint64_t)(int64_t)round_half_away(e[i * lde + j], p10) : 0;
+    for (int b = 0; b < P; ++b) pl.p[b][k] = (uint8_t)(v >> (8 * b));
+  }
+}
+
+// ---- per-column statistics (distinct nonzero |mantissa| and nonzero count)
+// Bitmap path: a CTA owns `C` consecutive columns; each has a (maxabs+1)-bit
+// bitmap in shared memory. Rows are swept with each thread reading one code.
+__global__ void k_colstats_bitmap(Planes pl, int P, int is_signed, int64_t rows, int64_t n,
+                                  int64_t ld, int C, int64_t words_per_col,
+                                  int64_t* __restrict__ distinct, int64_t* __restrict__ nonzero) {
+  extern __shared__ uint32_t bm[];
+  int64_t j0 = (int64_t)blockIdx.x * C;
+  int ncols = (int)min((int64_t)C, n - j0);
+  for (int64_t w = threadIdx.x; w < words_per_col * C; w += blockDim.x) bm[w] = 0u;
+  __syncthreads();
+  __shared__ unsigned long long s_nz[64];
+  for (int c = threadIdx.x; c < C; c += blockDim.x) s_nz[c] = 0ull;
+  __syncthreads();
+  int64_t total = rows * ncols;
+  for (int64_t k = threadIdx.x; k < total; k += blockDim.x) {
+    int64_t i = k / ncols;
+    int c = (int)(k - i * ncols);
+    int64_t v = load_code(pl, P, is_signed, i * ld + j0 + c);
+    if (v != 0) {
+      uint64_t a = (uint64_t)(v < 0 ? -v : v);
+      atomicOr(&bm[c * words_per_col + (a >> 5)], 1u << (a & 31));
+      atomicAdd(&s_nz[c], 1ull);
+    }
+  }
+  __syncthreads();
+  int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int c = warp; c < ncols; c += nw) {
+    int64_t cnt = 0;
+    for (int64_t w = lane; w < words_per_col; w += 32) cnt += __popc(bm[c * words_per_col + w]);
+    cnt = warp_sum64(cnt);
+    if (lane == 0) {
+      distinct[j0 + c] = cnt;
+      nonzero[j0 + c] = (int64_t)s_nz[c];
+    }
+  }
+}
+
+// Sort path (any magnitude, n <= 16384): one CTA per column sorts the
+// (|v|, row) pairs of the column with a shared-memory bitonic sort. It also
+// emits the reference CSC group tables when `emit` is set.
+__device__ __forceinline__ bool pair_less(uint64_t ka, uint32_t ra, uint64_t kb, uint32_t rb) {
+  return ka < kb || (ka == kb && ra < rb);
+}
+
+__global__ void k_col_sort(Planes pl, int P, int is_signed, int64_t rows, int64_t n,
+                           int64_t ld, int npow2, int64_t* __restrict__ distinct,
+                           int64_t* __restrict__ nonzero, int emit,
+                           const int64_t* __restrict__ grp_off,   // [n] first group of column
+                           const int64_t* __restrict__ ent_off,   // [n] first entry of column
+                           int64_t* __restrict__ group_abs, double* __restrict__ group_coeff,
+                           int64_t* __restrict__ group_ptr, int32_t* __restrict__ entry_rows,
+                           int8_t* __restrict__ entry_signs, double scale) {
+  extern __shared__ unsigned char smem_raw[];
+  uint64_t* key = reinterpret_cast<uint64_t*>(smem_raw);
+  uint32_t* row = reinterpret_cast<uint32_t*>(key + npow2);
+  int8_t* sgn = reinterpret_cast<int8_t*>(row + npow2);
+  __shared__ int s_cnt[2];
+  int64_t j = blockIdx.x;
+  for (int i = threadIdx.x; i < npow2; i += blockDim.x) {
+    if (i < rows) {
+      int64_t v = load_code(pl, P, is_signed, (int64_t)i * ld + j);
+      // zeros sort to the end (key = max)
+      key[i] = v == 0 ? ~0ull : (uint64_t)(v < 0 ? -v : v);
+      sgn[i] = v < 0 ? -1 : 1;
+    } else {
+      key[i] = ~0ull;
+      sgn[i] = 1;
+    }
+    row[i] = (uint32_t)i;
+  }
+  __syncthreads();
+  for (int k = 2; k <= npow2; k <<= 1) {
+    for (int jj = k >> 1; jj > 0; jj >>= 1) {
+      for (int i = threadIdx.x; i < npow2; i += blockDim.x) {
+        int ixj = i ^ jj;
+        if (ixj > i) {
+          bool up = (i & k) == 0;
+          uint64_t ka = key[i], kb = key[ixj];
+          uint32_t ra = row[i], rb = row[ixj];
+          bool swap = up ? pair_less(kb, rb, ka, ra) : pair_less(ka, ra, kb, rb);
+          if (swap) {
+            key[i] = kb; key[ixj] = ka;
+            row[i] = rb; row[ixj] = ra;
+            int8_t t = sgn[i]; sgn[i] = sgn[ixj]; sgn[ixj] = t;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // count nonzero (prefix of non-max keys) and group starts
+  if (threadIdx.x == 0) { s_cnt[0] = 0; s_cnt[1] = 0; }
+  __syncthreads();
+  int nz_local = 0, g_local = 0;
+  for (int i = threadIdx.x; i < npow2; i += blockDim.x) {
+    if (key[i] != ~0ull) {
+      nz_local++;
+      if (i == 0 || key[i - 1] != key[i]) g_local++;
+    }
+  }
+  atomicAdd(&s_cnt[0], nz_local);
+  atomicAdd(&s_cnt[1], g_local);
+  __syncthreads();
+  int nz = s_cnt[0];
+  if (threadIdx.x == 0) {
+    distinct[j] = s_cnt[1];
+    nonzero[j] = nz;
+  }
+  if (!emit) return;
+  int64_t e0 = ent_off[j], g0 = grp_off[j];
+  for (int i = threadIdx.x; i < nz; i += blockDim.x) {
+    entry_rows[e0 + i] = (int32_t)row[i];
+    entry_signs[e0 + i] = sgn[i];
+  }
+  // group index of entry i = number of group starts in [0, i]; a single warp
+  // scans to keep it simple (columns are short here: n <= 16384)
+  if (threadIdx.x < 32) {
+    int lane = threadIdx.x;
+    int base = 0;
+    for (int i0 = 0; i0 < nz; i0 += 32) {
+      int i = i0 + lane;
+      int start = (i < nz) && (i == 0 || key[i - 1] != key[i]);
+      unsigned bal = __ballot_sync(0xffffffffu, start);
+      int pos = base + __popc(bal & ((1u << lane) - 1));
+      if (start) {
+        group_abs[g0 + pos] = (int64_t)key[i];
+        group_coeff[g0 + pos] = __dmul_rn((double)(int64_t)key[i], scale);
+        group_ptr[g0 + pos] = e0 + i;
+      }
+      base += __popc(bal);
+    }
+  }
+}
+
+__global__ void k_from_csc(int64_t n, const int64_t* __restrict__ col_ptr,
+                           const int64_t* __restrict__ gabs, const int64_t* __restrict__ gptr,
+                           const int32_t* __restrict__ rows, const int8_t* __restrict__ signs,
+                           int64_t* __restrict__ mant) {
+  // one warp per column
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (warp >= n) return;
+  int64_t j = warp;
+  for (int64_t g = col_ptr[j]; g < col_ptr[j + 1]; ++g) {
+    int64_t a = gabs[g];
+    for (int64_t e = gptr[g] + lane; e < gptr[g + 1]; e += 32)
+      mant[(int64_t)rows[e] * n + j] = signs[e] > 0 ? a : -a;
+  }
+}
+
+// ---------------------------------------------------------------- host side
+static int grid_for(int64_t total, int threads = 256) {
+  int64_t blocks = cdiv(total, threads);
+  int64_t cap = (int64_t)num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  return (int)blocks;
+}
+
+static Planes planes_of(const invop_plan* p) {
+  Planes pl;
+  for (int b = 0; b < INVOP_MAX_PLANES; ++b) pl.p[b] = p->planes[b];
+  return pl;
+}
+
+int plan_alloc_planes(invop_plan* p, int P) {
+  size_t bytes = (size_t)p->rows * (size_t)p->ld;
+  for (int b = 0; b < P; ++b) {
+    if (!p->planes[b]) {
+      INVOP_CUDA(cudaMalloc(&p->planes[b], bytes > 0 ? bytes : 1));
+    }
+  }
+  p->P = P;
+  return INVOP_OK;
+}
+
+// choose the narrowest byte width for [mn, mx]
+static int width_for(int64_t mn, int64_t mx, int* is_signed) {
+  *is_signed = mn < 0;
+  for (int P = 1; P < 8; ++P) {
+    if (*is_signed) {
+      int64_t lo = -((int64_t)1 << (8 * P - 1)), hi = ((int64_t)1 << (8 * P - 1)) - 1;
+      if (mn >= lo && mx <= hi) return P;
+    } else {
+      if ((uint64_t)mx < ((uint64_t)1 << (8 * P))) return P;
+    }
+  }
+  return 8;
+}
+
+int plan_finalize_width(invop_plan* p, int64_t mn, int64_t mx, int64_t nnz) {
+  if (p->rows == 0 || p->n == 0) { mn = 0; mx = 0; nnz = 0; }
+  p->min_val = mn;
+  p->max_val = mx;
+  int64_t amn = mn < 0 ? -mn : mn;
+  p->max_abs = amn > mx ? amn : mx;
+  p->nnz = nnz;
+  return INVOP_OK;
+}
+
+static int read_stats(long long* d_stats, long long* h, cudaStream_t s) {
+  INVOP_CUDA(cudaMemcpyAsync(h, d_stats, 3 * sizeof(long long), cudaMemcpyDeviceToHost, s));
+  INVOP_CUDA(cudaStreamSynchronize(s));
+  return INVOP_OK;
+}
+
+static int init_stats(long long* d_stats, cudaStream_t s) {
+  long long init[3] = {INT64_MAX, INT64_MIN, 0};
+  INVOP_CUDA(cudaMemcpyAsync(d_stats, init, sizeof(init), cudaMemcpyHostToDevice, s));
+  INVOP_CUDA(cudaStreamSynchronize(s));
+  return INVOP_OK;
+}
+
+int encode_int64(invop_plan* p, const int64_t* mant, int64_t ldm, cudaStream_t s) {
+  long long* d_stats = nullptr;
+  INVOP_CUDA(cudaMalloc(&d_stats, 3 * sizeof(long long)));
+  int rc = init_stats(d_stats, s);
+  if (rc) { cudaFree(d_stats); return rc; }
+  int64_t total = p->rows * p->n;
+  if (total > 0) {
+    k_stats_int64<<<grid_for(total), 256, 0, s>>>(mant, p->rows, p->n, ldm, d_stats);
+  }
+  long long h[3];
+  rc = read_stats(d_stats, h, s);
+  cudaFree(d_stats);
+  if (rc) return rc;
+  plan_finalize_width(p, h[0], h[1], h[2]);
+  int sgn = 0;
+  int P = width_for(p->min_val, p->max_val, &sgn);
+  p->is_signed = sgn;
+  rc = plan_alloc_planes(p, P);
+  if (rc) return rc;
+  int64_t tot2 = p->rows * p->ld;
+  if (tot2 > 0) {
+    k_encode_int64<<<grid_for(tot2), 256, 0, s>>>(mant, p->rows, p->n, ldm, planes_of(p), P,
+                                                   p->ld);
+    INVOP_CHECK_LAUNCH("encode");
+  }
+  return INVOP_OK;
+}
+
+int quantize_check(const double* e, int64_t rows, int64_t cols, int64_t ld, double p10,
+                   int64_t* bad_index, cudaStream_t s) {
+  int64_t total = rows * cols;
+  if (total == 0) return INVOP_OK;
+  unsigned long long* d = nullptr;
+  INVOP_CUDA(cudaMalloc(&d, 2 * sizeof(unsigned long long)));
+  unsigned long long init[2] = {0ull, ~0ull};
+  INVOP_CUDA(cudaMemcpyAsync(d, init, sizeof(init), cudaMemcpyHostToDevice, s));
+  k_quant_maxabs<<<grid_for(total), 256, 0, s>>>(e, rows, cols, ld, p10, d);
+  unsigned long long h[2];
+  INVOP_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, s));
+  INVOP_CUDA(cudaStreamSynchronize(s));
+  double worst; memcpy(&worst, &h[0], sizeof(double));
+  if (worst > 9007199254740992.0) {
+    k_quant_first_index<<<grid_for(total), 256, 0, s>>>(e, rows, cols, ld, p10, h[0], d + 1);
+    INVOP_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, s));
+    INVOP_CUDA(cudaStreamSynchronize(s));
+    cudaFree(d);
+    if (bad_index) *bad_index = (int64_t)h[1];
+    return fail(INVOP_E_OVERFLOW, "mantissa beyond 2^53");
+  }
+  cudaFree(d);
+  return INVOP_OK;
+}
+
+}  // namespace invop
+
+using namespace invop;
+
+// ------------------------------------------------------------------ C ABI
+extern "C" int invop_quantize(const double* entries, int64_t rows, int64_t cols, int64_t ld,
+                              int digits, int64_t* mant, int64_t ldm, int64_t* bad_index,
+                              void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (digits < 0 || digits > 12) return fail(INVOP_E_VALUE, "digits must be in 0..12");
+  if (rows < 0 || cols < 0 || ld < cols || ldm < cols)
+    return fail(INVOP_E_VALUE, "bad matrix geometry");
+  double p10 = invop_pow10_exact(digits);
+  int rc = quantize_check(entries, rows, cols, ld, p10, bad_index, s);
+  if (rc) return rc;
+  int64_t total = rows * cols;
+  if (total > 0) {
+    k_quant_write<<<grid_for(total), 256, 0, s>>>(entries, rows, cols, ld, p10, mant, ldm);
+    INVOP_CHECK_LAUNCH("quantize");
+  }
+  return INVOP_OK;
+}
+
+static invop_plan* new_plan(int64_t rows, int64_t n, int64_t row0, int digits) {
+  invop_plan* p = new invop_plan();
+  p->n = n; p->rows = rows; p->row0 = row0; p->digits = digits;
+  p->ld = round_up(n > 0 ? n : 1, 512);
+  // 10.0 ** -digits as CPython computes it (pow(10.0, -d), correctly rounded)
+  p->scale = 1.0 / invop_pow10_exact(digits);
+  cudaGetDevice(&p->device);
+  return p;
+}
+
+extern "C" int invop_plan_create(const int64_t* mant, int64_t rows, int64_t n, int64_t ldm,
+                                 int64_t row0, int scale_digits, void* stream,
+                                 invop_plan** out) {
+  if (!out) return fail(INVOP_E_VALUE, "out is NULL");
+  *out = nullptr;
+  if (scale_digits < 0) return fail(INVOP_E_VALUE, "scale_digits must be non-negative");
+  if (scale_digits > 22) return fail(INVOP_E_UNSUPPORTED, "scale_digits > 22");
+  if (n < 0 || rows < 0 || row0 < 0 || row0 + rows > n || ldm < n)
+    return fail(INVOP_E_VALUE, "bad plan geometry");
+  invop_plan* p = new_plan(rows, n, row0, scale_digits);
+  int rc = encode_int64(p, mant, ldm, (cudaStream_t)stream);
+  if (rc) { invop_plan_destroy(p); return rc; }
+  *out = p;
+  return INVOP_OK;
+}
+
+extern "C" int invop_plan_from_f64(const double* entries, int64_t rows, int64_t n, int64_t ld,
+                                   int64_t row0, int digits, int64_t* bad_index, void* stream,
+                                   invop_plan** out) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!out) return fail(INVOP_E_VALUE, "out is NULL");
+  *out = nullptr;
+  if (digits < 0 || digits > 12) return fail(INVOP_E_VALUE, "digits must be in 0..12");
+  if (n < 0 || rows < 0 || row0 < 0 || row0 + rows > n || ld < n)
+    return fail(INVOP_E_VALUE, "bad plan geometry");
+  double p10 = invop_pow10_exact(digits);
+  int rc = quantize_check(entries, rows, n, ld, p10, bad_index, s);
+  if (rc) return rc;
+  invop_plan* p = new_plan(rows, n, row0, digits);
+  long long* d_stats = nullptr;
+  if (cudaMalloc(&d_stats, 3 * sizeof(long long)) != cudaSuccess) {
+    invop_plan_destroy(p);
+    return fail(INVOP_E_CUDA, "cudaMalloc stats");
+  }
+  rc = init_stats(d_stats, s);
+  int64_t total = rows * n;
+  if (!rc && total > 0)
+    k_quant_stats<<<grid_for(total), 256, 0, s>>>(entries, rows, n, ld, p10, d_stats);
+  long long h[3] = {0, 0, 0};
+  if (!rc) rc = read_stats(d_stats, h, s);
+  cudaFree(d_stats);
+  if (rc) { invop_plan_destroy(p); return rc; }
+  plan_finalize_width(p, h[0], h[1], h[2]);
+  int sgn = 0;
+  int P = width_for(p->min_val, p->max_val, &sgn);
+  p->is_signed = sgn;
+  rc = plan_alloc_planes(p, P);
+  if (rc) { invop_plan_destroy(p); return rc; }
+  int64_t tot2 = rows * p->ld;
+  if (tot2 > 0)
+    k_quant_encode<<<grid_for(tot2), 256, 0, s>>>(entries, rows, n, ld, p10, planes_of(p), P,
+                                                   p->ld);
+  if (cudaGetLastError() != cudaSuccess) {
+    invop_plan_destroy(p);
+    return fail(INVOP_E_CUDA, "quantize-encode launch");
+  }
+  *out = p;
+  return INVOP_OK;
+}
+
+extern "C" int invop_plan_from_csc(int64_t n, int scale_digits, const int64_t* col_ptr,
+                                   const int64_t* group_abs_mantissa, const int64_t* group_ptr,
+                                   const int32_t* entry_rows, const int8_t* entry_signs,
+                                   int64_t groups, int64_t entries, void* stream,
+                                   invop_plan** out) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!out) return fail(INVOP_E_VALUE, "out is NULL");
+  *out = nullptr;
+  if (n < 0 || groups < 0 || entries < 0) return fail(INVOP_E_VALUE, "bad table sizes");
+  int64_t* mant = nullptr;
+  size_t bytes = (size_t)(n > 0 ? n : 1) * (size_t)(n > 0 ? n : 1) * sizeof(int64_t);
+  INVOP_CUDA(cudaMalloc(&mant, bytes));
+  INVOP_CUDA(cudaMemsetAsync(mant, 0, bytes, s));
+  if (n > 0 && groups > 0) {
+    int threads = 256;
+    int64_t blocks = cdiv(n * 32, threads);
+    k_from_csc<<<(unsigned)blocks, threads, 0, s>>>(n, col_ptr, group_abs_mantissa, group_ptr,
+                                                    entry_rows, entry_signs, mant);
+  }
+  int rc = invop_plan_create(mant, n, n, n, 0, scale_digits, stream, out);
+  cudaStreamSynchronize(s);
+  cudaFree(mant);
+  return rc;
+}
+
+extern "C" int invop_plan_decode(const invop_plan* p, int64_t* mant, int64_t ldm, void* stream) {
+  if (!p) return fail(INVOP_E_VALUE, "plan is NULL");
+  if (ldm < p->n) return fail(INVOP_E_VALUE, "ldm < n");
+  int64_t total = p->rows * p->n;
+  if (total == 0) return INVOP_OK;
+  k_decode<<<grid_for(total), 256, 0, (cudaStream_t)stream>>>(planes_of(p), p->P, p->is_signed,
+                                                              p->rows, p->n, p->ld, mant, ldm);
+  INVOP_CHECK_LAUNCH("decode");
+  return INVOP_OK;
+}
+
+static int column_stats(invop_plan* p, int64_t* distinct, int64_t* nonzero, cudaStream_t s) {
+  if (p->rows == 0 || p->n == 0) {
+    if (p->n > 0) {
+      INVOP_CUDA(cudaMemsetAsync(distinct, 0, p->n * sizeof(int64_t), s));
+      INVOP_CUDA(cudaMemsetAsync(nonzero, 0, p->n * sizeof(int64_t), s));
+    }
+    return INVOP_OK;
+  }
+  const int64_t smem_budget = 200 * 1024;
+  int64_t words = (int64_t)((uint64_t)p->max_abs / 32 + 1);
+  int64_t bytes_per_col = words * 4;
+  if (bytes_per_col <= smem_budget) {
+    int C = (int)std::min<int64_t>(64, smem_budget / bytes_per_col);
+    if (C < 1) C = 1;
+    size_t smem = (size_t)C * bytes_per_col;
+    cudaFuncSetAttribute(k_colstats_bitmap, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)std::max<size_t>(smem, 48 * 1024));
+    int64_t blocks = cdiv(p->n, C);
+    k_colstats_bitmap<<<(unsigned)blocks, 1024, smem, s>>>(planes_of(p), p->P, p->is_signed,
+                                                           p->rows, p->n, p->ld, C, words,
+                                                           distinct, nonzero);
+    INVOP_CHECK_LAUNCH("colstats_bitmap");
+    return INVOP_OK;
+  }
+  if (p->rows <= 16384) {
+    int npow2 = 1;
+    while (npow2 < p->rows) npow2 <<= 1;
+    size_t smem = (size_t)npow2 * (8 + 4 + 1);
+    cudaFuncSetAttribute(k_col_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)std::max<size_t>(smem, 48 * 1024));
+    k_col_sort<<<(unsigned)p->n, 1024, smem, s>>>(planes_of(p), p->P, p->is_signed, p->rows,
+                                                  p->n, p->ld, npow2, distinct, nonzero, 0,
+                                                  nullptr, nullptr, nullptr, nullptr, nullptr,
+                                                  nullptr, nullptr, p->scale);
+    INVOP_CHECK_LAUNCH("col_sort");
+    return INVOP_OK;
+  }
+  return fail(INVOP_E_CAPACITY,
+              "distinct-value statistics need max|mantissa| < 1.6e6 or at most 16384 rows");
+}
+
+extern "C" int invop_plan_column_stats(invop_plan* p, int64_t* distinct, int64_t* nonzero,
+                                       void* stream) {
+  if (!p) return fail(INVOP_E_VALUE, "plan is NULL");
+  return column_stats(p, distinct, nonzero, (cudaStream_t)stream);
+}
+
+extern "C" int invop_plan_counts(invop_plan* p, int64_t* mults, int64_t* adds, void* stream) {
+  if (!p) return fail(INVOP_E_VALUE, "plan is NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (p->mults < 0) {
+    if (p->n == 0 || p->rows == 0) {
+      p->mults = 0;
+    } else {
+      int64_t *d = nullptr;
+      INVOP_CUDA(cudaMalloc(&d, 2 * p->n * sizeof(int64_t)));
+      int rc = column_stats(p, d, d + p->n, s);
+      if (rc) { cudaFree(d); return rc; }
+      std::vector<int64_t> h(p->n);
+      INVOP_CUDA(cudaMemcpyAsync(h.data(), d, p->n * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      INVOP_CUDA(cudaStreamSynchronize(s));
+      cudaFree(d);
+      int64_t g = 0;
+      for (int64_t v : h) g += v;
+      p->mults = g;
+    }
+  }
+  if (mults) *mults = p->mults;
+  if (adds) *adds = p->nnz;
+  return INVOP_OK;
+}
+
+extern "C" int invop_plan_csc(invop_plan* p, int64_t* col_ptr, int64_t* group_abs_mantissa,
+                              double* group_coeff, int64_t* group_ptr, int32_t* entry_rows,
+                              int8_t* entry_signs, int64_t* groups, int64_t* entries,
+                              void* stream) {
+  if (!p) return fail(INVOP_E_VALUE, "plan is NULL");
+  if (p->rows != p->n || p->row0 != 0)
+    return fail(INVOP_E_VALUE, "CSC tables need the whole operator (not a row shard)");
+  if (p->n > 16384)
+    return fail(INVOP_E_CAPACITY, "CSC tables are only materialised for n <= 16384");
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t n = p->n;
+  if (n == 0) {
+    if (groups) *groups = 0;
+    if (entries) *entries = 0;
+    if (col_ptr) INVOP_CUDA(cudaMemsetAsync(col_ptr, 0, sizeof(int64_t), s));
+    if (group_ptr) INVOP_CUDA(cudaMemsetAsync(group_ptr, 0, sizeof(int64_t), s));
+    return INVOP_OK;
+  }
+  // pass 1: per-column counts (sort path gives both)
+  int npow2 = 1;
+  while (npow2 < p->rows) npow2 <<= 1;
+  size_t smem = (size_t)npow2 * (8 + 4 + 1);
+  cudaFuncSetAttribute(k_col_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)std::max<size_t>(smem, 48 * 1024));
+  int64_t* d = nullptr;
+  INVOP_CUDA(cudaMalloc(&d, 4 * n * sizeof(int64_t)));
+  int64_t *d_dist = d, *d_nz = d + n, *d_goff = d + 2 * n, *d_eoff = d + 3 * n;
+  k_col_sort<<<(unsigned)n, 1024, smem, s>>>(planes_of(p), p->P, p->is_signed, p->rows, n,
+                                             p->ld, npow2, d_dist, d_nz, 0, nullptr, nullptr,
+                                             nullptr, nullptr, nullptr, nullptr, nullptr,
+                                             p->scale);
+  std::vector<int64_t> hd(n), hn(n), goff(n + 1), eoff(n + 1);
+  INVOP_CUDA(cudaMemcpyAsync(hd.data(), d_dist, n * 8, cudaMemcpyDeviceToHost, s));
+  INVOP_CUDA(cudaMemcpyAsync(hn.data(), d_nz, n * 8, cudaMemcpyDeviceToHost, s));
+  INVOP_CUDA(cudaStreamSynchronize(s));
+  goff[0] = 0; eoff[0] = 0;
+  for (int64_t j = 0; j < n; ++j) { goff[j + 1] = goff[j] + hd[j]; eoff[j + 1] = eoff[j] + hn[j]; }
+  if (groups) *groups = goff[n];
+  if (entries) *entries = eoff[n];
+  p->mults = goff[n];
+  if (!col_ptr) { cudaFree(d); return INVOP_OK; }
+  INVOP_CUDA(cudaMemcpyAsync(col_ptr, goff.data(), (n + 1) * 8, cudaMemcpyHostToDevice, s));
+  INVOP_CUDA(cudaMemcpyAsync(d_goff, goff.data(), n * 8, cudaMemcpyHostToDevice, s));
+  INVOP_CUDA(cudaMemcpyAsync(d_eoff, eoff.data(), n * 8, cudaMemcpyHostToDevice, s));
+  // group_ptr[G] = E
+  int64_t E = eoff[n];
+  INVOP_CUDA(cudaMemcpyAsync(group_ptr + goff[n], &E, 8, cudaMemcpyHostToDevice, s));
+  k_col_sort<<<(unsigned)n, 1024, smem, s>>>(planes_of(p), p->P, p->is_signed, p->rows, n,
+                                             p->ld, npow2, d_dist, d_nz, 1, d_goff, d_eoff,
+                                             group_abs_mantissa, group_coeff, group_ptr,
+                                             entry_rows, entry_signs, p->scale);
+  cudaError_t e = cudaStreamSynchronize(s);
+  cudaFree(d);
+  if (e != cudaSuccess) return cuda_fail(e, "csc tables");
+  return INVOP_OK;
+}

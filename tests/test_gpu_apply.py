@@ -1,0 +1,307 @@
+"""GPU parity: device quantize / plan / apply through the C ABI against the
+golden vectors of the reference and the CPU oracle.
+
+Bars: integer outputs (mantissas, counts, tables) bit-exact; the fp64
+ordered apply bitwise equal to the reference; the fp32 apply within
+max relative error 1e-5 of the fp64 reference (BASELINE.json north_star).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import battery_cases, random_quantized_mant
+
+pytestmark = pytest.mark.gpu
+
+F32_TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def invop():
+    import torch
+
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_1602_00001_b200 as m
+
+    return m
+
+
+@pytest.fixture(scope="module")
+def O():
+    from oracle import invop_oracle
+
+    return invop_oracle
+
+
+def qm(invop, mant, m):
+    mant = np.asarray(mant, dtype=np.int64)
+    return invop.QuantizedMatrix(n=mant.shape[0], scale_digits=m, mantissas=mant)
+
+
+def relerr(y, r):
+    r = np.asarray(r, dtype=np.float64)
+    den = np.abs(r).max()
+    return float(np.abs(np.asarray(y, np.float64) - r).max() / (den if den else 1.0))
+
+
+# ------------------------------------------------------------------ reference known answers
+def test_plan_identity(invop):
+    q = invop.quantize(invop.DenseMatrix(n=4, entries=np.eye(4)), 2)
+    plan = invop.build_plan(q)
+    assert plan.planned_multiplications == 4
+    assert plan.planned_additions == 4
+    assert (plan.group_abs_mantissa == 100).all()
+    x = np.array([3.5, -1.0, 0.0, 2.0])
+    y, c = invop.apply(plan, x)
+    assert (y == x).all()
+    assert c.as_tuple() == (4, 4)
+
+
+def test_plan_shares_equal_magnitudes(invop):
+    mant = np.zeros((4, 4), dtype=np.int64)
+    mant[:, 0] = [25, 25, -25, 0]
+    plan = invop.build_plan(qm(invop, mant, 2))
+    assert plan.planned_multiplications == 1
+    assert plan.planned_additions == 3
+    assert list(plan.group_abs_mantissa) == [25]
+    assert list(plan.entry_rows) == [0, 1, 2]
+    assert list(plan.entry_signs) == [1, 1, -1]
+    y, c = invop.apply(plan, [1.0, 0.0, 0.0, 0.0])
+    assert list(y) == [0.25, 0.25, -0.25, 0.0]
+    assert c.as_tuple() == (1, 3)
+
+
+def test_zero_matrix_plan(invop):
+    plan = invop.build_plan(qm(invop, np.zeros((3, 3)), 1))
+    y, c = invop.apply(plan, np.ones(3))
+    assert (y == 0.0).all()
+    assert c.as_tuple() == (0, 0)
+    y32, _ = invop.apply(plan, np.ones(3), precision="f32")
+    assert (y32 == 0.0).all()
+
+
+def test_groups_ordered_ascending_magnitude(invop):
+    mant = np.zeros((3, 3), dtype=np.int64)
+    mant[:, 1] = [30, -7, 7]
+    plan = invop.build_plan(qm(invop, mant, 1))
+    assert list(plan.group_abs_mantissa) == [7, 30]
+    assert list(plan.entry_rows) == [1, 2, 0]
+
+
+def test_naive_hand_example(invop):
+    q = qm(invop, [[10, -5], [0, 20]], 1)
+    y, c = invop.apply_naive_quantized(q, [2.0, 4.0])
+    assert list(y) == [0.0, 8.0]
+    assert c.as_tuple() == (3, 3)
+
+
+def test_apply_length_mismatch(invop):
+    plan = invop.build_plan(qm(invop, np.zeros((3, 3)), 1))
+    with pytest.raises(ValueError):
+        invop.apply(plan, np.ones(4))
+    with pytest.raises(ValueError):
+        invop.apply_naive_quantized(qm(invop, np.zeros((3, 3)), 1), np.ones(2))
+
+
+def test_plan_validation_rejects_bad_tables(invop):
+    with pytest.raises(ValueError):
+        invop.ApplyPlan(n=2, scale_digits=1, col_ptr=np.array([0, 1, 1]),
+                        group_abs_mantissa=np.array([-5]), group_coeff=np.array([0.5]),
+                        group_ptr=np.array([0, 1]), entry_rows=np.array([0], dtype=np.int32),
+                        entry_signs=np.array([1], dtype=np.int8))
+    with pytest.raises(ValueError):
+        invop.ApplyPlan(n=2, scale_digits=1, col_ptr=np.array([0, 2]),
+                        group_abs_mantissa=np.array([5]), group_coeff=np.array([0.5]),
+                        group_ptr=np.array([0, 1]), entry_rows=np.array([0], dtype=np.int32),
+                        entry_signs=np.array([1], dtype=np.int8))
+
+
+def test_plan_from_tables_roundtrip(invop, golden):
+    g = golden("grid_cases")
+    for m in (1, 2, 3, 5):
+        tabs = {k: g["g5_m%d_%s" % (m, k)] for k in ("col_ptr", "group_abs_mantissa", "group_coeff",
+                                                       "group_ptr", "entry_rows", "entry_signs")}
+        plan = invop.ApplyPlan(n=25, scale_digits=m, **tabs)
+        y, c = invop.apply(plan, g["g5_rhs"])
+        assert y.tobytes() == g["g5_m%d_y" % m].tobytes()
+        assert c.as_tuple() == tuple(g["g5_m%d_counts" % m])
+
+
+# ------------------------------------------------------------------ golden batteries
+@pytest.mark.parametrize("name", ["battery_2024", "battery_7"])
+def test_ordered_apply_bitwise_battery(invop, golden, name):
+    for n, m, mant, x, y_ref, counts in battery_cases(golden(name)):
+        plan = invop.build_plan(qm(invop, mant, m))
+        y, c = invop.apply(plan, x)
+        assert y.tobytes() == y_ref.tobytes(), (n, m)
+        assert c.as_tuple() == counts
+        yn, cn = invop.apply_naive_quantized(qm(invop, mant, m), x)
+        assert yn.tobytes() == y_ref.tobytes()
+        assert cn.as_tuple() == (counts[1], counts[1])
+
+
+@pytest.mark.parametrize("name", ["battery_2024", "battery_7"])
+def test_fast_apply_tolerance_battery(invop, golden, name):
+    for n, m, mant, x, y_ref, counts in battery_cases(golden(name)):
+        plan = invop.build_plan(qm(invop, mant, m))
+        y, _ = invop.apply(plan, x, precision="f32")
+        assert relerr(y, y_ref) <= F32_TOL, (n, m)
+
+
+def test_grid_plans_match_reference(invop, golden):
+    g = golden("grid_cases")
+    for side in (5, 11):
+        inv = invop.DenseMatrix(n=side * side, entries=g["g%d_inverse" % side])
+        for m in (1, 2, 3, 5):
+            q = invop.quantize(inv, m)
+            assert (q.mantissas == g["g%d_m%d_mant" % (side, m)]).all()
+            plan = invop.build_plan(q)
+            y, c = invop.apply(plan, g["g%d_rhs" % side])
+            assert y.tobytes() == g["g%d_m%d_y" % (side, m)].tobytes()
+            assert c.as_tuple() == tuple(g["g%d_m%d_counts" % (side, m)])
+            nz, distinct = invop.sparsity_stats(q)
+            assert distinct == list(g["g%d_m%d_distinct" % (side, m)])
+            if side == 5:
+                for k in ("col_ptr", "group_abs_mantissa", "group_coeff", "group_ptr",
+                          "entry_rows", "entry_signs"):
+                    assert np.array_equal(getattr(plan, k), g["g5_m%d_%s" % (m, k)]), k
+
+
+def test_config1_bitwise(invop, golden):
+    g = golden("config1")
+    q = invop.quantize(invop.DenseMatrix(n=100, entries=g["inverse"]), 3)
+    assert (q.mantissas == g["mant"]).all()
+    plan = invop.build_plan(q)
+    y, c = invop.apply(plan, g["x"])
+    assert y.tobytes() == g["y"].tobytes()
+    assert c.as_tuple() == tuple(g["counts"])
+
+
+# ------------------------------------------------------------------ quantize edge cases
+def test_quantize_rounding_cases(invop, golden):
+    g = golden("quant_cases")
+    for m in range(7):
+        for v, want in zip(g["vals"], g["m%d" % m]):
+            q = invop.quantize(invop.DenseMatrix(n=1, entries=np.array([[v]])), m)
+            assert q.mantissas[0, 0] == want, (v, m)
+    for m in (0, 3, 6, 12):
+        q = invop.quantize(invop.DenseMatrix(n=8, entries=g["rand8"]), m)
+        assert (q.mantissas == g["rand8_m%d" % m]).all()
+
+
+def test_quantize_overflow_names_entry(invop):
+    big = invop.DenseMatrix(n=2, entries=np.array([[1.0, 1e300], [0.0, 1.0]]))
+    with pytest.raises(invop.MantissaOverflowError) as exc:
+        invop.quantize(big, 2)
+    assert "(0, 1)" in str(exc.value)
+    with pytest.raises(ValueError):
+        invop.quantize(big, 13)
+
+
+def test_quantize_dequantize_fixed_point(invop):
+    rng = np.random.default_rng(3)
+    for m in range(0, 5):
+        mant = rng.integers(-10 ** 9, 10 ** 9, size=(6, 6))
+        q = invop.QuantizedMatrix(n=6, scale_digits=m, mantissas=mant)
+        q2 = invop.quantize(invop.dequantize(q), m)
+        assert (q2.mantissas == q.mantissas).all()
+
+
+# ------------------------------------------------------------------ code widths / signs
+@pytest.mark.parametrize("lo,hi", [(0, 200), (-100, 100), (0, 60000), (-30000, 30000),
+                                   (0, 9_000_000), (-4_000_000, 4_000_000),
+                                   (0, 2_000_000_000), (-2_000_000_000, 2_000_000_000),
+                                   (-(2 ** 50), 2 ** 50)])
+def test_code_widths(invop, O, lo, hi):
+    rng = np.random.default_rng(abs(lo) + hi)
+    for n in (1, 7, 33, 130, 700):
+        mant = rng.integers(lo, hi + 1, size=(n, n))
+        mant[rng.random((n, n)) < 0.2] = 0
+        m = 3
+        plan = invop.build_plan(qm(invop, mant, m))
+        x = rng.standard_normal(n)
+        y, c = invop.apply(plan, x)
+        yo = O.ordered_apply(mant, m, x)
+        assert y.tobytes() == yo.tobytes()
+        nz, distinct = O.sparsity_stats(mant)
+        assert c.as_tuple() == (sum(distinct), nz)
+        if plan.device_plan.code_bytes <= 4:
+            y32, _ = invop.apply(plan, x, precision="f32")
+            # fp32 holds mantissas exactly only below 2^24
+            tol = F32_TOL if max(abs(lo), hi) < 2 ** 24 else 1e-4
+            assert relerr(y32, yo) <= tol
+
+
+def test_nonfinite_x_skips_zero_mantissas(invop, O):
+    mant = np.array([[5, 0, 3], [0, 0, 2], [1, 0, 0]], dtype=np.int64)
+    plan = invop.build_plan(qm(invop, mant, 1))
+    for bad in (np.inf, -np.inf, np.nan):
+        x = np.array([1.0, bad, 2.0])
+        y, _ = invop.apply(plan, x)
+        yo = O.ordered_apply(mant, 1, x)
+        assert np.array_equal(y, yo, equal_nan=True)
+        assert np.isfinite(y).all()
+        y32, _ = invop.apply(plan, x, precision="f32")
+        assert np.isfinite(y32).all()
+        assert relerr(y32, yo) <= F32_TOL
+
+
+def test_device_tensor_roundtrip(invop, O):
+    import torch
+
+    rng = np.random.default_rng(11)
+    mant = rng.integers(0, 40000, size=(1000, 1000))
+    plan = invop.build_plan(qm(invop, mant, 4))
+    x = rng.standard_normal(1000)
+    y, _ = invop.apply(plan, torch.tensor(x, device="cuda"))
+    assert y.is_cuda and y.dtype == torch.float64
+    assert y.cpu().numpy().tobytes() == O.ordered_apply(mant, 4, x).tobytes()
+    X = rng.standard_normal((7, 1000))
+    Y, _ = invop.apply_many(plan, torch.tensor(X, device="cuda", dtype=torch.float32))
+    Yo = O.ordered_apply(mant, 4, X)
+    for t in range(7):
+        assert relerr(Y[t].cpu().numpy(), Yo[t]) <= F32_TOL
+    Y64, _ = invop.apply_many(plan, X, precision="f64")
+    assert Y64.tobytes() == Yo.tobytes()
+
+
+# ------------------------------------------------------------------ dense path
+def test_invert_and_dense_apply(invop, O, golden):
+    g = golden("grid_cases")
+    inv = invop.invert(invop.DenseMatrix(n=4, entries=np.eye(4)))
+    assert (inv.entries == np.eye(4)).all()
+    inv = invop.invert(invop.DenseMatrix(n=2, entries=np.diag([2.0, 4.0])))
+    assert (inv.entries == np.diag([0.5, 0.25])).all()
+    with pytest.raises(invop.SingularMatrixError):
+        invop.invert(invop.DenseMatrix(n=3, entries=np.zeros((3, 3))))
+    with pytest.raises(invop.SingularMatrixError):
+        invop.invert(invop.DenseMatrix(n=2, entries=np.ones((2, 2))))
+    for side in (5, 11):
+        grid = invop.Grid2D(side, side)
+        op = invop.build_uniform(grid)
+        ainv = invop.invert(op)   # stencil path (block LU on device)
+        assert np.abs(ainv.entries - g["g%d_inverse" % side]).max() <= 1e-13
+        assert invop.residual_check(op, ainv) <= 1e-12
+        dense_generic = invop.invert(invop.DenseMatrix(n=op.n, entries=op.entries))
+        assert np.abs(dense_generic.entries - g["g%d_inverse" % side]).max() <= 1e-12
+        y, c = invop.apply_dense(invop.DenseMatrix(n=op.n, entries=g["g%d_inverse" % side]),
+                                 g["g%d_rhs" % side])
+        assert y.tobytes() == g["g%d_dense_y" % side].tobytes()
+        assert c.as_tuple() == (op.n ** 2, op.n * (op.n - 1))
+    opv = invop.build_variable(invop.Grid2D(6, 5), invop.CoefficientField(g["var_beta"]))
+    assert np.array_equal(opv.entries, g["var_entries"])
+    assert np.abs(invop.invert(opv).entries - g["var_inverse"]).max() <= 1e-13
+
+
+def test_construct_matches_scipy(invop, O):
+    for st in (invop.uniform_interior(13), invop.uniform_interior(7, 11),
+               invop.variable_interior(24, seed=3)):
+        dop = invop.DeviceOperator(st).factor()
+        rows = np.array([0, 1, st.n // 2, st.n - 1])
+        ref = O.inverse_rows(st, rows)
+        got = dop.inverse_rows().cpu().numpy()[rows]
+        assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+        q = dop.quantized_rows(4)
+        full = dop.inverse_rows().cpu().numpy()
+        want = O.quantize(full, 4)
+        assert (q.decode().cpu().numpy() == want).all()
