@@ -47,6 +47,8 @@ def to_device(arr, dtype) -> "torch.Tensor":
     np_dtype = {t.float64: np.float64, t.float32: np.float32, t.int64: np.int64,
                 t.int32: np.int32, t.int8: np.int8}[dtype]
     a = np.ascontiguousarray(arr, dtype=np_dtype)
+    if not a.flags.writeable:
+        a = a.copy()
     return t.from_numpy(a).to("cuda", non_blocking=False)
 
 
