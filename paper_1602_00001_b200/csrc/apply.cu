@@ -26,8 +26,14 @@
 //    is conflict-free LDS.128.
 #include "common.cuh"
 #include <algorithm>
+#include <cstdlib>
 
 namespace invop {
+
+static bool getenv_flag(const char* name) {
+  const char* v = std::getenv(name);
+  return v && *v && *v != '0';
+}
 
 // ------------------------------------------------------------------ helpers
 __device__ __forceinline__ uint4 ldg_stream(const uint8_t* p) {
@@ -239,10 +245,238 @@ static int launch_fast_p(FastArgs a, int KR, int grid, cudaStream_t s) {
 static int fast_R(int P, int KR) { return KR == 1 ? (P <= 2 ? 4 : 2) : 2; }
 static int fast_SW(int KR) { return KR == 1 ? 2 : 1; }
 
+// ------------------------------------------------------------- k2_stream
+// Single-RHS fp32 apply for long rows (>= 16 column steps of 512). Same math
+// as k2_fast, but the operator rows are streamed HBM -> shared memory by the
+// bulk-copy (TMA) engine through a ring of mbarrier-guarded stages filled by
+// one producer thread, so memory-level parallelism no longer costs consumer
+// registers: each stage is one row x one x-slab x P planes (up to 48 KB) and
+// ~4 stages are in flight per SM.
+constexpr int ST_CONSUMERS = 16;     // consumer warps (one column piece each)
+constexpr int ST_SW = 2;             // 512-column steps per consumer warp per slab
+constexpr int ST_SLAB = ST_CONSUMERS * ST_SW * 512;   // 16384 columns
+
+struct StreamArgs {
+  const uint8_t* planes[4];
+  int64_t rows, n, ld;
+  float scale;
+  const float* x;
+  float* y;
+  int nslabs;
+  int stages;
+  int stage_bytes;     // P * ST_SLAB
+  int slot_rows;
+};
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint32_t bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar), "l"(policy)
+      : "memory");
+}
+
+template <int P, bool SIGNED>
+__global__ void __launch_bounds__((ST_CONSUMERS + 1) * 32, 1) k2_stream(StreamArgs a) {
+  constexpr bool TWO = (P >= 3);
+  extern __shared__ __align__(128) unsigned char smem[];
+  // layout: [stages][P][ST_SLAB] codes | full[stages] | empty[stages] | slot
+  const int S = a.stages;
+  unsigned char* ring = smem;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)S * a.stage_bytes);
+  float* slot = reinterpret_cast<float*>(bars + 2 * S);   // [slot_rows][ST_CONSUMERS]
+  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
+  const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(bars);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  const int64_t row_lo = (int64_t)blockIdx.x * a.rows / gridDim.x;
+  const int64_t row_hi = (int64_t)(blockIdx.x + 1) * a.rows / gridDim.x;
+  const int64_t nrows = row_hi - row_lo;
+  const int64_t units = nrows * a.nslabs;       // slab-major: u = slab*nrows + r
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(bar_s + 8 * i, 1);                       // full: producer arrive + tx
+      mbar_init(bar_s + 8 * (S + i), ST_CONSUMERS);      // empty: one arrive per consumer
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == ST_CONSUMERS) {
+    // ---------------------------------------------------------- producer
+    if (lane == 0) {
+      uint64_t policy;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+      for (int64_t u = 0; u < units; ++u) {
+        const int st = (int)(u % S);
+        const uint32_t ph = (uint32_t)((u / S) & 1);
+        if (u >= S) mbar_wait(bar_s + 8 * (S + st), ph ^ 1);
+        const int slab = (int)(u / nrows);
+        const int64_t r = row_lo + (u - (int64_t)slab * nrows);
+        const int64_t c0 = (int64_t)slab * ST_SLAB;
+        const uint32_t bytes = (uint32_t)min((int64_t)ST_SLAB, a.ld - c0);
+        mbar_expect_tx(bar_s + 8 * st, bytes * P);
+#pragma unroll
+        for (int b = 0; b < P; ++b)
+          bulk_g2s(ring_s + st * a.stage_bytes + b * ST_SLAB, a.planes[b] + r * a.ld + c0,
+                   bytes, bar_s + 8 * st, policy);
+      }
+    }
+  } else {
+    // ---------------------------------------------------------- consumers
+    const int wc = warp;
+    float xr[ST_SW][16];
+    bool stepv[ST_SW];
+    bool masked = false;
+    int cur_slab = -1;
+    for (int64_t u = 0; u < units; ++u) {
+      const int st = (int)(u % S);
+      const uint32_t ph = (uint32_t)((u / S) & 1);
+      const int slab = (int)(u / nrows);
+      const int64_t lr = u - (int64_t)slab * nrows;
+      if (slab != cur_slab) {
+        cur_slab = slab;
+        bool finite = true;
+#pragma unroll
+        for (int t = 0; t < ST_SW; ++t) {
+          int64_t col = (int64_t)slab * ST_SLAB + (int64_t)(wc + t * ST_CONSUMERS) * 512;
+          stepv[t] = col < a.n;
+          int64_t c0 = col + lane * 16;
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            float v = (stepv[t] && c0 + q < a.n) ? a.x[c0 + q] : 0.0f;
+            finite = finite && isfinite(v);
+            xr[t][q] = v;
+          }
+        }
+        masked = __any_sync(0xffffffffu, !finite);
+      }
+      mbar_wait(bar_s + 8 * st, ph);
+      const unsigned char* sb = ring + (size_t)st * a.stage_bytes;
+      float acc = 0.0f, acch = 0.0f;
+#pragma unroll
+      for (int t = 0; t < ST_SW; ++t) {
+        if (!stepv[t]) continue;   // warp-uniform
+        const int off = (wc + t * ST_CONSUMERS) * 512 + lane * 16;
+        uint4 cw[P];
+#pragma unroll
+        for (int b = 0; b < P; ++b) cw[b] = *reinterpret_cast<const uint4*>(sb + b * ST_SLAB + off);
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          float fl[4], fh[4];
+          if (P == 1) {
+            dec8<SIGNED>(u4get(cw[0], w), fl);
+          } else if (P == 2) {
+            dec16<SIGNED>(u4get(cw[0], w), u4get(cw[P > 1 ? 1 : 0], w), fl);
+          } else {
+            dec16<false>(u4get(cw[0], w), u4get(cw[P > 1 ? 1 : 0], w), fl);
+            if (P == 3) dec8<SIGNED>(u4get(cw[P > 2 ? 2 : 0], w), fh);
+            else dec16<SIGNED>(u4get(cw[P > 2 ? 2 : 0], w), u4get(cw[P > 3 ? 3 : 0], w), fh);
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            float xv = xr[t][4 * w + i];
+            if (masked) {
+              bool nz = TWO ? (fl[i] != 0.0f || fh[i] != 0.0f) : (fl[i] != 0.0f);
+              if (!nz) xv = 0.0f;
+              if (!nz) continue;
+            }
+            acc = fmaf(fl[i], xv, acc);
+            if (TWO) acch = fmaf(fh[i], xv, acch);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_s + 8 * (S + st));   // stage consumed by this warp
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (TWO) acch += __shfl_xor_sync(0xffffffffu, acch, o);
+      }
+      if (TWO) acc = fmaf(acch, 65536.0f, acc);
+      if (lane == 0) {
+        float* sp = &slot[lr * ST_CONSUMERS + wc];
+        *sp = (slab == 0) ? acc : (*sp + acc);
+      }
+    }
+  }
+  __syncthreads();
+  for (int64_t r = threadIdx.x; r < nrows; r += blockDim.x) {
+    float s = 0.0f;
+#pragma unroll
+    for (int c = 0; c < ST_CONSUMERS; ++c) s += slot[r * ST_CONSUMERS + c];
+    a.y[row_lo + r] = s * a.scale;
+  }
+}
+
+template <int P, bool SIGNED>
+static int launch_stream_p(const invop_plan* p, const float* x, float* y, cudaStream_t s) {
+  StreamArgs a;
+  for (int b = 0; b < 4; ++b) a.planes[b] = p->planes[b < p->P ? b : 0];
+  a.rows = p->rows; a.n = p->n; a.ld = p->ld;
+  a.scale = (float)p->scale;
+  a.x = x; a.y = y;
+  a.nslabs = (int)cdiv(p->ld, ST_SLAB);
+  a.stage_bytes = P * ST_SLAB;
+  int grid = (int)std::min<int64_t>(num_sms(), p->rows);
+  a.slot_rows = (int)cdiv(p->rows, grid);
+  size_t slot_bytes = (size_t)a.slot_rows * ST_CONSUMERS * sizeof(float);
+  const size_t budget = 225 * 1024;
+  int stages = (int)((budget - slot_bytes - 256) / (a.stage_bytes + 16));
+  stages = std::min(stages, 8);
+  if (stages < 2) return fail(INVOP_E_UNSUPPORTED, "k2_stream: not enough shared memory");
+  a.stages = stages;
+  size_t smem = (size_t)stages * a.stage_bytes + 2 * stages * 8 + slot_bytes;
+  auto kern = k2_stream<P, SIGNED>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  kern<<<grid, (ST_CONSUMERS + 1) * 32, smem, s>>>(a);
+  INVOP_CHECK_LAUNCH("k2_stream");
+  return INVOP_OK;
+}
+
+static int apply_stream(const invop_plan* p, const float* x, float* y, cudaStream_t s) {
+  switch (p->P * 2 + p->is_signed) {
+    case 2: return launch_stream_p<1, false>(p, x, y, s);
+    case 3: return launch_stream_p<1, true>(p, x, y, s);
+    case 4: return launch_stream_p<2, false>(p, x, y, s);
+    case 5: return launch_stream_p<2, true>(p, x, y, s);
+    case 6: return launch_stream_p<3, false>(p, x, y, s);
+    case 7: return launch_stream_p<3, true>(p, x, y, s);
+    case 8: return launch_stream_p<4, false>(p, x, y, s);
+    default: return launch_stream_p<4, true>(p, x, y, s);
+  }
+}
+
 int apply_fast_launch(const invop_plan* p, const float* x, int64_t ldx, float* y, int64_t ldy,
                       int64_t nrhs, cudaStream_t s) {
   if (p->P > 4) return fail(INVOP_E_UNSUPPORTED, "fast mode needs codes of at most 4 bytes");
   if (p->rows == 0 || nrhs == 0) return INVOP_OK;
+  // long rows, one right-hand side: stream rows through shared memory
+  if (nrhs == 1 && p->ld / 512 >= ST_CONSUMERS && !getenv_flag("INVOP_NO_STREAM")) {
+    int64_t rows_per_cta = cdiv(p->rows, std::min<int64_t>(num_sms(), p->rows));
+    if (rows_per_cta * ST_CONSUMERS * 4 <= 96 * 1024) return apply_stream(p, x, y, s);
+  }
   const int warps = 16;
   const int sms = num_sms();
   int Cp = (int)(p->ld / 512);
@@ -427,26 +661,35 @@ __global__ void __launch_bounds__(128) k2_ordered(OrdArgs a) {
       for (int b = 0; b < P; ++b)
         w[b] = *reinterpret_cast<const uint4*>(sb + b * CODE_BYTES + sr * 128 +
                                                ((c ^ (sr & 7)) << 4));
+      // all 16 products first (independent), then the ordered fp64 chain.
+      // For finite x, adding (0*10^-m)*x_j = +-0 leaves the accumulator
+      // bitwise unchanged (it starts at +0 and x+(-x) rounds to +0), so the
+      // reference's zero skip only matters when the tile holds inf/nan: then
+      // the product of a zero code is replaced by +0.
+      double d[16];
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
         uint8_t bytes[P];
 #pragma unroll
         for (int b = 0; b < P; ++b) bytes[b] = (uint8_t)(u4get(w[b], q >> 2) >> (8 * (q & 3)));
-        // For finite x, adding (0*10^-m)*x_j = +-0 leaves the accumulator
-        // bitwise unchanged (it starts at +0 and x+(-x) rounds to +0), so the
-        // reference's zero skip only matters when the tile holds inf/nan.
-        bool take = true;
+        d[q] = __dmul_rn(code_to_double<P, SIGNED>(bytes), a.scale);
+      }
+#pragma unroll
+      for (int k = 0; k < KR; ++k) {
+        const double2* xk = reinterpret_cast<const double2*>(xs + k * ORD_TILE + c * 16);
+        double t[16];
+#pragma unroll
+        for (int q2 = 0; q2 < 8; ++q2) {
+          double2 xv = xk[q2];
+          t[2 * q2] = __dmul_rn(d[2 * q2], xv.x);
+          t[2 * q2 + 1] = __dmul_rn(d[2 * q2 + 1], xv.y);
+        }
         if (masked) {
-          take = false;
 #pragma unroll
-          for (int b = 0; b < P; ++b) take |= bytes[b] != 0;
+          for (int q = 0; q < 16; ++q) t[q] = d[q] != 0.0 ? t[q] : 0.0;
         }
-        if (take) {
-          const double d = __dmul_rn(code_to_double<P, SIGNED>(bytes), a.scale);
 #pragma unroll
-          for (int k = 0; k < KR; ++k)
-            acc[k] = __dadd_rn(acc[k], __dmul_rn(d, xs[k * ORD_TILE + c * 16 + q]));
-        }
+        for (int q = 0; q < 16; ++q) acc[k] = __dadd_rn(acc[k], t[q]);
       }
     }
     __syncwarp();
@@ -462,7 +705,9 @@ template <int P, bool SIGNED, int KR>
 static int launch_ord_t(OrdArgs a, cudaStream_t s) {
   constexpr int STAGE_BYTES = 32 * ORD_TILE * P + ORD_TILE * 8 * KR;
   size_t per_warp = (size_t)STAGE_BYTES * ORD_STAGES;
-  int wpb = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / per_warp));
+  // 2 warps (64 rows) per block: small blocks pack 2-3 per SM so all row
+  // warps of a 16K-row operator are resident in a single wave
+  int wpb = (int)std::max<size_t>(1, std::min<size_t>(2, (200 * 1024) / per_warp));
   size_t smem = per_warp * wpb;
   auto kern = k2_ordered<P, SIGNED, KR>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -305,3 +305,64 @@ def test_construct_matches_scipy(invop, O):
         full = dop.inverse_rows().cpu().numpy()
         want = O.quantize(full, 4)
         assert (q.decode().cpu().numpy() == want).all()
+
+
+# ------------------------------------------------------------------ full-size configs
+def _config_parity(invop, O, key, sample=24, seed=0):
+    """Full-size config: device construction (K4+K1) vs the oracle's sparse-LU
+    rows; apply parity on the device's own codes for sampled rows."""
+    import torch
+    from paper_1602_00001_b200 import configs
+
+    cfg = configs.get(key)
+    st = cfg.operator()
+    N = st.n
+    dplan = invop.DeviceOperator(st).factor().quantized_rows(cfg.digits)
+    rng = np.random.default_rng(seed)
+    rows = np.unique(np.concatenate([[0, N // 2 + st.nx // 2, N - 1], rng.choice(N, sample, replace=False)]))
+    # construction agreement: mantissas from the oracle's fp64 rows
+    ref_rows = O.inverse_rows(st, rows)
+    ref_mant = O.quantize(ref_rows, cfg.digits)
+    dev_mant = dplan.decode()[torch.as_tensor(rows, device="cuda")].cpu().numpy()
+    diff = np.abs(dev_mant - ref_mant)
+    assert diff.max() <= 1, "construction differs by more than one unit"
+    assert (diff != 0).mean() < 1e-4, "too many rounding-tie disagreements"
+    X = cfg.rhs()
+    plan = invop.ApplyPlan(n=N, scale_digits=cfg.digits, _dplan=dplan)
+    for t in range(min(X.shape[0], 4)):
+        x = X[t]
+        y64, _ = invop.apply(plan, x)
+        y32, _ = invop.apply(plan, x, precision="f32")
+        yo = O.ordered_apply(dev_mant, cfg.digits, x)        # identical codes -> bitwise
+        assert y64[rows].tobytes() == yo.tobytes()
+        assert O.relative_error(y32[rows], yo) <= F32_TOL
+        assert O.relative_error(y32, y64) <= F32_TOL
+    return dplan
+
+
+def test_config3_full_size(invop, O):
+    _config_parity(invop, O, 3)
+
+
+def test_config4_full_size(invop, O):
+    d = _config_parity(invop, O, 4)
+    assert d.code_bytes == 3
+
+
+def test_config2_against_reference_outputs(invop, O, golden):
+    g = golden("config2")
+    from paper_1602_00001_b200 import configs
+
+    cfg = configs.get(2)
+    dplan = invop.DeviceOperator(cfg.operator()).factor().quantized_rows(cfg.digits)
+    mant = dplan.decode().cpu().numpy()
+    # construction agreement with the reference's LU-based mantissas
+    assert mant.sum() == g["mant_sum"][0]
+    assert (mant[g["rows_sample"]] == g["mant_rows"]).all()
+    plan = invop.ApplyPlan(n=2500, scale_digits=4, _dplan=dplan)
+    assert (plan.planned_multiplications, plan.planned_additions) == tuple(g["counts"])
+    Y64, _ = invop.apply_many(plan, g["X"], precision="f64")
+    assert Y64.tobytes() == g["Y"].tobytes()      # bitwise = the reference's own apply
+    Y32, _ = invop.apply_many(plan, g["X"], precision="f32")
+    for t in range(16):
+        assert O.relative_error(Y32[t], g["Y"][t]) <= F32_TOL
