@@ -246,20 +246,31 @@ static int fast_R(int P, int KR) { return KR == 1 ? (P <= 2 ? 4 : 2) : 2; }
 static int fast_SW(int KR) { return KR == 1 ? 2 : 1; }
 
 // ------------------------------------------------------------- k2_stream
-// Single-RHS fp32 apply for long rows (>= 16 column steps of 512). Same math
-// as k2_fast, but the operator rows are streamed HBM -> shared memory by the
-// bulk-copy (TMA) engine through a ring of mbarrier-guarded stages filled by
-// one producer thread, so memory-level parallelism no longer costs consumer
-// registers: each stage is one row x one x-slab x P planes (up to 48 KB) and
-// ~4 stages are in flight per SM.
-constexpr int ST_CONSUMERS = 16;     // consumer warps (one column piece each)
-constexpr int ST_SW = 2;             // 512-column steps per consumer warp per slab
+// Single-RHS apply for long rows (>= 16 column steps of 512), fp32 in/out.
+//
+// Memory: operator rows are streamed HBM -> shared memory by the bulk-copy
+// (TMA) engine through a ring of mbarrier-guarded stages filled by one
+// producer thread (one row x one 16K-column slab x P planes per stage), so
+// memory-level parallelism costs no consumer registers.
+//
+// Arithmetic (the paper's "sum shared values, multiply once"): each consumer
+// warp owns a 2048-column piece of the slab; it converts its x values once to
+// 23-bit fixed point X = rint(x * 2^e) with a warp-wide exponent e, and sums
+// the integer mantissas exactly: acc += v * X with one IMAD.WIDE per code into
+// an int64 (|v| < 2^24, |X| < 2^23, <= 2^16 terms: no overflow). The exact
+// integer row sum is scaled once, y = 10^-m * 2^-e * acc. The only rounding
+// is x -> X (relative 2^-24 of the piece's max|x|) and the final scaling, so
+// the result is deterministic and independent of summation order.
+// A warp whose x piece holds inf/nan falls back to fp32 decoding with the
+// reference's zero-mantissa skip.
+constexpr int ST_CONSUMERS = 8;      // consumer warps (one column piece each)
+constexpr int ST_SW = 4;             // 512-column steps per consumer warp per slab
 constexpr int ST_SLAB = ST_CONSUMERS * ST_SW * 512;   // 16384 columns
 
 struct StreamArgs {
   const uint8_t* planes[4];
   int64_t rows, n, ld;
-  float scale;
+  double scale;
   const float* x;
   float* y;
   int nslabs;
@@ -296,6 +307,52 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
       : "memory");
 }
 
+// 4 integer mantissas from the P plane words (byte q of word b = byte b of
+// code q). SIGNED: two's complement, sign-extended with PRMT's replicate mode.
+template <int P, bool SIGNED>
+__device__ __forceinline__ void dec_int4(const uint32_t* wds, int32_t* u) {
+  if (P == 1) {
+    const uint32_t a = wds[0];
+    if (SIGNED) {
+      u[0] = (int32_t)__byte_perm(a, 0, 0x8880); u[1] = (int32_t)__byte_perm(a, 0, 0x9991);
+      u[2] = (int32_t)__byte_perm(a, 0, 0xAAA2); u[3] = (int32_t)__byte_perm(a, 0, 0xBBB3);
+    } else {
+      u[0] = (int32_t)__byte_perm(a, 0, 0x4440); u[1] = (int32_t)__byte_perm(a, 0, 0x4441);
+      u[2] = (int32_t)__byte_perm(a, 0, 0x4442); u[3] = (int32_t)__byte_perm(a, 0, 0x4443);
+    }
+  } else if (P == 2) {
+    const uint32_t t01 = __byte_perm(wds[0], wds[1], 0x5140);   // [a0 b0 a1 b1]
+    const uint32_t t23 = __byte_perm(wds[0], wds[1], 0x7362);   // [a2 b2 a3 b3]
+    if (SIGNED) {
+      u[0] = (int32_t)__byte_perm(t01, 0, 0x9910); u[1] = (int32_t)__byte_perm(t01, 0, 0xBB32);
+      u[2] = (int32_t)__byte_perm(t23, 0, 0x9910); u[3] = (int32_t)__byte_perm(t23, 0, 0xBB32);
+    } else {
+      u[0] = (int32_t)(t01 & 0xffffu); u[1] = (int32_t)(t01 >> 16);
+      u[2] = (int32_t)(t23 & 0xffffu); u[3] = (int32_t)(t23 >> 16);
+    }
+  } else {
+    const uint32_t t01 = __byte_perm(wds[0], wds[1], 0x5140);
+    const uint32_t t23 = __byte_perm(wds[0], wds[1], 0x7362);
+    const uint32_t c = wds[2];
+    if (P == 3) {
+      if (SIGNED) {
+        u[0] = (int32_t)__byte_perm(t01, c, 0xC410); u[1] = (int32_t)__byte_perm(t01, c, 0xD532);
+        u[2] = (int32_t)__byte_perm(t23, c, 0xE610); u[3] = (int32_t)__byte_perm(t23, c, 0xF732);
+      } else {
+        u[0] = (int32_t)(__byte_perm(t01, c, 0x0410) & 0xffffffu);
+        u[1] = (int32_t)(__byte_perm(t01, c, 0x0532) & 0xffffffu);
+        u[2] = (int32_t)(__byte_perm(t23, c, 0x0610) & 0xffffffu);
+        u[3] = (int32_t)(__byte_perm(t23, c, 0x0732) & 0xffffffu);
+      }
+    } else {
+      const uint32_t h01 = __byte_perm(wds[2], wds[3], 0x5140);
+      const uint32_t h23 = __byte_perm(wds[2], wds[3], 0x7362);
+      u[0] = (int32_t)__byte_perm(t01, h01, 0x5410); u[1] = (int32_t)__byte_perm(t01, h01, 0x7632);
+      u[2] = (int32_t)__byte_perm(t23, h23, 0x5410); u[3] = (int32_t)__byte_perm(t23, h23, 0x7632);
+    }
+  }
+}
+
 template <int P, bool SIGNED>
 __global__ void __launch_bounds__((ST_CONSUMERS + 1) * 32, 1) k2_stream(StreamArgs a) {
   constexpr bool TWO = (P >= 3);
@@ -304,7 +361,7 @@ __global__ void __launch_bounds__((ST_CONSUMERS + 1) * 32, 1) k2_stream(StreamAr
   const int S = a.stages;
   unsigned char* ring = smem;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)S * a.stage_bytes);
-  float* slot = reinterpret_cast<float*>(bars + 2 * S);   // [slot_rows][ST_CONSUMERS]
+  double* slot = reinterpret_cast<double*>(bars + 2 * S);   // [slot_rows][ST_CONSUMERS]
   const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
   const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(bars);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -346,9 +403,10 @@ __global__ void __launch_bounds__((ST_CONSUMERS + 1) * 32, 1) k2_stream(StreamAr
   } else {
     // ---------------------------------------------------------- consumers
     const int wc = warp;
-    float xr[ST_SW][16];
+    int32_t X[ST_SW][16];
     bool stepv[ST_SW];
     bool masked = false;
+    double inv2e = 1.0;
     int cur_slab = -1;
     for (int64_t u = 0; u < units; ++u) {
       const int st = (int)(u % S);
@@ -356,8 +414,10 @@ __global__ void __launch_bounds__((ST_CONSUMERS + 1) * 32, 1) k2_stream(StreamAr
       const int slab = (int)(u / nrows);
       const int64_t lr = u - (int64_t)slab * nrows;
       if (slab != cur_slab) {
+        // x piece of this warp -> registers; fixed-point exponent from its max
         cur_slab = slab;
         bool finite = true;
+        float mx = 0.0f;
 #pragma unroll
         for (int t = 0; t < ST_SW; ++t) {
           int64_t col = (int64_t)slab * ST_SLAB + (int64_t)(wc + t * ST_CONSUMERS) * 512;
@@ -367,66 +427,112 @@ __global__ void __launch_bounds__((ST_CONSUMERS + 1) * 32, 1) k2_stream(StreamAr
           for (int q = 0; q < 16; ++q) {
             float v = (stepv[t] && c0 + q < a.n) ? a.x[c0 + q] : 0.0f;
             finite = finite && isfinite(v);
-            xr[t][q] = v;
+            mx = fmaxf(mx, fabsf(v));
           }
         }
         masked = __any_sync(0xffffffffu, !finite);
-      }
-      mbar_wait(bar_s + 8 * st, ph);
-      const unsigned char* sb = ring + (size_t)st * a.stage_bytes;
-      float acc = 0.0f, acch = 0.0f;
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        int e = 0;
+        if (mx > 0.0f && !masked) {
+          int ex;
+          frexpf(mx, &ex);            // mx < 2^ex
+          e = 22 - ex;                // |x * 2^e| < 2^22 < 2^23
+        }
+        inv2e = ldexp(1.0, -e);
 #pragma unroll
-      for (int t = 0; t < ST_SW; ++t) {
-        if (!stepv[t]) continue;   // warp-uniform
-        const int off = (wc + t * ST_CONSUMERS) * 512 + lane * 16;
-        uint4 cw[P];
+        for (int t = 0; t < ST_SW; ++t) {
+          int64_t c0 = (int64_t)slab * ST_SLAB + (int64_t)(wc + t * ST_CONSUMERS) * 512 + lane * 16;
 #pragma unroll
-        for (int b = 0; b < P; ++b) cw[b] = *reinterpret_cast<const uint4*>(sb + b * ST_SLAB + off);
-#pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          float fl[4], fh[4];
-          if (P == 1) {
-            dec8<SIGNED>(u4get(cw[0], w), fl);
-          } else if (P == 2) {
-            dec16<SIGNED>(u4get(cw[0], w), u4get(cw[P > 1 ? 1 : 0], w), fl);
-          } else {
-            dec16<false>(u4get(cw[0], w), u4get(cw[P > 1 ? 1 : 0], w), fl);
-            if (P == 3) dec8<SIGNED>(u4get(cw[P > 2 ? 2 : 0], w), fh);
-            else dec16<SIGNED>(u4get(cw[P > 2 ? 2 : 0], w), u4get(cw[P > 3 ? 3 : 0], w), fh);
-          }
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            float xv = xr[t][4 * w + i];
-            if (masked) {
-              bool nz = TWO ? (fl[i] != 0.0f || fh[i] != 0.0f) : (fl[i] != 0.0f);
-              if (!nz) xv = 0.0f;
-              if (!nz) continue;
-            }
-            acc = fmaf(fl[i], xv, acc);
-            if (TWO) acch = fmaf(fh[i], xv, acch);
+          for (int q = 0; q < 16; ++q) {
+            float v = (stepv[t] && c0 + q < a.n) ? a.x[c0 + q] : 0.0f;
+            X[t][q] = masked ? 0 : __float2int_rn(ldexpf(v, e));
           }
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(bar_s + 8 * (S + st));   // stage consumed by this warp
+      mbar_wait(bar_s + 8 * st, ph);
+      const unsigned char* sb = ring + (size_t)st * a.stage_bytes;
+      double part;
+      if (!masked) {
+        long long acc = 0;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (TWO) acch += __shfl_xor_sync(0xffffffffu, acch, o);
+        for (int t = 0; t < ST_SW; ++t) {
+          if (!stepv[t]) continue;   // warp-uniform
+          const int off = (wc + t * ST_CONSUMERS) * 512 + lane * 16;
+          uint4 cw[P];
+#pragma unroll
+          for (int b = 0; b < P; ++b)
+            cw[b] = *reinterpret_cast<const uint4*>(sb + b * ST_SLAB + off);
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            uint32_t wds[P];
+#pragma unroll
+            for (int b = 0; b < P; ++b) wds[b] = u4get(cw[b], w);
+            int32_t uv[4];
+            dec_int4<P, SIGNED>(wds, uv);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc += (long long)uv[i] * X[t][4 * w + i];
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_s + 8 * (S + st));   // stage consumed by this warp
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        part = (double)acc * inv2e;
+      } else {
+        float acc = 0.0f, acch = 0.0f;
+#pragma unroll
+        for (int t = 0; t < ST_SW; ++t) {
+          if (!stepv[t]) continue;
+          const int off = (wc + t * ST_CONSUMERS) * 512 + lane * 16;
+          const int64_t gc = (int64_t)slab * ST_SLAB + off;
+          uint4 cw[P];
+#pragma unroll
+          for (int b = 0; b < P; ++b)
+            cw[b] = *reinterpret_cast<const uint4*>(sb + b * ST_SLAB + off);
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            float fl[4], fh[4];
+            if (P == 1) {
+              dec8<SIGNED>(u4get(cw[0], w), fl);
+            } else if (P == 2) {
+              dec16<SIGNED>(u4get(cw[0], w), u4get(cw[P > 1 ? 1 : 0], w), fl);
+            } else {
+              dec16<false>(u4get(cw[0], w), u4get(cw[P > 1 ? 1 : 0], w), fl);
+              if (P == 3) dec8<SIGNED>(u4get(cw[P > 2 ? 2 : 0], w), fh);
+              else dec16<SIGNED>(u4get(cw[P > 2 ? 2 : 0], w), u4get(cw[P > 3 ? 3 : 0], w), fh);
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const bool nz = TWO ? (fl[i] != 0.0f || fh[i] != 0.0f) : (fl[i] != 0.0f);
+              if (!nz) continue;     // reference skips zero mantissas (0*inf)
+              const int64_t col = gc + 4 * w + i;
+              const float xv = col < a.n ? a.x[col] : 0.0f;
+              acc = fmaf(fl[i], xv, acc);
+              if (TWO) acch = fmaf(fh[i], xv, acch);
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_s + 8 * (S + st));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          acc += __shfl_xor_sync(0xffffffffu, acc, o);
+          if (TWO) acch += __shfl_xor_sync(0xffffffffu, acch, o);
+        }
+        part = TWO ? (double)acc + 65536.0 * (double)acch : (double)acc;
       }
-      if (TWO) acc = fmaf(acch, 65536.0f, acc);
       if (lane == 0) {
-        float* sp = &slot[lr * ST_CONSUMERS + wc];
-        *sp = (slab == 0) ? acc : (*sp + acc);
+        double* sp = &slot[lr * ST_CONSUMERS + wc];
+        *sp = (slab == 0) ? part : (*sp + part);
       }
     }
   }
   __syncthreads();
   for (int64_t r = threadIdx.x; r < nrows; r += blockDim.x) {
-    float s = 0.0f;
+    double s = 0.0;
 #pragma unroll
     for (int c = 0; c < ST_CONSUMERS; ++c) s += slot[r * ST_CONSUMERS + c];
-    a.y[row_lo + r] = s * a.scale;
+    a.y[row_lo + r] = (float)(s * a.scale);
   }
 }
 
@@ -435,13 +541,13 @@ static int launch_stream_p(const invop_plan* p, const float* x, float* y, cudaSt
   StreamArgs a;
   for (int b = 0; b < 4; ++b) a.planes[b] = p->planes[b < p->P ? b : 0];
   a.rows = p->rows; a.n = p->n; a.ld = p->ld;
-  a.scale = (float)p->scale;
+  a.scale = p->scale;
   a.x = x; a.y = y;
   a.nslabs = (int)cdiv(p->ld, ST_SLAB);
   a.stage_bytes = P * ST_SLAB;
   int grid = (int)std::min<int64_t>(num_sms(), p->rows);
   a.slot_rows = (int)cdiv(p->rows, grid);
-  size_t slot_bytes = (size_t)a.slot_rows * ST_CONSUMERS * sizeof(float);
+  size_t slot_bytes = (size_t)a.slot_rows * ST_CONSUMERS * sizeof(double);
   const size_t budget = 225 * 1024;
   int stages = (int)((budget - slot_bytes - 256) / (a.stage_bytes + 16));
   stages = std::min(stages, 8);
@@ -475,7 +581,7 @@ int apply_fast_launch(const invop_plan* p, const float* x, int64_t ldx, float* y
   // long rows, one right-hand side: stream rows through shared memory
   if (nrhs == 1 && p->ld / 512 >= ST_CONSUMERS && !getenv_flag("INVOP_NO_STREAM")) {
     int64_t rows_per_cta = cdiv(p->rows, std::min<int64_t>(num_sms(), p->rows));
-    if (rows_per_cta * ST_CONSUMERS * 4 <= 96 * 1024) return apply_stream(p, x, y, s);
+    if (rows_per_cta * ST_CONSUMERS * 8 <= 64 * 1024) return apply_stream(p, x, y, s);
   }
   const int warps = 16;
   const int sms = num_sms();

@@ -489,12 +489,12 @@ extern "C" int invop_construct_rows(invop_operator* op, int64_t row0, int64_t ro
   }
   plan_finalize_width(p, rows > 0 ? h[0] : 0, rows > 0 ? h[1] : 0, h[2]);
   // narrowest width; the low planes already hold the right bytes
-  int sgn = p->min_val < 0;
+  int sgn = 1;
   int P = 4;
   for (int q = 1; q <= 4; ++q) {
-    bool fits = sgn ? (p->min_val >= -(1ll << (8 * q - 1)) && p->max_val <= (1ll << (8 * q - 1)) - 1)
-                    : ((uint64_t)p->max_val < (1ull << (8 * q)));
-    if (fits) { P = q; break; }
+    int64_t lo = -(1ll << (8 * q - 1)), hi = (1ll << (8 * q - 1)) - 1;
+    if (p->min_val >= lo && p->max_val <= hi) { P = q; sgn = 1; break; }
+    if (p->min_val >= 0 && (uint64_t)p->max_val < (1ull << (8 * q))) { P = q; sgn = 0; break; }
   }
   for (int b = P; b < 4; ++b) { cudaFree(p->planes[b]); p->planes[b] = nullptr; }
   p->P = P;

@@ -352,15 +352,15 @@ int plan_alloc_planes(invop_plan* p, int P) {
 
 // choose the narrowest byte width for [mn, mx]
 static int width_for(int64_t mn, int64_t mx, int* is_signed) {
-  *is_signed = mn < 0;
+  // Two's complement whenever the range fits P signed bytes (decoders
+  // sign-extend with one PRMT); unsigned only when non-negative values need
+  // the extra top bit.
   for (int P = 1; P < 8; ++P) {
-    if (*is_signed) {
-      int64_t lo = -((int64_t)1 << (8 * P - 1)), hi = ((int64_t)1 << (8 * P - 1)) - 1;
-      if (mn >= lo && mx <= hi) return P;
-    } else {
-      if ((uint64_t)mx < ((uint64_t)1 << (8 * P))) return P;
-    }
+    int64_t lo = -((int64_t)1 << (8 * P - 1)), hi = ((int64_t)1 << (8 * P - 1)) - 1;
+    if (mn >= lo && mx <= hi) { *is_signed = 1; return P; }
+    if (mn >= 0 && (uint64_t)mx < ((uint64_t)1 << (8 * P))) { *is_signed = 0; return P; }
   }
+  *is_signed = mn < 0;
   return 8;
 }
 

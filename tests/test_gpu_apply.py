@@ -366,3 +366,36 @@ def test_config2_against_reference_outputs(invop, O, golden):
     Y32, _ = invop.apply_many(plan, g["X"], precision="f32")
     for t in range(16):
         assert O.relative_error(Y32[t], g["Y"][t]) <= F32_TOL
+
+
+@pytest.mark.parametrize("lo,hi", [(0, 250), (-120, 120), (0, 60000), (-30000, 30000),
+                                   (0, 9_000_000), (-4_000_000, 4_000_000), (0, 16_000_000),
+                                   (-2_000_000_000, 2_000_000_000)])
+def test_stream_kernel_long_rows(invop, O, lo, hi):
+    """Rows of >= 16 column steps take the bulk-copy streaming kernel (k2_stream)."""
+    import torch
+
+    N, rows = 8704, 300
+    rng = np.random.default_rng(hi)
+    mant = rng.integers(lo, hi + 1, size=(rows, N))
+    mant[rng.random((rows, N)) < 0.1] = 0
+    dplan = invop._plan.DevicePlan.from_mantissas(mant, 3, row0=0, n=N)
+    x = rng.standard_normal(N)
+    x[::7] *= 1e-3
+    y32 = dplan.apply_device(torch.tensor(x, device="cuda", dtype=torch.float32), mode=0)
+    yo = O.ordered_apply(mant, 3, x.astype(np.float32).astype(np.float64))
+    tol = F32_TOL if max(abs(lo), hi) < 2 ** 24 else 1e-4
+    assert relerr(y32.cpu().numpy(), yo) <= tol
+    # a non-finite entry of x: zero mantissas in that column must be skipped
+    col = 4321
+    mant2 = mant.copy()
+    mant2[::2, col] = 0
+    dplan2 = invop._plan.DevicePlan.from_mantissas(mant2, 3, row0=0, n=N)
+    xb = x.copy()
+    xb[col] = np.inf
+    y = dplan2.apply_device(torch.tensor(xb, device="cuda", dtype=torch.float32), mode=0).cpu().numpy()
+    yo2 = O.ordered_apply(mant2, 3, xb.astype(np.float32).astype(np.float64))
+    fin = np.isfinite(yo2)
+    assert np.array_equal(np.isfinite(y), fin)
+    assert np.array_equal(np.sign(y[~fin]), np.sign(yo2[~fin]))
+    assert relerr(y[fin], yo2[fin]) <= tol
