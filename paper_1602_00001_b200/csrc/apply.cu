@@ -176,9 +176,11 @@ __global__ void __launch_bounds__(512, 1) k2_fast(FastArgs a) {
                 for (int k = 0; k < KR; ++k) {
                   float xv = xr[t][k][q];
                   if (masked) {
-                    // reference skips zero mantissas: 0*inf must not poison
-                    bool nz = TWO ? (fl[i] != 0.0f || fh[i] != 0.0f) : (fl[i] != 0.0f);
-                    if (!nz) continue;
+                    // reference skips zero mantissas (0*inf must not poison) and
+                    // v*inf must keep v's sign: use v as one float here
+                    const float vf = TWO ? fmaf(fh[i], 65536.0f, fl[i]) : fl[i];
+                    if (vf != 0.0f) acc[r][k] = fmaf(vf, xv, acc[r][k]);
+                    continue;
                   }
                   acc[r][k] = fmaf(fl[i], xv, acc[r][k]);
                   if (TWO) acch[r][k] = fmaf(fh[i], xv, acch[r][k]);
@@ -487,7 +489,7 @@ __global__ void __launch_bounds__((ST_CONSUMERS + 1) * 32, 1) k2_stream(StreamAr
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         part = (double)acc * inv2e;
       } else {
-        float acc = 0.0f, acch = 0.0f;
+        float acc = 0.0f;
 #pragma unroll
         for (int t = 0; t < ST_SW; ++t) {
           if (!stepv[t]) continue;
@@ -511,23 +513,20 @@ __global__ void __launch_bounds__((ST_CONSUMERS + 1) * 32, 1) k2_stream(StreamAr
             }
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-              const bool nz = TWO ? (fl[i] != 0.0f || fh[i] != 0.0f) : (fl[i] != 0.0f);
-              if (!nz) continue;     // reference skips zero mantissas (0*inf)
+              // reference skips zero mantissas (0*inf); v*inf keeps v's sign
+              const float vf = TWO ? fmaf(fh[i], 65536.0f, fl[i]) : fl[i];
+              if (vf == 0.0f) continue;
               const int64_t col = gc + 4 * w + i;
               const float xv = col < a.n ? a.x[col] : 0.0f;
-              acc = fmaf(fl[i], xv, acc);
-              if (TWO) acch = fmaf(fh[i], xv, acch);
+              acc = fmaf(vf, xv, acc);
             }
           }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_s + 8 * (S + st));
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          acc += __shfl_xor_sync(0xffffffffu, acc, o);
-          if (TWO) acch += __shfl_xor_sync(0xffffffffu, acch, o);
-        }
-        part = TWO ? (double)acc + 65536.0 * (double)acch : (double)acc;
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        part = (double)acc;
       }
       if (lane == 0) {
         double* sp = &slot[lr * ST_CONSUMERS + wc];
