@@ -395,12 +395,13 @@ __global__ void __launch_bounds__((ST_CONSUMERS + 1) * 32, 1) k2_stream(StreamAr
     if (lane == 0) {
       uint64_t policy;
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+      // incremental counters: no integer division on the per-row path
+      int st = 0, slab = 0;
+      uint32_t ph = 0;
+      int64_t lr = 0;
       for (int64_t u = 0; u < units; ++u) {
-        const int st = (int)(u % S);
-        const uint32_t ph = (uint32_t)((u / S) & 1);
         if (u >= S) mbar_wait(bar_s + 8 * (S + st), ph ^ 1);
-        const int slab = (int)(u / nrows);
-        const int64_t r = row_lo + (u - (int64_t)slab * nrows);
+        const int64_t r = row_lo + lr;
         const int64_t c0 = (int64_t)slab * ST_SLAB;
         const uint32_t bytes = (uint32_t)min((int64_t)ST_SLAB, a.ld - c0);
         mbar_expect_tx(bar_s + 8 * st, bytes * P);
@@ -408,6 +409,8 @@ __global__ void __launch_bounds__((ST_CONSUMERS + 1) * 32, 1) k2_stream(StreamAr
         for (int b = 0; b < P; ++b)
           bulk_g2s(ring_s + st * a.stage_bytes + b * ST_SLAB, a.planes[b] + r * a.ld + c0,
                    bytes, bar_s + 8 * st, policy);
+        if (++st == S) { st = 0; ph ^= 1; }
+        if (++lr == nrows) { lr = 0; ++slab; }
       }
     }
   } else {
@@ -418,11 +421,10 @@ __global__ void __launch_bounds__((ST_CONSUMERS + 1) * 32, 1) k2_stream(StreamAr
     bool masked = false;
     double inv2e = 1.0;
     int cur_slab = -1;
+    int st = 0, slab = 0;
+    uint32_t ph = 0;
+    int64_t lr = 0;
     for (int64_t u = 0; u < units; ++u) {
-      const int st = (int)(u % S);
-      const uint32_t ph = (uint32_t)((u / S) & 1);
-      const int slab = (int)(u / nrows);
-      const int64_t lr = u - (int64_t)slab * nrows;
       if (slab != cur_slab) {
         // x piece of this warp -> registers; fixed-point exponent from its max
         cur_slab = slab;
@@ -463,7 +465,7 @@ __global__ void __launch_bounds__((ST_CONSUMERS + 1) * 32, 1) k2_stream(StreamAr
       const unsigned char* sb = ring + (size_t)st * a.stage_bytes;
       double part;
       if (!masked) {
-        long long acc = 0;
+        long long acc = 0, acc2 = 0;
 #pragma unroll
         for (int t = 0; t < ST_SW; ++t) {
           if (!stepv[t]) continue;   // warp-uniform
@@ -479,10 +481,13 @@ __global__ void __launch_bounds__((ST_CONSUMERS + 1) * 32, 1) k2_stream(StreamAr
             for (int b = 0; b < P; ++b) wds[b] = u4get(cw[b], w);
             int32_t uv[4];
             dec_int4<P, SIGNED>(wds, uv);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) acc += (long long)uv[i] * X[t][4 * w + i];
+            acc += (long long)uv[0] * X[t][4 * w + 0];
+            acc2 += (long long)uv[1] * X[t][4 * w + 1];
+            acc += (long long)uv[2] * X[t][4 * w + 2];
+            acc2 += (long long)uv[3] * X[t][4 * w + 3];
           }
         }
+        acc += acc2;
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_s + 8 * (S + st));   // stage consumed by this warp
 #pragma unroll
@@ -532,6 +537,8 @@ __global__ void __launch_bounds__((ST_CONSUMERS + 1) * 32, 1) k2_stream(StreamAr
         double* sp = &slot[lr * ST_CONSUMERS + wc];
         *sp = (slab == 0) ? part : (*sp + part);
       }
+      if (++st == S) { st = 0; ph ^= 1; }
+      if (++lr == nrows) { lr = 0; ++slab; }
     }
   }
   __syncthreads();
