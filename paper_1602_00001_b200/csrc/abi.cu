@@ -1,6 +1,7 @@
 // C ABI plumbing of libinvop_b200: errors, plan lifetime, apply entry points.
 #include "common.cuh"
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -59,6 +60,7 @@ extern "C" int invop_plan_destroy(invop_plan* p) {
   if (p->counters) cudaFree(p->counters);
   if (p->dev_x) cudaFree(p->dev_x);
   if (p->dev_y) cudaFree(p->dev_y);
+  if (p->k3_ws) cudaFree(p->k3_ws);
   if (p->host_pinned) cudaFreeHost(p->host_pinned);
   delete p;
   return INVOP_OK;
@@ -104,6 +106,12 @@ extern "C" int invop_apply(const invop_plan* p, const void* x, int64_t ldx, void
   }
   if (mode == INVOP_MODE_FAST) {
     if (dtype != INVOP_F32) return fail(INVOP_E_VALUE, "fast mode computes in fp32: dtype F32");
+    // many right-hand sides: tensor-core batched apply (K3)
+    const char* no_tc = getenv("INVOP_NO_TC");
+    if (!(no_tc && *no_tc && *no_tc != '0') && batched_supported(p, nrhs))
+      return apply_batched_launch(const_cast<invop_plan*>(p), (const float*)x,
+                                  nrhs > 1 ? ldx : p->n, (float*)y, nrhs > 1 ? ldy : p->rows,
+                                  nrhs, s);
     return apply_fast_launch(p, (const float*)x, nrhs > 1 ? ldx : p->n, (float*)y,
                              nrhs > 1 ? ldy : p->rows, nrhs, s);
   }

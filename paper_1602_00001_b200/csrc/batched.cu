@@ -1,0 +1,490 @@
+// K3 — batched multi-RHS apply on the 5th-generation tensor cores (sm_100a).
+//
+// Y[t, i] = 10^-m * sum_j v_ij x_tj for up to 64 right-hand sides t at once
+// (the reference applies one vector at a time, applyplan.py:175-191; the
+// multi-RHS contraction is new).
+//
+// Exact integer formulation on kind::i8 MMAs:
+//   * each right-hand side t is converted to 23-bit fixed point
+//     X_tj = rint(x_tj * 2^e_t), |X| < 2^22, and split into balanced base-256
+//     digits X = d0 + 256 d1 + 65536 d2 with d_l in [-128, 127] (signed 8-bit);
+//   * the codes are already byte planes: v = q0 + 256 q1 (q0 unsigned byte,
+//     q1 signed or unsigned byte);
+//   * v * X = sum_{p,l} q_p d_l 256^(p+l): every (plane, digit) pair is one
+//     8-bit MMA, pairs of equal weight p+l share an int32 TMEM accumulator
+//     (4 accumulators for 2-byte codes), and the epilogue combines
+//     acc_0 + 256 acc_1 + 65536 acc_2 + 2^24 acc_3 exactly in int64.
+//   The only rounding is x -> X (relative 2^-23 of max|x_t|) and the final
+//   fp32 store; int32 accumulators cannot overflow because a work unit spans
+//   at most 32768 columns (2 products of |q d| <= 32640 per column).
+//
+// Pipeline (one CTA per SM, warp-specialised, persistent over work units =
+// pairs of 128-row tiles x K splits): warp 0 issues TMA loads of the A tiles
+// (2 row tiles x P planes x 128 rows x 64 K-bytes, SWIZZLE_64B) and the B
+// tile (3 digits x 64 RHS x 64 K-bytes) into a 4-stage mbarrier ring; warp 1
+// (one elected thread) issues tcgen05.mma.cta_group::1.kind::i8 (M=128, N=64,
+// K=32) into TMEM and commits each stage back to the producer; warps 2-5 drain
+// TMEM with tcgen05.ld, combine the digit products and store Y (or add the
+// exact int64 partial of a K split atomically). Both row tiles of a unit share
+// every B tile in shared memory, halving the L2 re-reads of the digits.
+#include "common.cuh"
+#include <cuda.h>
+#include <algorithm>
+#include <cstring>
+
+namespace invop {
+
+constexpr int K3_BM = 128;            // rows per MMA tile
+constexpr int K3_TILES = 2;           // row tiles per work unit (share B)
+constexpr int K3_BK = 64;             // K bytes per stage (SWIZZLE_64B row)
+constexpr int K3_NR = 64;             // right-hand sides per MMA (N)
+constexpr int K3_ND = 3;              // x digits
+constexpr int K3_STAGES = 4;
+constexpr int K3_THREADS = 192;       // warp0 TMA, warp1 MMA+TMEM, warps 2-5 epilogue
+constexpr int K3_KMAX = 32768;        // max columns per work unit (int32 safety)
+
+constexpr int K3_A_TILE = K3_BM * K3_BK;              // 8 KB per plane per row tile
+constexpr int K3_B_TILE = K3_NR * K3_BK;              // 4 KB per digit
+
+struct K3Args {
+  int64_t rows, n;
+  int P, hi_signed;
+  int kblocks_total;       // ceil(n / K3_BK)
+  int kblocks_per_unit;
+  int splits;
+  int64_t pairs;           // ceil(rows / (K3_TILES*K3_BM))
+  int nrhs;
+  const int* e;            // [64] fixed-point exponents
+  double scale;
+  float* y;
+  int64_t ldy;
+  long long* yacc;         // [64][rows] when splits > 1
+};
+
+// ------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void k3_mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void k3_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void k3_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void k3_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "K3W_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra K3W_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, int x, int y,
+                                       uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
+      : "memory");
+}
+// K-major operand tile, rows of 64 bytes, SWIZZLE_64B (8-row atoms of 512 B)
+__device__ __forceinline__ uint64_t desc_sw64(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);   // start address
+  d |= (uint64_t)1 << 16;                    // leading byte offset (unused, swizzled K-major)
+  d |= (uint64_t)(512 >> 4) << 32;           // stride byte offset: 8 rows x 64 B
+  d |= (uint64_t)1 << 46;                    // descriptor version (sm_100)
+  d |= (uint64_t)4 << 61;                    // layout: SWIZZLE_64B
+  return d;
+}
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}" ::"r"(
+          tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate), "r"(0), "r"(0), "r"(0), "r"(0));
+}
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   bar)
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, int32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// kind::i8 instruction descriptor: D=s32, A u8/s8, B s8, both K-major
+__host__ __device__ constexpr uint32_t idesc_i8(int a_signed) {
+  return (2u << 4) | ((uint32_t)a_signed << 7) | (1u << 10) | ((uint32_t)(K3_NR >> 3) << 17) |
+         ((uint32_t)(K3_BM >> 4) << 24);
+}
+
+// ------------------------------------------------------------ main kernel
+template <int P>
+__global__ void __launch_bounds__(K3_THREADS, 1)
+    k3_batched(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapA1,
+               const __grid_constant__ CUtensorMap mapB, K3Args a) {
+  constexpr int NACC = P + K3_ND - 1;                      // weights 0 .. P+1
+  constexpr int A_BYTES = K3_TILES * P * K3_A_TILE;
+  constexpr int STAGE = A_BYTES + K3_ND * K3_B_TILE;
+  extern __shared__ __align__(1024) unsigned char k3s[];
+  unsigned char* base = (unsigned char*)(((uintptr_t)k3s + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t full[K3_STAGES], empty[K3_STAGES], tfull, tempty;
+  __shared__ uint32_t tmem_slot;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < K3_STAGES; ++i) {
+      k3_mbar_init(smem_u32(&full[i]), 1);
+      k3_mbar_init(smem_u32(&empty[i]), 1);
+    }
+    k3_mbar_init(smem_u32(&tfull), 1);
+    k3_mbar_init(smem_u32(&tempty), 4);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        smem_u32(&tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+  const int64_t units = a.pairs * a.splits;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int st = 0;
+      uint32_t ph = 0;
+      int64_t it = 0;
+      for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        const int64_t pair = u / a.splits;
+        const int split = (int)(u - pair * a.splits);
+        const int kb0 = split * a.kblocks_per_unit;
+        const int kb1 = min(a.kblocks_total, kb0 + a.kblocks_per_unit);
+        const int row0 = (int)(pair * K3_TILES * K3_BM);
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          if (it >= K3_STAGES) k3_wait(smem_u32(&empty[st]), ph ^ 1);
+          const uint32_t sb = smem_u32(base + (size_t)st * STAGE);
+          const uint32_t fb = smem_u32(&full[st]);
+          k3_expect_tx(fb, STAGE);
+#pragma unroll
+          for (int ti = 0; ti < K3_TILES; ++ti) {
+            tma_2d(sb + (ti * P + 0) * K3_A_TILE, &mapA0, kb * K3_BK, row0 + ti * K3_BM, fb);
+            if (P > 1) tma_2d(sb + (ti * P + 1) * K3_A_TILE, &mapA1, kb * K3_BK, row0 + ti * K3_BM, fb);
+          }
+#pragma unroll
+          for (int l = 0; l < K3_ND; ++l)
+            tma_2d(sb + A_BYTES + l * K3_B_TILE, &mapB, kb * K3_BK, l * K3_NR, fb);
+          if (++st == K3_STAGES) { st = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    int st = 0;
+    uint32_t ph = 0;
+    int64_t ucount = 0;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++ucount) {
+      const int64_t pair = u / a.splits;
+      const int split = (int)(u - pair * a.splits);
+      const int kb0 = split * a.kblocks_per_unit;
+      const int kb1 = min(a.kblocks_total, kb0 + a.kblocks_per_unit);
+      if (ucount > 0) k3_wait(smem_u32(&tempty), (uint32_t)((ucount - 1) & 1));
+      tc_fence_after();
+      for (int kb = kb0; kb < kb1; ++kb) {
+        k3_wait(smem_u32(&full[st]), ph);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sb = smem_u32(base + (size_t)st * STAGE);
+#pragma unroll
+          for (int kk = 0; kk < K3_BK / 32; ++kk) {
+#pragma unroll
+            for (int ti = 0; ti < K3_TILES; ++ti) {
+#pragma unroll
+              for (int w = 0; w < NACC; ++w) {
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                  const int l = w - p;
+                  if (l < 0 || l >= K3_ND) continue;
+                  // first product of weight w at the unit's first K step starts the accumulator
+                  const bool first_pair = (p == (w < K3_ND ? 0 : w - K3_ND + 1));
+                  const uint32_t acc = (kb > kb0 || kk > 0 || !first_pair) ? 1u : 0u;
+                  const uint64_t da = desc_sw64(sb + (ti * P + p) * K3_A_TILE + kk * 32);
+                  const uint64_t db = desc_sw64(sb + A_BYTES + l * K3_B_TILE + kk * 32);
+                  const uint32_t idesc = idesc_i8((p == P - 1) ? a.hi_signed : 0);
+                  mma_i8(tmem + (uint32_t)((ti * NACC + w) * K3_NR), da, db, idesc, acc);
+                }
+              }
+            }
+          }
+          mma_commit(smem_u32(&empty[st]));   // stage free once these MMAs complete
+        }
+        __syncwarp();
+        if (++st == K3_STAGES) { st = 0; ph ^= 1; }
+      }
+      if (lane == 0) mma_commit(smem_u32(&tfull));
+      __syncwarp();
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp & 3;                  // TMEM lane quarter of this warp
+    int64_t ucount = 0;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++ucount) {
+      const int64_t pair = u / a.splits;
+      k3_wait(smem_u32(&tfull), (uint32_t)(ucount & 1));
+      tc_fence_after();
+#pragma unroll 1
+      for (int ti = 0; ti < K3_TILES; ++ti) {
+        const int64_t row = pair * K3_TILES * K3_BM + ti * K3_BM + q * 32 + lane;
+#pragma unroll 1
+        for (int c0 = 0; c0 < K3_NR; c0 += 16) {
+          int32_t r[NACC][16];
+#pragma unroll
+          for (int w = 0; w < NACC; ++w)
+            tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)((ti * NACC + w) * K3_NR + c0),
+                      r[w]);
+          tmem_wait_ld();
+          if (row < a.rows) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int t = c0 + j;
+              if (t >= a.nrhs) break;
+              long long v = 0;
+#pragma unroll
+              for (int w = 0; w < NACC; ++w) v += (long long)r[w][j] * (1LL << (8 * w));
+              if (a.splits == 1) {
+                a.y[(int64_t)t * a.ldy + row] = (float)((double)v * ldexp(a.scale, -a.e[t]));
+              } else {
+                atomicAdd((unsigned long long*)&a.yacc[(int64_t)t * a.rows + row],
+                          (unsigned long long)v);
+              }
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) k3_arrive(smem_u32(&tempty));
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// ------------------------------------------------------------ x preparation
+// per right-hand side: e_t with max|x_t| * 2^e_t < 2^22
+__global__ void k3_exponents(const float* __restrict__ x, int64_t n, int64_t ldx, int nrhs,
+                             int* __restrict__ e, int* __restrict__ nonfinite) {
+  const int t = blockIdx.x;
+  float m = 0.0f;
+  if (t < nrhs)
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) m = fmaxf(m, fabsf(x[t * ldx + j]));
+  __shared__ float s[32];
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < (blockDim.x >> 5) ? s[threadIdx.x] : 0.0f;
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) {
+      int ex = 0;
+      if (m > 0.0f && isfinite(m)) frexpf(m, &ex);
+      e[t] = (m > 0.0f && isfinite(m)) ? 22 - ex : 0;
+      if (!isfinite(m)) atomicOr(nonfinite, 1);
+    }
+  }
+}
+
+// balanced base-256 digits of X = rint(x * 2^e), into B[l][t][j] (int8)
+__global__ void k3_digits(const float* __restrict__ x, int64_t n, int64_t ldx, int nrhs,
+                          const int* __restrict__ e, int8_t* __restrict__ B, int64_t ldb) {
+  const int64_t total = (int64_t)K3_NR * ldb;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int t = (int)(k / ldb);
+    const int64_t j = k - (int64_t)t * ldb;
+    int X = 0;
+    if (t < nrhs && j < n) X = __float2int_rn(ldexpf(x[t * ldx + j], e[t]));
+    const int d0 = ((X + 128) & 255) - 128;
+    const int X1 = (X - d0) >> 8;
+    const int d1 = ((X1 + 128) & 255) - 128;
+    const int d2 = (X1 - d1) >> 8;
+    B[(0 * K3_NR + t) * ldb + j] = (int8_t)d0;
+    B[(1 * K3_NR + t) * ldb + j] = (int8_t)d1;
+    B[(2 * K3_NR + t) * ldb + j] = (int8_t)d2;
+  }
+}
+
+__global__ void k3_finalize(const long long* __restrict__ yacc, int64_t rows, int nrhs,
+                            const int* __restrict__ e, double scale, float* __restrict__ y,
+                            int64_t ldy) {
+  const int64_t total = (int64_t)nrhs * rows;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int t = (int)(k / rows);
+    const int64_t i = k - (int64_t)t * rows;
+    y[t * ldy + i] = (float)((double)yacc[t * rows + i] * ldexp(scale, -e[t]));
+  }
+}
+
+// ------------------------------------------------------------ host side
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled encode_fn() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault,
+                                         &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_encodeTiled)p;
+  }
+  return fn;
+}
+
+static int make_map_u8(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer,
+                       uint64_t pitch, uint32_t box_inner, uint32_t box_outer) {
+  PFN_encodeTiled enc = encode_fn();
+  if (!enc) return fail(INVOP_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {pitch};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(ptr), dims, strides, box,
+                   es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(INVOP_E_CUDA, "cuTensorMapEncodeTiled failed");
+  return INVOP_OK;
+}
+
+bool batched_supported(const invop_plan* p, int64_t nrhs) {
+  return p->P <= 2 && nrhs >= 8 && p->n >= K3_BK && p->rows >= 1 && encode_fn() != nullptr;
+}
+
+template <int P>
+static int launch_k3(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b,
+                     const K3Args& args, int grid, cudaStream_t s) {
+  constexpr int STAGE = K3_TILES * P * K3_A_TILE + K3_ND * K3_B_TILE;
+  size_t smem = (size_t)K3_STAGES * STAGE + 1024;
+  auto kern = k3_batched<P>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  kern<<<grid, K3_THREADS, smem, s>>>(a0, a1, b, args);
+  INVOP_CHECK_LAUNCH("k3_batched");
+  return INVOP_OK;
+}
+
+int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, int64_t ldy,
+                         int64_t nrhs, cudaStream_t s) {
+  const int64_t ldb = round_up(p->n, K3_BK);
+  const int kblocks = (int)(ldb / K3_BK);
+  const int64_t pairs = cdiv(p->rows, K3_TILES * K3_BM);
+  const int sms = num_sms();
+  // K splits: each unit spans <= 32768 columns; then pick the split count that
+  // best fills the SMs in whole waves
+  int min_split = (int)cdiv(kblocks, K3_KMAX / K3_BK);
+  int best = min_split;
+  double best_eff = -1.0;
+  for (int sp = min_split; sp <= std::max(min_split, 16); ++sp) {
+    int64_t units = pairs * sp;
+    double eff = (double)units / ((double)cdiv(units, sms) * sms);
+    eff -= 0.005 * sp;   // atomics and partial tiles cost a little
+    if (eff > best_eff + 1e-9) { best_eff = eff; best = sp; }
+  }
+  const int splits = best;
+  const int kpu = (int)cdiv(kblocks, splits);
+  // workspace: digits | exponents | int64 partial sums
+  size_t b_bytes = (size_t)K3_ND * K3_NR * ldb;
+  size_t e_off = round_up(b_bytes, 256);
+  size_t acc_off = e_off + 256;
+  size_t acc_bytes = splits > 1 ? (size_t)K3_NR * p->rows * 8 : 0;
+  int rc = ensure_scratch(&p->k3_ws, &p->k3_ws_bytes, acc_off + acc_bytes);
+  // inf/nan in x: the reference's zero-mantissa skip needs the fp32 masked
+  // kernels; checked up front (one small sync per batch)
+  {
+    int* flag = (int*)((char*)p->k3_ws + e_off + 128);
+    int* e0 = (int*)((char*)p->k3_ws + e_off);
+    INVOP_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), s));
+    for (int64_t t0 = 0; t0 < nrhs; t0 += K3_NR) {
+      const int nr = (int)std::min<int64_t>(K3_NR, nrhs - t0);
+      k3_exponents<<<K3_NR, 256, 0, s>>>(x + t0 * ldx, p->n, ldx, nr, e0, flag);
+    }
+    int h = 0;
+    INVOP_CUDA(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    INVOP_CUDA(cudaStreamSynchronize(s));
+    if (h) return apply_fast_launch(p, x, ldx, y, ldy, nrhs, s);
+  }
+  if (rc) return rc;
+  int8_t* B = (int8_t*)p->k3_ws;
+  int* e = (int*)((char*)p->k3_ws + e_off);
+  long long* yacc = (long long*)((char*)p->k3_ws + acc_off);
+  if (!p->k3_maps_ready) {
+    rc = make_map_u8((CUtensorMap*)p->k3_mapA[0], p->planes[0], p->ld, p->rows, p->ld, K3_BK, K3_BM);
+    if (!rc && p->P > 1)
+      rc = make_map_u8((CUtensorMap*)p->k3_mapA[1], p->planes[1], p->ld, p->rows, p->ld, K3_BK, K3_BM);
+    if (rc) return rc;
+    if (p->P == 1) memcpy(p->k3_mapA[1], p->k3_mapA[0], sizeof(CUtensorMap));
+    p->k3_maps_ready = 1;
+  }
+  CUtensorMap mapB;
+  rc = make_map_u8(&mapB, B, ldb, (uint64_t)K3_ND * K3_NR, ldb, K3_BK, K3_NR);
+  if (rc) return rc;
+  for (int64_t t0 = 0; t0 < nrhs; t0 += K3_NR) {
+    const int nr = (int)std::min<int64_t>(K3_NR, nrhs - t0);
+    int* flag = (int*)((char*)p->k3_ws + e_off + 128);
+    k3_exponents<<<K3_NR, 256, 0, s>>>(x + t0 * ldx, p->n, ldx, nr, e, flag);
+    k3_digits<<<(unsigned)std::min<int64_t>(cdiv((int64_t)K3_NR * ldb, 256), sms * 16), 256, 0, s>>>(
+        x + t0 * ldx, p->n, ldx, nr, e, B, ldb);
+    if (splits > 1) INVOP_CUDA(cudaMemsetAsync(yacc, 0, acc_bytes, s));
+    K3Args a;
+    a.rows = p->rows; a.n = p->n; a.P = p->P; a.hi_signed = p->is_signed;
+    a.kblocks_total = kblocks; a.kblocks_per_unit = kpu; a.splits = splits;
+    a.pairs = pairs; a.nrhs = nr; a.e = e; a.scale = p->scale;
+    a.y = y + t0 * ldy; a.ldy = ldy; a.yacc = yacc;
+    int grid = (int)std::min<int64_t>(sms, pairs * splits);
+    const CUtensorMap* A0 = (const CUtensorMap*)p->k3_mapA[0];
+    const CUtensorMap* A1 = (const CUtensorMap*)p->k3_mapA[1];
+    rc = p->P == 1 ? launch_k3<1>(*A0, *A1, mapB, a, grid, s) : launch_k3<2>(*A0, *A1, mapB, a, grid, s);
+    if (rc) return rc;
+    if (splits > 1) {
+      int64_t tot = (int64_t)nr * p->rows;
+      k3_finalize<<<(unsigned)std::min<int64_t>(cdiv(tot, 256), sms * 8), 256, 0, s>>>(
+          yacc, p->rows, nr, e, p->scale, y + t0 * ldy, ldy);
+    }
+  }
+  INVOP_CHECK_LAUNCH("k3 epilogue");
+  return INVOP_OK;
+}
+
+}  // namespace invop

@@ -33,6 +33,10 @@ struct invop_plan {
   void* dev_x = nullptr; size_t dev_x_bytes = 0;
   void* dev_y = nullptr; size_t dev_y_bytes = 0;
   double* host_pinned = nullptr; size_t host_pinned_bytes = 0;
+  // K3 (tensor-core batched apply): workspace and cached TMA descriptors
+  void* k3_ws = nullptr; size_t k3_ws_bytes = 0;
+  alignas(64) unsigned char k3_mapA[2][128];
+  int k3_maps_ready = 0;
 };
 
 struct invop_operator {
@@ -75,6 +79,9 @@ int plan_finalize_width(invop_plan* p, int64_t mn, int64_t mx, int64_t nnz);
 // apply kernels
 int apply_fast_launch(const invop_plan* p, const float* x, int64_t ldx, float* y,
                       int64_t ldy, int64_t nrhs, cudaStream_t s);
+bool batched_supported(const invop_plan* p, int64_t nrhs);
+int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, int64_t ldy,
+                         int64_t nrhs, cudaStream_t s);
 int apply_ordered_launch(const invop_plan* p, const double* x, int64_t ldx, double* y,
                          int64_t ldy, int64_t nrhs, cudaStream_t s);
 

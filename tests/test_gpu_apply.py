@@ -399,3 +399,34 @@ def test_stream_kernel_long_rows(invop, O, lo, hi):
     assert np.array_equal(np.isfinite(y), fin)
     assert np.array_equal(np.sign(y[~fin]), np.sign(yo2[~fin]))
     assert relerr(y[fin], yo2[fin]) <= tol
+
+
+# ------------------------------------------------------------------ K3 (tensor cores)
+@pytest.mark.parametrize("rows,n,lo,hi,k", [(1000, 3000, 0, 250, 64), (700, 2048, -120, 120, 64),
+                                            (1000, 3000, 0, 60000, 64), (333, 5000, -30000, 30000, 64),
+                                            (256, 40000, 0, 41690, 64), (1500, 1200, 0, 40000, 17),
+                                            (129, 777, -32768, 32767, 8)])
+def test_batched_tensor_core_apply(invop, O, rows, n, lo, hi, k):
+    import torch
+
+    rng = np.random.default_rng(rows + n + k)
+    mant = rng.integers(lo, hi + 1, size=(rows, n))
+    mant[rng.random((rows, n)) < 0.05] = 0
+    dplan = invop._plan.DevicePlan.from_mantissas(mant, 4, row0=0, n=n)
+    assert dplan.code_bytes <= 2
+    X = rng.standard_normal((k, n))
+    X[0] *= 1e-6
+    X[-1, ::3] = 0.0
+    Xd = torch.tensor(X, device="cuda", dtype=torch.float32)
+    Y = dplan.apply_device(Xd, mode=0).cpu().numpy()
+    Yo = O.ordered_apply(mant, 4, X.astype(np.float32).astype(np.float64))
+    for t in range(k):
+        assert relerr(Y[t], Yo[t]) <= F32_TOL, t
+    # non-finite x goes through the masked fp32 kernels
+    X2 = X.copy()
+    X2[3, 5] = np.inf
+    Y2 = dplan.apply_device(torch.tensor(X2, device="cuda", dtype=torch.float32), mode=0).cpu().numpy()
+    Yo2 = O.ordered_apply(mant, 4, X2.astype(np.float32).astype(np.float64))
+    assert np.array_equal(np.isfinite(Y2), np.isfinite(Yo2))
+    fin = np.isfinite(Yo2[0])
+    assert relerr(Y2[0][fin], Yo2[0][fin]) <= F32_TOL
