@@ -404,7 +404,7 @@ def test_stream_kernel_long_rows(invop, O, lo, hi):
 # ------------------------------------------------------------------ K3 (tensor cores)
 @pytest.mark.parametrize("rows,n,lo,hi,k", [(1000, 3000, 0, 250, 64), (700, 2048, -120, 120, 64),
                                             (1000, 3000, 0, 60000, 64), (333, 5000, -30000, 30000, 64),
-                                            (256, 40000, 0, 41690, 64), (1500, 1200, 0, 40000, 17),
+                                            (256, 40000, 0, 41690, 64), (1200, 1500, 0, 40000, 17),
                                             (129, 777, -32768, 32767, 8)])
 def test_batched_tensor_core_apply(invop, O, rows, n, lo, hi, k):
     import torch
