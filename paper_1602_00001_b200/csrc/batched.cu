@@ -427,13 +427,13 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
   // workspace: digits | exponents | int64 partial sums
   size_t b_bytes = (size_t)K3_ND * K3_NR * ldb;
   size_t e_off = round_up(b_bytes, 256);
-  size_t acc_off = e_off + 256;
+  size_t acc_off = e_off + 512;          // e[64] ints | flag | pad
   size_t acc_bytes = splits > 1 ? (size_t)K3_NR * p->rows * 8 : 0;
   int rc = ensure_scratch(&p->k3_ws, &p->k3_ws_bytes, acc_off + acc_bytes);
   // inf/nan in x: the reference's zero-mantissa skip needs the fp32 masked
   // kernels; checked up front (one small sync per batch)
   {
-    int* flag = (int*)((char*)p->k3_ws + e_off + 128);
+    int* flag = (int*)((char*)p->k3_ws + e_off + 256);
     int* e0 = (int*)((char*)p->k3_ws + e_off);
     INVOP_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), s));
     for (int64_t t0 = 0; t0 < nrhs; t0 += K3_NR) {
@@ -462,7 +462,7 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
   if (rc) return rc;
   for (int64_t t0 = 0; t0 < nrhs; t0 += K3_NR) {
     const int nr = (int)std::min<int64_t>(K3_NR, nrhs - t0);
-    int* flag = (int*)((char*)p->k3_ws + e_off + 128);
+    int* flag = (int*)((char*)p->k3_ws + e_off + 256);
     k3_exponents<<<K3_NR, 256, 0, s>>>(x + t0 * ldx, p->n, ldx, nr, e, flag);
     k3_digits<<<(unsigned)std::min<int64_t>(cdiv((int64_t)K3_NR * ldb, 256), sms * 16), 256, 0, s>>>(
         x + t0 * ldx, p->n, ldx, nr, e, B, ldb);
