@@ -61,6 +61,8 @@ extern "C" int invop_plan_destroy(invop_plan* p) {
   if (p->dev_x) cudaFree(p->dev_x);
   if (p->dev_y) cudaFree(p->dev_y);
   if (p->k3_ws) cudaFree(p->k3_ws);
+  for (int b = 0; b < 2; ++b)
+    if (p->k3_tiles[b]) cudaFree(p->k3_tiles[b]);
   if (p->host_pinned) cudaFreeHost(p->host_pinned);
   delete p;
   return INVOP_OK;

@@ -50,6 +50,7 @@ struct K3Args {
   int64_t rows, n;
   int P, hi_signed;
   int kblocks_total;       // ceil(n / K3_BK)
+  int kb_stride;           // tiles per row tile in the tiled planes (ld / K3_BK)
   int kblocks_per_unit;
   int splits;
   int64_t pairs;           // ceil(rows / (K3_TILES*K3_BM))
@@ -194,8 +195,10 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
           k3_expect_tx(fb, STAGE);
 #pragma unroll
           for (int ti = 0; ti < K3_TILES; ++ti) {
-            tma_2d(sb + (ti * P + 0) * K3_A_TILE, &mapA0, kb * K3_BK, row0 + ti * K3_BM, fb);
-            if (P > 1) tma_2d(sb + (ti * P + 1) * K3_A_TILE, &mapA1, kb * K3_BK, row0 + ti * K3_BM, fb);
+            // tiled planes: tile (rt, kb) starts at tensor row (rt*kblocks + kb)*128
+            const int trow = (int)(((int64_t)(row0 / K3_BM + ti) * a.kb_stride + kb) * K3_BM);
+            tma_2d(sb + (ti * P + 0) * K3_A_TILE, &mapA0, 0, trow, fb);
+            if (P > 1) tma_2d(sb + (ti * P + 1) * K3_A_TILE, &mapA1, 0, trow, fb);
           }
 #pragma unroll
           for (int l = 0; l < K3_ND; ++l)
@@ -296,6 +299,30 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// ------------------------------------------------------------ tiled planes
+// K3 streams 128-row x 64-column tiles. In the row-major planes a tile is 128
+// separate 64-byte pieces (one per row, ld bytes apart): every TMA box then
+// touches 128 DRAM pages. The tensor-core path therefore reads a tiled copy of
+// the planes, built once per plan: tile (rt, kb) = rows [128 rt, 128 rt+128) x
+// columns [64 kb, 64 kb+64) stored as one contiguous 8 KB block, tiles of a row
+// tile consecutive along K, so a row tile's whole K range is one contiguous run.
+__global__ void k3_tile_planes(const uint8_t* __restrict__ in, int64_t rows, int64_t ld,
+                               uint8_t* __restrict__ out, int64_t rtiles) {
+  const int64_t kbt = ld / K3_BK;
+  const int64_t total16 = rtiles * kbt * (K3_A_TILE / 16);
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total16;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t tile = k / (K3_A_TILE / 16);
+    const int within = (int)(k - tile * (K3_A_TILE / 16));
+    const int r = within >> 2, c16 = within & 3;
+    const int64_t rt = tile / kbt, kb = tile - rt * kbt;
+    const int64_t row = rt * K3_BM + r;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (row < rows) v = *reinterpret_cast<const uint4*>(in + row * ld + kb * K3_BK + c16 * 16);
+    *reinterpret_cast<uint4*>(out + tile * K3_A_TILE + r * K3_BK + c16 * 16) = v;
   }
 }
 
@@ -422,8 +449,8 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
     eff -= 0.005 * sp;   // atomics and partial tiles cost a little
     if (eff > best_eff + 1e-9) { best_eff = eff; best = sp; }
   }
-  const int splits = best;
-  const int kpu = (int)cdiv(kblocks, splits);
+  const int kpu = (int)cdiv(kblocks, best);
+  const int splits = (int)cdiv(kblocks, kpu);   // no empty K ranges
   // workspace: digits | exponents | int64 partial sums
   size_t b_bytes = (size_t)K3_ND * K3_NR * ldb;
   size_t e_off = round_up(b_bytes, 256);
@@ -450,9 +477,18 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
   int* e = (int*)((char*)p->k3_ws + e_off);
   long long* yacc = (long long*)((char*)p->k3_ws + acc_off);
   if (!p->k3_maps_ready) {
-    rc = make_map_u8((CUtensorMap*)p->k3_mapA[0], p->planes[0], p->ld, p->rows, p->ld, K3_BK, K3_BM);
+    const int64_t rtiles = pairs * K3_TILES;   // row tiles, padded to whole pairs
+    const int64_t tile_bytes = rtiles * (p->ld / K3_BK) * K3_A_TILE;
+    for (int b = 0; b < p->P; ++b) {
+      if (!p->k3_tiles[b]) INVOP_CUDA(cudaMalloc(&p->k3_tiles[b], tile_bytes));
+      k3_tile_planes<<<(unsigned)std::min<int64_t>(cdiv(tile_bytes / 16, 256), sms * 16), 256, 0, s>>>(
+          p->planes[b], p->rows, p->ld, p->k3_tiles[b], rtiles);
+      INVOP_CHECK_LAUNCH("k3_tile_planes");
+    }
+    const uint64_t trows = (uint64_t)rtiles * (p->ld / K3_BK) * K3_BM;
+    rc = make_map_u8((CUtensorMap*)p->k3_mapA[0], p->k3_tiles[0], K3_BK, trows, K3_BK, K3_BK, K3_BM);
     if (!rc && p->P > 1)
-      rc = make_map_u8((CUtensorMap*)p->k3_mapA[1], p->planes[1], p->ld, p->rows, p->ld, K3_BK, K3_BM);
+      rc = make_map_u8((CUtensorMap*)p->k3_mapA[1], p->k3_tiles[1], K3_BK, trows, K3_BK, K3_BK, K3_BM);
     if (rc) return rc;
     if (p->P == 1) memcpy(p->k3_mapA[1], p->k3_mapA[0], sizeof(CUtensorMap));
     p->k3_maps_ready = 1;
@@ -470,6 +506,7 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
     K3Args a;
     a.rows = p->rows; a.n = p->n; a.P = p->P; a.hi_signed = p->is_signed;
     a.kblocks_total = kblocks; a.kblocks_per_unit = kpu; a.splits = splits;
+    a.kb_stride = (int)(p->ld / K3_BK);
     a.pairs = pairs; a.nrhs = nr; a.e = e; a.scale = p->scale;
     a.y = y + t0 * ldy; a.ldy = ldy; a.yacc = yacc;
     int grid = (int)std::min<int64_t>(sms, pairs * splits);

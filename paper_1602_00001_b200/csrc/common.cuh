@@ -35,6 +35,7 @@ struct invop_plan {
   double* host_pinned = nullptr; size_t host_pinned_bytes = 0;
   // K3 (tensor-core batched apply): workspace and cached TMA descriptors
   void* k3_ws = nullptr; size_t k3_ws_bytes = 0;
+  uint8_t* k3_tiles[2] = {nullptr, nullptr};   // tiled copy of planes 0/1
   alignas(64) unsigned char k3_mapA[2][128];
   int k3_maps_ready = 0;
 };
