@@ -31,6 +31,8 @@
 #include <cuda.h>
 #include <algorithm>
 #include <cstring>
+#include <cstdio>
+#include <cstdlib>
 
 namespace invop {
 
@@ -143,21 +145,21 @@ __host__ __device__ constexpr uint32_t idesc_i8(int a_signed) {
 }
 
 // ------------------------------------------------------------ main kernel
-template <int P>
+template <int P, int TILES, int STAGES>
 __global__ void __launch_bounds__(K3_THREADS, 1)
     k3_batched(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapA1,
                const __grid_constant__ CUtensorMap mapB, K3Args a) {
   constexpr int NACC = P + K3_ND - 1;                      // weights 0 .. P+1
-  constexpr int A_BYTES = K3_TILES * P * K3_A_TILE;
+  constexpr int A_BYTES = TILES * P * K3_A_TILE;
   constexpr int STAGE = A_BYTES + K3_ND * K3_B_TILE;
   extern __shared__ __align__(1024) unsigned char k3s[];
   unsigned char* base = (unsigned char*)(((uintptr_t)k3s + 1023) & ~(uintptr_t)1023);
-  __shared__ __align__(8) uint64_t full[K3_STAGES], empty[K3_STAGES], tfull, tempty;
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], tfull, tempty;
   __shared__ uint32_t tmem_slot;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < K3_STAGES; ++i) {
+    for (int i = 0; i < STAGES; ++i) {
       k3_mbar_init(smem_u32(&full[i]), 1);
       k3_mbar_init(smem_u32(&empty[i]), 1);
     }
@@ -187,14 +189,14 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
         const int split = (int)(u - pair * a.splits);
         const int kb0 = split * a.kblocks_per_unit;
         const int kb1 = min(a.kblocks_total, kb0 + a.kblocks_per_unit);
-        const int row0 = (int)(pair * K3_TILES * K3_BM);
+        const int row0 = (int)(pair * TILES * K3_BM);
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
-          if (it >= K3_STAGES) k3_wait(smem_u32(&empty[st]), ph ^ 1);
+          if (it >= STAGES) k3_wait(smem_u32(&empty[st]), ph ^ 1);
           const uint32_t sb = smem_u32(base + (size_t)st * STAGE);
           const uint32_t fb = smem_u32(&full[st]);
           k3_expect_tx(fb, STAGE);
 #pragma unroll
-          for (int ti = 0; ti < K3_TILES; ++ti) {
+          for (int ti = 0; ti < TILES; ++ti) {
             // tiled planes: tile (rt, kb) starts at tensor row (rt*kblocks + kb)*128
             const int trow = (int)(((int64_t)(row0 / K3_BM + ti) * a.kb_stride + kb) * K3_BM);
             tma_2d(sb + (ti * P + 0) * K3_A_TILE, &mapA0, 0, trow, fb);
@@ -203,7 +205,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
 #pragma unroll
           for (int l = 0; l < K3_ND; ++l)
             tma_2d(sb + A_BYTES + l * K3_B_TILE, &mapB, kb * K3_BK, l * K3_NR, fb);
-          if (++st == K3_STAGES) { st = 0; ph ^= 1; }
+          if (++st == STAGES) { st = 0; ph ^= 1; }
         }
       }
     }
@@ -227,7 +229,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
 #pragma unroll
           for (int kk = 0; kk < K3_BK / 32; ++kk) {
 #pragma unroll
-            for (int ti = 0; ti < K3_TILES; ++ti) {
+            for (int ti = 0; ti < TILES; ++ti) {
 #pragma unroll
               for (int w = 0; w < NACC; ++w) {
 #pragma unroll
@@ -248,7 +250,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
           mma_commit(smem_u32(&empty[st]));   // stage free once these MMAs complete
         }
         __syncwarp();
-        if (++st == K3_STAGES) { st = 0; ph ^= 1; }
+        if (++st == STAGES) { st = 0; ph ^= 1; }
       }
       if (lane == 0) mma_commit(smem_u32(&tfull));
       __syncwarp();
@@ -262,8 +264,8 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
       k3_wait(smem_u32(&tfull), (uint32_t)(ucount & 1));
       tc_fence_after();
 #pragma unroll 1
-      for (int ti = 0; ti < K3_TILES; ++ti) {
-        const int64_t row = pair * K3_TILES * K3_BM + ti * K3_BM + q * 32 + lane;
+      for (int ti = 0; ti < TILES; ++ti) {
+        const int64_t row = pair * TILES * K3_BM + ti * K3_BM + q * 32 + lane;
 #pragma unroll 1
         for (int c0 = 0; c0 < K3_NR; c0 += 16) {
           int32_t r[NACC][16];
@@ -420,12 +422,12 @@ bool batched_supported(const invop_plan* p, int64_t nrhs) {
   return p->P <= 2 && nrhs >= 8 && p->n >= K3_BK && p->rows >= 1 && encode_fn() != nullptr;
 }
 
-template <int P>
+template <int P, int TILES, int STAGES>
 static int launch_k3(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b,
                      const K3Args& args, int grid, cudaStream_t s) {
-  constexpr int STAGE = K3_TILES * P * K3_A_TILE + K3_ND * K3_B_TILE;
-  size_t smem = (size_t)K3_STAGES * STAGE + 1024;
-  auto kern = k3_batched<P>;
+  constexpr int STAGE = TILES * P * K3_A_TILE + K3_ND * K3_B_TILE;
+  size_t smem = (size_t)STAGES * STAGE + 1024;
+  auto kern = k3_batched<P, TILES, STAGES>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   kern<<<grid, K3_THREADS, smem, s>>>(a0, a1, b, args);
   INVOP_CHECK_LAUNCH("k3_batched");
@@ -436,7 +438,10 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
                          int64_t nrhs, cudaStream_t s) {
   const int64_t ldb = round_up(p->n, K3_BK);
   const int kblocks = (int)(ldb / K3_BK);
-  const int64_t pairs = cdiv(p->rows, K3_TILES * K3_BM);
+  // variant: row tiles per unit (share B) and pipeline depth
+  int tiles = K3_TILES, stages = K3_STAGES;
+  if (const char* v = getenv("INVOP_K3_CFG")) sscanf(v, "%d,%d", &tiles, &stages);
+  const int64_t pairs = cdiv(p->rows, tiles * K3_BM);
   const int sms = num_sms();
   // K splits: each unit spans <= 32768 columns; then pick the split count that
   // best fills the SMs in whole waves
@@ -449,6 +454,7 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
     eff -= 0.005 * sp;   // atomics and partial tiles cost a little
     if (eff > best_eff + 1e-9) { best_eff = eff; best = sp; }
   }
+  if (const char* v = getenv("INVOP_K3_SPLITS")) best = std::max(min_split, atoi(v));
   const int kpu = (int)cdiv(kblocks, best);
   const int splits = (int)cdiv(kblocks, kpu);   // no empty K ranges
   // workspace: digits | exponents | int64 partial sums
@@ -477,7 +483,7 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
   int* e = (int*)((char*)p->k3_ws + e_off);
   long long* yacc = (long long*)((char*)p->k3_ws + acc_off);
   if (!p->k3_maps_ready) {
-    const int64_t rtiles = pairs * K3_TILES;   // row tiles, padded to whole pairs
+    const int64_t rtiles = round_up(cdiv(p->rows, K3_BM), 2);   // row tiles (even)
     const int64_t tile_bytes = rtiles * (p->ld / K3_BK) * K3_A_TILE;
     for (int b = 0; b < p->P; ++b) {
       if (!p->k3_tiles[b]) INVOP_CUDA(cudaMalloc(&p->k3_tiles[b], tile_bytes));
@@ -512,7 +518,16 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
     int grid = (int)std::min<int64_t>(sms, pairs * splits);
     const CUtensorMap* A0 = (const CUtensorMap*)p->k3_mapA[0];
     const CUtensorMap* A1 = (const CUtensorMap*)p->k3_mapA[1];
-    rc = p->P == 1 ? launch_k3<1>(*A0, *A1, mapB, a, grid, s) : launch_k3<2>(*A0, *A1, mapB, a, grid, s);
+    const int key = p->P * 100 + tiles * 10 + stages;
+    switch (key) {
+      case 124: rc = launch_k3<1, 2, 4>(*A0, *A1, mapB, a, grid, s); break;
+      case 116: rc = launch_k3<1, 1, 6>(*A0, *A1, mapB, a, grid, s); break;
+      case 224: rc = launch_k3<2, 2, 4>(*A0, *A1, mapB, a, grid, s); break;
+      case 216: rc = launch_k3<2, 1, 6>(*A0, *A1, mapB, a, grid, s); break;
+      case 214: rc = launch_k3<2, 1, 4>(*A0, *A1, mapB, a, grid, s); break;
+      case 223: rc = launch_k3<2, 2, 3>(*A0, *A1, mapB, a, grid, s); break;
+      default: return fail(INVOP_E_VALUE, "unsupported INVOP_K3_CFG");
+    }
     if (rc) return rc;
     if (splits > 1) {
       int64_t tot = (int64_t)nr * p->rows;
