@@ -273,6 +273,7 @@ def run_ours(args, world, rank, local):
         if world > 1:
             torch.distributed.all_gather_into_tensor(full.view(-1), y32.view(-1))
 
+    plan_ld = (N + 511) // 512 * 512
     L.check(L.lib.invop_apply(h, x32.data_ptr(), N, y32.data_ptr(), rows, k, L.F32, L.MODE_FAST,
                               C.c_void_p(sptr)), "apply")
     for _ in range(max(args.warmup, 3)):
@@ -351,7 +352,10 @@ def run_ours(args, world, rank, local):
     # ---- roofline of the dominant kernel (K2 fast, one launch per step)
     peak, peak_src = _peaks()
     code_bytes = plan.code_bytes
-    alg_bytes = rows * N * code_bytes + k * N * 4 + k * rows * 4
+    op_bytes = C.c_int64()
+    L.check(L.lib.invop_plan_apply_bytes(h, k, L.MODE_FAST, C.byref(op_bytes), C.c_void_p(sptr)))
+    op_bytes = op_bytes.value
+    alg_bytes = op_bytes + k * N * 4 + k * rows * 4
     achieved = alg_bytes / (k_ms * 1e-3) / 1e9
     int8_ops = 2.0 * rows * N * k * (code_bytes * 3) if k > 1 else None
     traffic = None
@@ -382,7 +386,8 @@ def run_ours(args, world, rank, local):
             "config": {
                 "workload": cfg.name, "N": N, "digits": cfg.digits, "nrhs": k,
                 "rows_per_gpu": rows, "code_bytes_per_entry": code_bytes,
-                "operator_bytes_per_gpu": rows * N * code_bytes,
+                "operator_bytes_per_gpu": op_bytes,
+                "operator_bytes_per_entry": op_bytes / (rows * N),
                 "parallelism": "row-shard x%d + all-gather" % world if world > 1 else "single GPU",
                 "l2": "inputs larger than L2 (operator %.0f MB vs 126 MB L2); no flush"
                       % (rows * N * code_bytes / 1e6),
@@ -390,7 +395,9 @@ def run_ours(args, world, rank, local):
             "roofline": {
                 "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
-                "kernel": ("k2_stream<P=%d>" % code_bytes) if k == 1 else ("k3_batched<P=%d> (tcgen05 kind::i8)" % code_bytes),
+                "kernel": (("k2_vw (variable-width chunks, %.3f B/entry)" % (op_bytes / (rows * N)))
+                           if op_bytes != rows * plan_ld * code_bytes else "k2_stream<P=%d>" % code_bytes)
+                          if k == 1 else ("k3_batched<P=%d> (tcgen05 kind::i8)" % code_bytes),
                 "kernel_ms": k_ms,
                 "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_src,
             },

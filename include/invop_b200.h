@@ -134,6 +134,12 @@ int invop_apply(const invop_plan* plan, const void* x, int64_t ldx, void* y, int
 int invop_apply_host(invop_plan* plan, const double* x, double* y, int64_t nrhs,
                      int mode, void* stream);
 
+/* Bytes of operator data one apply of `nrhs` right-hand sides in `mode`
+   streams from HBM (codes + per-chunk metadata), i.e. the algorithmic bytes
+   of the roofline; builds the lazily created layouts first (synchronous). */
+int invop_plan_apply_bytes(invop_plan* plan, int64_t nrhs, int mode, int64_t* bytes,
+                           void* stream);
+
 /* A8 — naive quantized apply of the reference (applyplan.py:194-209):
    identical arithmetic to ORDERED mode; provided under its own name. */
 int invop_apply_naive(const invop_plan* plan, const double* x, double* y, int64_t nrhs,

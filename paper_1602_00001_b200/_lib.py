@@ -55,6 +55,7 @@ SIGNATURES = {
     "invop_apply": [_vp, _vp, _i64, _vp, _i64, _i64, _int, _int, _vp],
     "invop_apply_host": [_vp, _vp, _vp, _i64, _int, _vp],
     "invop_apply_naive": [_vp, _vp, _vp, _i64, _vp],
+    "invop_plan_apply_bytes": [_vp, _i64, _int, _pi64, _vp],
     "invop_operator_create": [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, C.POINTER(_vp)],
     "invop_operator_factor": [_vp, _vp],
     "invop_operator_destroy": [_vp],

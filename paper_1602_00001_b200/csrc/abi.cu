@@ -63,6 +63,9 @@ extern "C" int invop_plan_destroy(invop_plan* p) {
   if (p->k3_ws) cudaFree(p->k3_ws);
   for (int b = 0; b < 2; ++b)
     if (p->k3_tiles[b]) cudaFree(p->k3_tiles[b]);
+  if (p->vw_data) cudaFree(p->vw_data);
+  if (p->vw_meta) cudaFree(p->vw_meta);
+  if (p->vw_rowptr) cudaFree(p->vw_rowptr);
   if (p->host_pinned) cudaFreeHost(p->host_pinned);
   delete p;
   return INVOP_OK;
@@ -114,10 +117,38 @@ extern "C" int invop_apply(const invop_plan* p, const void* x, int64_t ldx, void
       return apply_batched_launch(const_cast<invop_plan*>(p), (const float*)x,
                                   nrhs > 1 ? ldx : p->n, (float*)y, nrhs > 1 ? ldy : p->rows,
                                   nrhs, s);
+    // one right-hand side over long rows: variable-width chunk layout (VW)
+    const char* no_vw = getenv("INVOP_NO_VW");
+    if (nrhs == 1 && p->ld / 512 >= 16 && !(no_vw && *no_vw && *no_vw != '0')) {
+      invop_plan* mp = const_cast<invop_plan*>(p);
+      int rc = vw_build(mp, s);
+      if (rc == INVOP_OK) return apply_vw_launch(mp, (const float*)x, (float*)y, s);
+      if (rc != INVOP_E_UNSUPPORTED) return rc;
+    }
     return apply_fast_launch(p, (const float*)x, nrhs > 1 ? ldx : p->n, (float*)y,
                              nrhs > 1 ? ldy : p->rows, nrhs, s);
   }
   return fail(INVOP_E_VALUE, "unknown mode");
+}
+
+extern "C" int invop_plan_apply_bytes(invop_plan* p, int64_t nrhs, int mode, int64_t* bytes,
+                                      void* stream) {
+  // bytes of operator data one fast/ordered apply streams from HBM (the
+  // roofline numerator), building the lazily created layouts first
+  if (!p || !bytes) return fail(INVOP_E_VALUE, "NULL argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  const char* no_vw = getenv("INVOP_NO_VW");
+  if (mode == INVOP_MODE_FAST && nrhs == 1 && p->ld / 512 >= 16 &&
+      !(no_vw && *no_vw && *no_vw != '0')) {
+    int rc = vw_build(p, s);
+    if (rc == INVOP_OK) {
+      const int64_t nch = p->ld / 512, nchp = (nch + 1) & ~1;
+      *bytes = p->vw_bytes + p->rows * nchp * 8 + (p->rows + 1) * 8;
+      return INVOP_OK;
+    }
+  }
+  *bytes = (int64_t)p->P * p->rows * p->ld;
+  return INVOP_OK;
 }
 
 __global__ void k_f64_to_f32(const double* __restrict__ a, float* __restrict__ b, int64_t n) {

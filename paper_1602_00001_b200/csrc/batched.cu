@@ -114,6 +114,26 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db
           tmem_d),
       "l"(da), "l"(db), "r"(idesc), "r"(accumulate), "r"(0), "r"(0), "r"(0), "r"(0));
 }
+// warp-wide issue: every lane executes (operands stay warp-uniform, so they
+// live in uniform registers) and elect.sync picks the one issuing thread
+__device__ __forceinline__ void mma_i8_elect(uint32_t tmem_d, uint64_t da, uint64_t db,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}" ::"r"(
+          tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate), "r"(0), "r"(0), "r"(0), "r"(0));
+}
+__device__ __forceinline__ void mma_commit_elect(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+          bar)
+      : "memory");
+}
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    bar)
@@ -224,8 +244,11 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
       for (int kb = kb0; kb < kb1; ++kb) {
         k3_wait(smem_u32(&full[st]), ph);
         tc_fence_after();
-        if (lane == 0) {
+        {
+          // descriptors: one base per stage plus compile-time offsets (>> 4)
           const uint32_t sb = smem_u32(base + (size_t)st * STAGE);
+          const uint64_t dbase = desc_sw64(sb);
+          const uint32_t id_lo = idesc_i8(0), id_hi = idesc_i8(a.hi_signed);
 #pragma unroll
           for (int kk = 0; kk < K3_BK / 32; ++kk) {
 #pragma unroll
@@ -239,20 +262,20 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
                   // first product of weight w at the unit's first K step starts the accumulator
                   const bool first_pair = (p == (w < K3_ND ? 0 : w - K3_ND + 1));
                   const uint32_t acc = (kb > kb0 || kk > 0 || !first_pair) ? 1u : 0u;
-                  const uint64_t da = desc_sw64(sb + (ti * P + p) * K3_A_TILE + kk * 32);
-                  const uint64_t db = desc_sw64(sb + A_BYTES + l * K3_B_TILE + kk * 32);
-                  const uint32_t idesc = idesc_i8((p == P - 1) ? a.hi_signed : 0);
-                  mma_i8(tmem + (uint32_t)((ti * NACC + w) * K3_NR), da, db, idesc, acc);
+                  const uint64_t da = dbase + (uint64_t)(((ti * P + p) * K3_A_TILE + kk * 32) >> 4);
+                  const uint64_t db = dbase + (uint64_t)((A_BYTES + l * K3_B_TILE + kk * 32) >> 4);
+                  mma_i8_elect(tmem + (uint32_t)((ti * NACC + w) * K3_NR), da, db,
+                               (p == P - 1) ? id_hi : id_lo, acc);
                 }
               }
             }
           }
-          mma_commit(smem_u32(&empty[st]));   // stage free once these MMAs complete
+          mma_commit_elect(smem_u32(&empty[st]));   // stage free once these MMAs complete
         }
         __syncwarp();
         if (++st == STAGES) { st = 0; ph ^= 1; }
       }
-      if (lane == 0) mma_commit(smem_u32(&tfull));
+      mma_commit_elect(smem_u32(&tfull));
       __syncwarp();
     }
   } else {

@@ -36,6 +36,13 @@ struct invop_plan {
   // K3 (tensor-core batched apply): workspace and cached TMA descriptors
   void* k3_ws = nullptr; size_t k3_ws_bytes = 0;
   uint8_t* k3_tiles[2] = {nullptr, nullptr};   // tiled copy of planes 0/1
+  // VW layout (vw.cu): per (row, 512-column chunk) base + w-byte offsets
+  uint8_t* vw_data = nullptr;
+  void* vw_meta = nullptr;          // int2 [rows][nchp]: {base, off<<3 | w}
+  int64_t* vw_rowptr = nullptr;     // [rows+1], 512-byte units
+  int64_t vw_bytes = 0;
+  int vw_ready = 0;                 // 0 not built, 1 built, -1 not applicable
+  int vw_wmax = 0;
   alignas(64) unsigned char k3_mapA[2][128];
   int k3_maps_ready = 0;
 };
@@ -83,6 +90,8 @@ int apply_fast_launch(const invop_plan* p, const float* x, int64_t ldx, float* y
 bool batched_supported(const invop_plan* p, int64_t nrhs);
 int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, int64_t ldy,
                          int64_t nrhs, cudaStream_t s);
+int vw_build(invop_plan* p, cudaStream_t s);
+int apply_vw_launch(invop_plan* p, const float* x, float* y, cudaStream_t s);
 int apply_ordered_launch(const invop_plan* p, const double* x, int64_t ldx, double* y,
                          int64_t ldy, int64_t nrhs, cudaStream_t s);
 

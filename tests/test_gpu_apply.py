@@ -371,9 +371,14 @@ def test_config2_against_reference_outputs(invop, O, golden):
 @pytest.mark.parametrize("lo,hi", [(0, 250), (-120, 120), (0, 60000), (-30000, 30000),
                                    (0, 9_000_000), (-4_000_000, 4_000_000), (0, 16_000_000),
                                    (-2_000_000_000, 2_000_000_000)])
-def test_stream_kernel_long_rows(invop, O, lo, hi):
-    """Rows of >= 16 column steps take the bulk-copy streaming kernel (k2_stream)."""
+@pytest.mark.parametrize("layout", ["vw", "planes"])
+def test_stream_kernel_long_rows(invop, O, lo, hi, layout, monkeypatch):
+    """Rows of >= 16 column steps take the bulk-copy streaming kernels: k2_vw on
+    the variable-width chunk layout, or k2_stream on the byte planes."""
     import torch
+
+    if layout == "planes":
+        monkeypatch.setenv("INVOP_NO_VW", "1")
 
     N, rows = 8704, 300
     rng = np.random.default_rng(hi)
