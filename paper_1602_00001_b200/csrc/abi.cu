@@ -66,6 +66,7 @@ extern "C" int invop_plan_destroy(invop_plan* p) {
   if (p->vw_data) cudaFree(p->vw_data);
   if (p->vw_meta) cudaFree(p->vw_meta);
   if (p->vw_rowptr) cudaFree(p->vw_rowptr);
+  if (p->vw_slaboff) cudaFree(p->vw_slaboff);
   if (p->host_pinned) cudaFreeHost(p->host_pinned);
   delete p;
   return INVOP_OK;

@@ -40,6 +40,7 @@ struct invop_plan {
   uint8_t* vw_data = nullptr;
   void* vw_meta = nullptr;          // int2 [rows][nchp]: {base, off<<3 | w}
   int64_t* vw_rowptr = nullptr;     // [rows+1], 512-byte units
+  uint32_t* vw_slaboff = nullptr;   // [rows][nslabs+1] slab offsets within a row
   int64_t vw_bytes = 0;
   int vw_ready = 0;                 // 0 not built, 1 built, -1 not applicable
   int vw_wmax = 0;

@@ -70,11 +70,13 @@ __global__ void k_vw_stats(VwPlanes pl, int P, int is_signed, int64_t rows, int6
 
 // per row: chunk offsets (in 512 B units) and the row's payload size
 __global__ void k_vw_rowscan(int64_t rows, int nch, int nchp, int2* __restrict__ meta,
-                             int64_t* __restrict__ rowsize) {
+                             int64_t* __restrict__ rowsize, uint32_t* __restrict__ slaboff,
+                             int nslabs) {
   const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (r >= rows) return;
   uint32_t off = 0;
   for (int c = 0; c < nch; ++c) {
+    if (c % VW_SLABCH == 0) slaboff[r * (nslabs + 1) + c / VW_SLABCH] = off;
     int2 m = meta[r * nchp + c];
     const int w = m.y & 7;
     m.y = (int)((off << 3) | w);
@@ -82,6 +84,7 @@ __global__ void k_vw_rowscan(int64_t rows, int nch, int nchp, int2* __restrict__
     off += w;
   }
   for (int c = nch; c < nchp; ++c) meta[r * nchp + c] = make_int2(0, (int)(off << 3));
+  slaboff[r * (nslabs + 1) + nslabs] = off;
   rowsize[r] = off;
 }
 
@@ -134,6 +137,7 @@ struct VwArgs {
   const uint8_t* data;
   const int2* meta;
   const int64_t* rowptr;     // [rows+1], 512 B units
+  const uint32_t* slaboff;   // [rows][nslabs+1] chunk-payload offsets of each slab
   int64_t rows, n;
   int nch, nchp;
   double scale;
@@ -194,6 +198,13 @@ __global__ void __launch_bounds__((VW_CONS + 1) * 32, 1) k2_vw(VwArgs a) {
   const int64_t nrows = row_hi - row_lo;
   const int64_t units = nrows * a.nslabs;
 
+  // producer lookups (row start, slab offsets) staged once: no dependent
+  // global loads on the per-stage issue path
+  int64_t* s_rowptr = reinterpret_cast<int64_t*>(slot + nrows * VW_CONS);
+  uint32_t* s_slab = reinterpret_cast<uint32_t*>(s_rowptr + nrows);
+  for (int64_t i = threadIdx.x; i < nrows; i += blockDim.x) s_rowptr[i] = a.rowptr[row_lo + i];
+  for (int64_t i = threadIdx.x; i < nrows * (a.nslabs + 1); i += blockDim.x)
+    s_slab[i] = a.slaboff[row_lo * (a.nslabs + 1) + i];
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
       mbar_init(bar_s + 8 * i, 1);
@@ -216,16 +227,15 @@ __global__ void __launch_bounds__((VW_CONS + 1) * 32, 1) k2_vw(VwArgs a) {
         const int c0 = slab * VW_SLABCH;
         const int c1 = min(a.nch, c0 + VW_SLABCH);
         const int2* mrow = a.meta + r * a.nchp;
-        const uint32_t o0 = (uint32_t)mrow[c0].y >> 3;
-        const uint32_t o1 = c1 < a.nchp ? ((uint32_t)mrow[c1].y >> 3)
-                                        : (uint32_t)(a.rowptr[r + 1] - a.rowptr[r]);
+        const uint32_t o0 = s_slab[lr * (a.nslabs + 1) + slab];
+        const uint32_t o1 = s_slab[lr * (a.nslabs + 1) + slab + 1];
         const uint32_t pay = (o1 - o0) * VW_CH;
         const uint32_t mbytes = (uint32_t)(((c1 - c0) + 1) & ~1) * 8;
         const uint32_t sb = ring_s + st * a.stage_bytes;
         mbar_expect_tx(bar_s + 8 * st, mbytes + pay);
         bulk_g2s(sb, mrow + c0, mbytes, bar_s + 8 * st, policy);
         if (pay)
-          bulk_g2s(sb + VW_META, a.data + (a.rowptr[r] + o0) * VW_CH, pay, bar_s + 8 * st, policy);
+          bulk_g2s(sb + VW_META, a.data + (s_rowptr[lr] + o0) * VW_CH, pay, bar_s + 8 * st, policy);
         if (++st == S) { st = 0; ph ^= 1; }
         if (++lr == nrows) { lr = 0; ++slab; }
       }
@@ -363,11 +373,14 @@ int vw_build(invop_plan* p, cudaStream_t s) {
   INVOP_CUDA(cudaMalloc(&p->vw_rowptr, (size_t)(p->rows + 1) * sizeof(int64_t)));
   int64_t* rowsize = nullptr;
   INVOP_CUDA(cudaMalloc(&rowsize, (size_t)p->rows * sizeof(int64_t)));
+  const int nslabs = (nch + VW_SLABCH - 1) / VW_SLABCH;
+  INVOP_CUDA(cudaMalloc(&p->vw_slaboff, (size_t)p->rows * (nslabs + 1) * sizeof(uint32_t)));
   const int64_t warps = p->rows * nch;
   k_vw_stats<<<(unsigned)cdiv(warps * 32, 256), 256, 0, s>>>(pl, p->P, p->is_signed, p->rows,
                                                              p->ld, nch, nchp, (int2*)p->vw_meta);
   k_vw_rowscan<<<(unsigned)cdiv(p->rows, 256), 256, 0, s>>>(p->rows, nch, nchp,
-                                                            (int2*)p->vw_meta, rowsize);
+                                                            (int2*)p->vw_meta, rowsize,
+                                                            p->vw_slaboff, nslabs);
   k_vw_rowptr<<<1, 1024, 0, s>>>(p->rows, rowsize, p->vw_rowptr);
   int64_t total = 0;
   INVOP_CUDA(cudaMemcpyAsync(&total, p->vw_rowptr + p->rows, sizeof(int64_t),
@@ -393,6 +406,7 @@ int apply_vw_launch(invop_plan* p, const float* x, float* y, cudaStream_t s) {
   a.data = p->vw_data;
   a.meta = (const int2*)p->vw_meta;
   a.rowptr = p->vw_rowptr;
+  a.slaboff = p->vw_slaboff;
   a.rows = p->rows; a.n = p->n;
   a.nch = (int)(p->ld / VW_CH);
   a.nchp = (a.nch + 1) & ~1;
@@ -408,7 +422,8 @@ int apply_vw_launch(invop_plan* p, const float* x, float* y, cudaStream_t s) {
   a.xbits = std::max(8, std::min(22, 61 - vb - nb));
   int grid = (int)std::min<int64_t>(num_sms(), p->rows);
   const int64_t rows_per_cta = cdiv(p->rows, grid);
-  const size_t slot_bytes = (size_t)rows_per_cta * VW_CONS * sizeof(double);
+  const size_t slot_bytes = (size_t)rows_per_cta * VW_CONS * sizeof(double) +
+                            (size_t)rows_per_cta * 8 + (size_t)rows_per_cta * (a.nslabs + 1) * 4 + 16;
   const size_t budget = 225 * 1024;
   int stages = (int)((budget - slot_bytes - 256) / (a.stage_bytes + 16));
   stages = std::min(stages, 8);
