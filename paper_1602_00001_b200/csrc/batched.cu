@@ -88,11 +88,11 @@ __device__ __forceinline__ void k3_wait(uint32_t bar, uint32_t parity) {
       : "memory");
 }
 __device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, int x, int y,
-                                       uint32_t bar) {
+                                       uint32_t bar, uint64_t policy) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar), "l"(policy)
       : "memory");
 }
 // K-major operand tile, rows of 64 bytes, SWIZZLE_64B (8-row atoms of 512 B)
@@ -201,6 +201,11 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
+      // the operator streams through L2 once (evict first); the x digits are
+      // re-read by every row-tile pair and must stay L2-resident (evict last)
+      uint64_t pol_a, pol_b;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_a));
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_b));
       int st = 0;
       uint32_t ph = 0;
       int64_t it = 0;
@@ -219,12 +224,12 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
           for (int ti = 0; ti < TILES; ++ti) {
             // tiled planes: tile (rt, kb) starts at tensor row (rt*kblocks + kb)*128
             const int trow = (int)(((int64_t)(row0 / K3_BM + ti) * a.kb_stride + kb) * K3_BM);
-            tma_2d(sb + (ti * P + 0) * K3_A_TILE, &mapA0, 0, trow, fb);
-            if (P > 1) tma_2d(sb + (ti * P + 1) * K3_A_TILE, &mapA1, 0, trow, fb);
+            tma_2d(sb + (ti * P + 0) * K3_A_TILE, &mapA0, 0, trow, fb, pol_a);
+            if (P > 1) tma_2d(sb + (ti * P + 1) * K3_A_TILE, &mapA1, 0, trow, fb, pol_a);
           }
 #pragma unroll
           for (int l = 0; l < K3_ND; ++l)
-            tma_2d(sb + A_BYTES + l * K3_B_TILE, &mapB, kb * K3_BK, l * K3_NR, fb);
+            tma_2d(sb + A_BYTES + l * K3_B_TILE, &mapB, kb * K3_BK, l * K3_NR, fb, pol_b);
           if (++st == STAGES) { st = 0; ph ^= 1; }
         }
       }

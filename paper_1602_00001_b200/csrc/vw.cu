@@ -21,8 +21,8 @@
 namespace invop {
 
 constexpr int VW_CH = 512;                       // columns per chunk
-constexpr int VW_CONS = 8;                       // consumer warps
-constexpr int VW_SW = 4;                         // chunks per consumer per slab
+constexpr int VW_CONS = 16;                      // consumer warps
+constexpr int VW_SW = 2;                         // chunks per consumer per slab
 constexpr int VW_SLABCH = VW_CONS * VW_SW;       // 32 chunks per slab
 constexpr int VW_SLAB = VW_SLABCH * VW_CH;       // 16384 columns
 constexpr int VW_META = VW_SLABCH * 8;           // 256 B of metadata per stage
@@ -149,13 +149,20 @@ struct VwArgs {
   int xbits;                 // fixed-point bits of x (overflow-safe int64 sums)
 };
 
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 r;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "r"(addr));
+  return r;
+}
+
 template <int W>
-__device__ __forceinline__ long long vw_chunk_dot(const unsigned char* cp, int lane,
-                                                  const int32_t* X) {
+__device__ __forceinline__ long long vw_chunk_dot(uint32_t cp, const int32_t* X) {
   long long acc = 0, acc2 = 0;
   uint4 cw[W > 0 ? W : 1];
 #pragma unroll
-  for (int b = 0; b < W; ++b) cw[b] = *reinterpret_cast<const uint4*>(cp + b * VW_CH + lane * 16);
+  for (int b = 0; b < W; ++b) cw[b] = lds128(cp + b * VW_CH);
 #pragma unroll
   for (int w = 0; w < 4; ++w) {
     uint32_t wds[4];
@@ -292,6 +299,7 @@ __global__ void __launch_bounds__((VW_CONS + 1) * 32, 1) k2_vw(VwArgs a) {
       }
       mbar_wait(bar_s + 8 * st, ph);
       const unsigned char* sb = ring + (size_t)st * a.stage_bytes;
+      const uint32_t sb_s = ring_s + st * a.stage_bytes;
       const int2* sm = reinterpret_cast<const int2*>(sb);
       const uint32_t o0 = (uint32_t)sm[0].y >> 3;
       double part = 0.0;
@@ -302,13 +310,13 @@ __global__ void __launch_bounds__((VW_CONS + 1) * 32, 1) k2_vw(VwArgs a) {
           if (!stepv[t]) continue;                 // warp-uniform
           const int2 m = sm[wc + t * VW_CONS];
           const int w = m.y & 7;
-          const unsigned char* cp = sb + VW_META + (((uint32_t)m.y >> 3) - o0) * VW_CH;
+          const uint32_t cp = sb_s + VW_META + (((uint32_t)m.y >> 3) - o0) * VW_CH + lane * 16;
           acc += (long long)m.x * Xs[t];
           switch (w) {                             // warp-uniform
-            case 1: acc += vw_chunk_dot<1>(cp, lane, X[t]); break;
-            case 2: acc += vw_chunk_dot<2>(cp, lane, X[t]); break;
-            case 3: acc += vw_chunk_dot<3>(cp, lane, X[t]); break;
-            case 4: acc += vw_chunk_dot<4>(cp, lane, X[t]); break;
+            case 1: acc += vw_chunk_dot<1>(cp, X[t]); break;
+            case 2: acc += vw_chunk_dot<2>(cp, X[t]); break;
+            case 3: acc += vw_chunk_dot<3>(cp, X[t]); break;
+            case 4: acc += vw_chunk_dot<4>(cp, X[t]); break;
             default: break;
           }
         }
