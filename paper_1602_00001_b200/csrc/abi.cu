@@ -118,9 +118,10 @@ extern "C" int invop_apply(const invop_plan* p, const void* x, int64_t ldx, void
       return apply_batched_launch(const_cast<invop_plan*>(p), (const float*)x,
                                   nrhs > 1 ? ldx : p->n, (float*)y, nrhs > 1 ? ldy : p->rows,
                                   nrhs, s);
-    // one right-hand side over long rows: variable-width chunk layout (VW)
-    const char* no_vw = getenv("INVOP_NO_VW");
-    if (nrhs == 1 && p->ld / 512 >= 16 && !(no_vw && *no_vw && *no_vw != '0')) {
+    // one right-hand side over long rows: variable-width chunk layout (VW),
+    // opt-in (INVOP_VW=1) until it beats the plane-streaming kernel
+    const char* use_vw = getenv("INVOP_VW");
+    if (nrhs == 1 && p->ld / 512 >= 16 && use_vw && *use_vw && *use_vw != '0') {
       invop_plan* mp = const_cast<invop_plan*>(p);
       int rc = vw_build(mp, s);
       if (rc == INVOP_OK) return apply_vw_launch(mp, (const float*)x, (float*)y, s);
@@ -138,9 +139,9 @@ extern "C" int invop_plan_apply_bytes(invop_plan* p, int64_t nrhs, int mode, int
   // roofline numerator), building the lazily created layouts first
   if (!p || !bytes) return fail(INVOP_E_VALUE, "NULL argument");
   cudaStream_t s = (cudaStream_t)stream;
-  const char* no_vw = getenv("INVOP_NO_VW");
-  if (mode == INVOP_MODE_FAST && nrhs == 1 && p->ld / 512 >= 16 &&
-      !(no_vw && *no_vw && *no_vw != '0')) {
+  const char* use_vw = getenv("INVOP_VW");
+  if (mode == INVOP_MODE_FAST && nrhs == 1 && p->ld / 512 >= 16 && use_vw && *use_vw &&
+      *use_vw != '0') {
     int rc = vw_build(p, s);
     if (rc == INVOP_OK) {
       const int64_t nch = p->ld / 512, nchp = (nch + 1) & ~1;

@@ -377,8 +377,8 @@ def test_stream_kernel_long_rows(invop, O, lo, hi, layout, monkeypatch):
     the variable-width chunk layout, or k2_stream on the byte planes."""
     import torch
 
-    if layout == "planes":
-        monkeypatch.setenv("INVOP_NO_VW", "1")
+    if layout == "vw":
+        monkeypatch.setenv("INVOP_VW", "1")
 
     N, rows = 8704, 300
     rng = np.random.default_rng(hi)
