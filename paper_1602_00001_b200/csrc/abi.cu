@@ -67,6 +67,10 @@ extern "C" int invop_plan_destroy(invop_plan* p) {
   if (p->vw_meta) cudaFree(p->vw_meta);
   if (p->vw_rowptr) cudaFree(p->vw_rowptr);
   if (p->vw_slaboff) cudaFree(p->vw_slaboff);
+  if (p->tv_data) cudaFree(p->tv_data);
+  if (p->tv_meta) cudaFree(p->tv_meta);
+  if (p->tv_gptr) cudaFree(p->tv_gptr);
+  if (p->tv_ws) cudaFree(p->tv_ws);
   if (p->host_pinned) cudaFreeHost(p->host_pinned);
   delete p;
   return INVOP_OK;
@@ -88,6 +92,12 @@ extern "C" int invop_plan_info(const invop_plan* p, int64_t* n, int64_t* rows, i
 }
 
 static bool aligned16(const void* ptr) { return ((uintptr_t)ptr & 15u) == 0; }
+
+static bool layout_enabled(const char* env, bool dflt) {
+  const char* v = getenv(env);
+  if (!v || !*v) return dflt;
+  return *v != '0';
+}
 
 extern "C" int invop_apply(const invop_plan* p, const void* x, int64_t ldx, void* y,
                            int64_t ldy, int64_t nrhs, int dtype, int mode, void* stream) {
@@ -118,8 +128,14 @@ extern "C" int invop_apply(const invop_plan* p, const void* x, int64_t ldx, void
       return apply_batched_launch(const_cast<invop_plan*>(p), (const float*)x,
                                   nrhs > 1 ? ldx : p->n, (float*)y, nrhs > 1 ? ldy : p->rows,
                                   nrhs, s);
-    // one right-hand side over long rows: variable-width chunk layout (VW),
-    // opt-in (INVOP_VW=1) until it beats the plane-streaming kernel
+    // one right-hand side over long rows: tiled variable-width layout (TVW)
+    if (nrhs == 1 && p->ld / 512 >= 16 && layout_enabled("INVOP_TVW", true)) {
+      invop_plan* mp = const_cast<invop_plan*>(p);
+      int rc = tvw_build(mp, s);
+      if (rc == INVOP_OK) return apply_tvw_launch(mp, (const float*)x, (float*)y, s);
+      if (rc != INVOP_E_UNSUPPORTED) return rc;
+    }
+    // row-chunk variable-width layout (VW), opt-in (INVOP_VW=1)
     const char* use_vw = getenv("INVOP_VW");
     if (nrhs == 1 && p->ld / 512 >= 16 && use_vw && *use_vw && *use_vw != '0') {
       invop_plan* mp = const_cast<invop_plan*>(p);
@@ -139,6 +155,14 @@ extern "C" int invop_plan_apply_bytes(invop_plan* p, int64_t nrhs, int mode, int
   // roofline numerator), building the lazily created layouts first
   if (!p || !bytes) return fail(INVOP_E_VALUE, "NULL argument");
   cudaStream_t s = (cudaStream_t)stream;
+  if (mode == INVOP_MODE_FAST && nrhs == 1 && p->ld / 512 >= 16 &&
+      layout_enabled("INVOP_TVW", true)) {
+    int rc = tvw_build(p, s);
+    if (rc == INVOP_OK) {
+      *bytes = tvw_stream_bytes(p);
+      return INVOP_OK;
+    }
+  }
   const char* use_vw = getenv("INVOP_VW");
   if (mode == INVOP_MODE_FAST && nrhs == 1 && p->ld / 512 >= 16 && use_vw && *use_vw &&
       *use_vw != '0') {

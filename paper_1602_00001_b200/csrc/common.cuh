@@ -44,6 +44,13 @@ struct invop_plan {
   int64_t vw_bytes = 0;
   int vw_ready = 0;                 // 0 not built, 1 built, -1 not applicable
   int vw_wmax = 0;
+  // TVW layout (tvw.cu): per (32-row group, 64-column tile) base + w-byte offsets
+  uint8_t* tv_data = nullptr;
+  void* tv_meta = nullptr;          // int2 [groups][nt]: {base, off2KB<<3 | w}
+  int64_t* tv_gptr = nullptr;       // [groups+1], 2 KB units
+  int64_t tv_bytes = 0;
+  int tv_ready = 0, tv_wmax = 0;
+  void* tv_ws = nullptr; size_t tv_ws_bytes = 0; int64_t tv_ws_cnt_off = -1;
   alignas(64) unsigned char k3_mapA[2][128];
   int k3_maps_ready = 0;
 };
@@ -92,6 +99,9 @@ bool batched_supported(const invop_plan* p, int64_t nrhs);
 int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, int64_t ldy,
                          int64_t nrhs, cudaStream_t s);
 int vw_build(invop_plan* p, cudaStream_t s);
+int tvw_build(invop_plan* p, cudaStream_t s);
+int64_t tvw_stream_bytes(const invop_plan* p);
+int apply_tvw_launch(invop_plan* p, const float* x, float* y, cudaStream_t s);
 int apply_vw_launch(invop_plan* p, const float* x, float* y, cudaStream_t s);
 int apply_ordered_launch(const invop_plan* p, const double* x, int64_t ldx, double* y,
                          int64_t ldy, int64_t nrhs, cudaStream_t s);

@@ -371,12 +371,15 @@ def test_config2_against_reference_outputs(invop, O, golden):
 @pytest.mark.parametrize("lo,hi", [(0, 250), (-120, 120), (0, 60000), (-30000, 30000),
                                    (0, 9_000_000), (-4_000_000, 4_000_000), (0, 16_000_000),
                                    (-2_000_000_000, 2_000_000_000)])
-@pytest.mark.parametrize("layout", ["vw", "planes"])
+@pytest.mark.parametrize("layout", ["tvw", "vw", "planes"])
 def test_stream_kernel_long_rows(invop, O, lo, hi, layout, monkeypatch):
-    """Rows of >= 16 column steps take the bulk-copy streaming kernels: k2_vw on
-    the variable-width chunk layout, or k2_stream on the byte planes."""
+    """Rows of >= 16 column steps take the bulk-copy streaming kernels: k2_tvw on
+    the tiled variable-width layout (default), k2_vw on row chunks, or
+    k2_stream on the byte planes."""
     import torch
 
+    if layout != "tvw":
+        monkeypatch.setenv("INVOP_TVW", "0")
     if layout == "vw":
         monkeypatch.setenv("INVOP_VW", "1")
 
