@@ -395,7 +395,7 @@ def run_ours(args, world, rank, local):
             "roofline": {
                 "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
-                "kernel": (("k2_vw (variable-width chunks, %.3f B/entry)" % (op_bytes / (rows * N)))
+                "kernel": (("k2_tvw (tiled variable-width codes, %.3f B/entry)" % (op_bytes / (rows * N)))
                            if op_bytes != rows * plan_ld * code_bytes else "k2_stream<P=%d>" % code_bytes)
                           if k == 1 else ("k3_batched<P=%d> (tcgen05 kind::i8)" % code_bytes),
                 "kernel_ms": k_ms,

@@ -70,6 +70,7 @@ extern "C" int invop_plan_destroy(invop_plan* p) {
   if (p->tv_data) cudaFree(p->tv_data);
   if (p->tv_meta) cudaFree(p->tv_meta);
   if (p->tv_gptr) cudaFree(p->tv_gptr);
+  if (p->tv_soff) cudaFree(p->tv_soff);
   if (p->tv_ws) cudaFree(p->tv_ws);
   if (p->host_pinned) cudaFreeHost(p->host_pinned);
   delete p;

@@ -48,6 +48,7 @@ struct invop_plan {
   uint8_t* tv_data = nullptr;
   void* tv_meta = nullptr;          // int2 [groups][nt]: {base, off2KB<<3 | w}
   int64_t* tv_gptr = nullptr;       // [groups+1], 2 KB units
+  int64_t* tv_soff = nullptr;       // [groups][nst+1] stage boundary offsets
   int64_t tv_bytes = 0;
   int tv_ready = 0, tv_wmax = 0;
   void* tv_ws = nullptr; size_t tv_ws_bytes = 0; int64_t tv_ws_cnt_off = -1;

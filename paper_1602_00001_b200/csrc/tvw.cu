@@ -113,6 +113,18 @@ __global__ void k_tv_scan(int64_t groups, const int64_t* __restrict__ gsize,
   for (int64_t g = a0; g < a1; ++g) { gptr[g] = acc; acc += gsize[g]; }
 }
 
+// stage boundary table: absolute payload offset (2 KB units) at tiles 0, 8, 16, ...
+__global__ void k_tv_soff(int64_t groups, int nt, const int2* __restrict__ meta,
+                          const int64_t* __restrict__ gptr, int64_t* __restrict__ soff) {
+  const int nst = (nt + TV_CONS - 1) / TV_CONS;
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= groups * (nst + 1)) return;
+  const int64_t g = k / (nst + 1);
+  const int s = (int)(k - g * (nst + 1));
+  const int t = s * TV_CONS;
+  soff[k] = t < nt ? gptr[g] + ((uint32_t)meta[g * nt + t].y >> 3) : gptr[g + 1];
+}
+
 // one warp per (row group, tile): lane r writes row r's 64 offsets, swizzled
 __global__ void k_tv_write(TvPlanes pl, int P, int is_signed, int64_t rows, int64_t ld,
                            int64_t groups, int nt, const int2* __restrict__ meta,
@@ -180,6 +192,7 @@ struct TvArgs {
   const uint8_t* data;
   const int2* meta;          // [groups][nt]
   const int64_t* gptr;       // [groups+1], 2 KB units
+  const int64_t* soff;       // [groups][nst+1] absolute offsets at every 8-tile stage boundary
   const unsigned char* xrec; // [nt] x records
   int64_t rows;
   int64_t groups;
@@ -267,34 +280,45 @@ __global__ void __launch_bounds__((TV_CONS + 1) * 32, 1) k2_tvw(TvArgs a) {
 
   if (warp == TV_CONS) {
     // ------------------------------------------------------------ producer
-    if (lane == 0) {
-      uint64_t policy;
-      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
-      int st = 0;
-      uint32_t ph = 0;
-      int64_t it = 0;
-      for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
-        const int64_t g = u / a.parts;
-        const int part = (int)(u - g * a.parts);
-        const int t0 = part * a.tiles_per_part;
-        const int t1 = min(a.nt, t0 + a.tiles_per_part);
-        const int2* mg = a.meta + g * a.nt;
-        for (int ts = t0; ts < t1; ts += TV_CONS, ++it) {
-          if (it >= S) mbar_wait(bar_s + 8 * (S + st), ph ^ 1);
-          const int te = min(t1, ts + TV_CONS);
-          const uint32_t o0 = (uint32_t)mg[ts].y >> 3;
-          const uint32_t o1 = te < a.nt ? ((uint32_t)mg[te].y >> 3)
-                                        : (uint32_t)(a.gptr[g + 1] - a.gptr[g]);
-          const uint32_t pay = (o1 - o0) * TV_PLANE;
-          const uint32_t mbytes = (uint32_t)(((te - ts) + 1) & ~1) * 8;
-          const uint32_t xbytes = (uint32_t)(te - ts) * TV_XREC;
-          const uint32_t sb = ring_s + st * a.stage_bytes;
-          mbar_expect_tx(bar_s + 8 * st, mbytes + xbytes + pay);
-          bulk_g2s(sb, mg + ts, mbytes, bar_s + 8 * st, policy);
-          bulk_g2s(sb + 64, a.xrec + (int64_t)ts * TV_XREC, xbytes, bar_s + 8 * st, policy);
-          if (pay)
-            bulk_g2s(sb + a.payload_off, a.data + (a.gptr[g] + o0) * (int64_t)TV_PLANE, pay,
-                     bar_s + 8 * st, policy);
+    // The whole warp walks the units; per unit its lanes fetch the stage
+    // boundary offsets in one parallel load (no dependent global load per
+    // stage), lane 0 issues the copies.
+    uint64_t policy;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+    int st = 0;
+    uint32_t ph = 0;
+    int64_t it = 0;
+    const int nst = (a.nt + TV_CONS - 1) / TV_CONS;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+      const int64_t g = u / a.parts;
+      const int part = (int)(u - g * a.parts);
+      const int t0 = part * a.tiles_per_part;
+      const int t1 = min(a.nt, t0 + a.tiles_per_part);
+      const int2* mg = a.meta + g * a.nt;
+      const int k0 = t0 / TV_CONS, k1 = (t1 + TV_CONS - 1) / TV_CONS;   // stage range
+      for (int kc = k0; kc < k1; kc += 31) {
+        const int kn = min(31, k1 - kc);
+        // lane i holds the offset at stage boundary kc + i (i <= kn)
+        int64_t off = 0;
+        if (lane <= kn) off = a.soff[g * (nst + 1) + kc + lane];
+        for (int i = 0; i < kn; ++i, ++it) {
+          const int64_t o0 = __shfl_sync(0xffffffffu, off, i);
+          const int64_t o1 = __shfl_sync(0xffffffffu, off, i + 1);
+          if (lane == 0) {
+            const int ts = (kc + i) * TV_CONS;
+            const int te = min(t1, ts + TV_CONS);
+            if (it >= S) mbar_wait(bar_s + 8 * (S + st), ph ^ 1);
+            const uint32_t pay = (uint32_t)(o1 - o0) * TV_PLANE;
+            const uint32_t mbytes = (uint32_t)(((te - ts) + 1) & ~1) * 8;
+            const uint32_t xbytes = (uint32_t)(te - ts) * TV_XREC;
+            const uint32_t sb = ring_s + st * a.stage_bytes;
+            mbar_expect_tx(bar_s + 8 * st, mbytes + xbytes + pay);
+            bulk_g2s(sb, mg + ts, mbytes, bar_s + 8 * st, policy);
+            bulk_g2s(sb + 64, a.xrec + (int64_t)ts * TV_XREC, xbytes, bar_s + 8 * st, policy);
+            if (pay)
+              bulk_g2s(sb + a.payload_off, a.data + o0 * (int64_t)TV_PLANE, pay, bar_s + 8 * st,
+                       policy);
+          }
           if (++st == S) { st = 0; ph ^= 1; }
         }
       }
@@ -408,6 +432,11 @@ int tvw_build(invop_plan* p, cudaStream_t s) {
   INVOP_CUDA(cudaStreamSynchronize(s));
   cudaFree(gsize);
   p->tv_bytes = total * TV_PLANE;
+  const int nst = (nt + TV_CONS - 1) / TV_CONS;
+  INVOP_CUDA(cudaMalloc(&p->tv_soff, (size_t)groups * (nst + 1) * sizeof(int64_t)));
+  k_tv_soff<<<(unsigned)cdiv(groups * (nst + 1), 256), 256, 0, s>>>(groups, nt,
+                                                                    (const int2*)p->tv_meta,
+                                                                    p->tv_gptr, p->tv_soff);
   INVOP_CUDA(cudaMalloc(&p->tv_data, p->tv_bytes > 0 ? p->tv_bytes : 16));
   k_tv_write<<<(unsigned)cdiv(warps * 32, 256), 256, 0, s>>>(pl, p->P, p->is_signed, p->rows,
                                                              p->ld, groups, nt,
@@ -465,6 +494,7 @@ int apply_tvw_launch(invop_plan* p, const float* x, float* y, cudaStream_t s) {
   a.data = p->tv_data;
   a.meta = (const int2*)p->tv_meta;
   a.gptr = p->tv_gptr;
+  a.soff = p->tv_soff;
   a.xrec = xrec;
   a.rows = p->rows;
   a.groups = groups;
