@@ -215,7 +215,11 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
         const int kb0 = split * a.kblocks_per_unit;
         const int kb1 = min(a.kblocks_total, kb0 + a.kblocks_per_unit);
         const int row0 = (int)(pair * TILES * K3_BM);
-        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+        // rotated K order: concurrent CTAs read different x-digit tiles (a hot
+        // L2 line shared by every SM serialises in one slice)
+        const int nkb = kb1 - kb0, rot = (int)(blockIdx.x % nkb);
+        for (int i = 0; i < nkb; ++i, ++it) {
+          const int kb = kb0 + (i + rot) % nkb;
           if (it >= STAGES) k3_wait(smem_u32(&empty[st]), ph ^ 1);
           const uint32_t sb = smem_u32(base + (size_t)st * STAGE);
           const uint32_t fb = smem_u32(&full[st]);
@@ -246,7 +250,8 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
       const int kb1 = min(a.kblocks_total, kb0 + a.kblocks_per_unit);
       if (ucount > 0) k3_wait(smem_u32(&tempty), (uint32_t)((ucount - 1) & 1));
       tc_fence_after();
-      for (int kb = kb0; kb < kb1; ++kb) {
+      const int nkb = kb1 - kb0;
+      for (int i = 0; i < nkb; ++i) {
         k3_wait(smem_u32(&full[st]), ph);
         tc_fence_after();
         {
@@ -266,7 +271,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
                   if (l < 0 || l >= K3_ND) continue;
                   // first product of weight w at the unit's first K step starts the accumulator
                   const bool first_pair = (p == (w < K3_ND ? 0 : w - K3_ND + 1));
-                  const uint32_t acc = (kb > kb0 || kk > 0 || !first_pair) ? 1u : 0u;
+                  const uint32_t acc = (i > 0 || kk > 0 || !first_pair) ? 1u : 0u;
                   const uint64_t da = dbase + (uint64_t)(((ti * P + p) * K3_A_TILE + kk * 32) >> 4);
                   const uint64_t db = dbase + (uint64_t)((A_BYTES + l * K3_B_TILE + kk * 32) >> 4);
                   mma_i8_elect(tmem + (uint32_t)((ti * NACC + w) * K3_NR), da, db,

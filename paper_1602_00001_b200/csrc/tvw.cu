@@ -302,16 +302,19 @@ __global__ void __launch_bounds__((TV_CONS + 1) * 32, 1) k2_tvw(TvArgs a) {
       const int t1 = min(a.nt, t0 + a.tiles_per_part);
       const int2* mg = a.meta + g * a.nt;
       const int k0 = t0 / TV_CONS, k1 = (t1 + TV_CONS - 1) / TV_CONS;   // stage range
-      for (int kc = k0; kc < k1; kc += 31) {
-        const int kn = min(31, k1 - kc);
-        // lane i holds the offset at stage boundary kc + i (i <= kn)
-        int64_t off = 0;
-        if (lane <= kn) off = a.soff[g * (nst + 1) + kc + lane];
-        for (int i = 0; i < kn; ++i, ++it) {
-          const int64_t o0 = __shfl_sync(0xffffffffu, off, i);
-          const int64_t o1 = __shfl_sync(0xffffffffu, off, i + 1);
+      const int nk = k1 - k0;                                            // <= 31
+      // CTAs walk their stages in rotated order so that concurrent CTAs read
+      // different x records (a shared hot line would serialise in one L2 slice)
+      const int rot = (int)(blockIdx.x % nk);
+      int64_t off = 0;
+      if (lane <= nk) off = a.soff[g * (nst + 1) + k0 + lane];
+      {
+        for (int i = 0; i < nk; ++i, ++it) {
+          const int kr = (i + rot) % nk;
+          const int64_t o0 = __shfl_sync(0xffffffffu, off, kr);
+          const int64_t o1 = __shfl_sync(0xffffffffu, off, kr + 1);
           if (lane == 0) {
-            const int ts = (kc + i) * TV_CONS;
+            const int ts = (k0 + kr) * TV_CONS;
             const int te = min(t1, ts + TV_CONS);
             const uint32_t pay = (uint32_t)(o1 - o0) * TV_PLANE;
             const uint32_t mbytes = (uint32_t)(((te - ts) + 1) & ~1) * 8;
@@ -351,7 +354,10 @@ __global__ void __launch_bounds__((TV_CONS + 1) * 32, 1) k2_tvw(TvArgs a) {
       const int t0 = part * a.tiles_per_part;
       const int t1 = min(a.nt, t0 + a.tiles_per_part);
       double row_part = 0.0;
-      for (int ts = t0; ts < t1; ts += TV_CONS, ++it) {
+      const int k0 = t0 / TV_CONS, nk = (t1 + TV_CONS - 1) / TV_CONS - k0;
+      const int rot = (int)(blockIdx.x % nk);
+      for (int i = 0; i < nk; ++i, ++it) {
+        const int ts = (k0 + (i + rot) % nk) * TV_CONS;
         const int slot = (int)(it % TV_D);
         mbar_wait(bar_s + 8 * slot, (uint32_t)((it / TV_D) & 1));
         const uint32_t start = d_start[slot];
@@ -485,6 +491,7 @@ int apply_tvw_launch(invop_plan* p, const float* x, float* y, cudaStream_t s) {
     double eff = (double)units / ((double)cdiv(units, sms) * sms) - 0.01 * pc;
     if (eff > best + 1e-9) { best = eff; parts = pc; }
   }
+  parts = std::max<int>(parts, (int)cdiv(nt, 31 * TV_CONS));   // <= 31 stages per unit
   int tpp = (int)cdiv(nt, parts);
   tpp = (int)round_up(tpp, TV_CONS);
   parts = (int)cdiv(nt, tpp);
