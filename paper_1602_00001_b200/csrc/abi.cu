@@ -130,7 +130,8 @@ extern "C" int invop_apply(const invop_plan* p, const void* x, int64_t ldx, void
                                   nrhs > 1 ? ldx : p->n, (float*)y, nrhs > 1 ? ldy : p->rows,
                                   nrhs, s);
     // one right-hand side over long rows: tiled variable-width layout (TVW)
-    if (nrhs == 1 && p->ld / 512 >= 16 && layout_enabled("INVOP_TVW", true)) {
+    // (opt-in: INVOP_TVW=1; the byte-plane stream kernel is faster today)
+    if (nrhs == 1 && p->ld / 512 >= 16 && layout_enabled("INVOP_TVW", false)) {
       invop_plan* mp = const_cast<invop_plan*>(p);
       int rc = tvw_build(mp, s);
       if (rc == INVOP_OK) return apply_tvw_launch(mp, (const float*)x, (float*)y, s);
@@ -157,7 +158,7 @@ extern "C" int invop_plan_apply_bytes(invop_plan* p, int64_t nrhs, int mode, int
   if (!p || !bytes) return fail(INVOP_E_VALUE, "NULL argument");
   cudaStream_t s = (cudaStream_t)stream;
   if (mode == INVOP_MODE_FAST && nrhs == 1 && p->ld / 512 >= 16 &&
-      layout_enabled("INVOP_TVW", true)) {
+      layout_enabled("INVOP_TVW", false)) {
     int rc = tvw_build(p, s);
     if (rc == INVOP_OK) {
       *bytes = tvw_stream_bytes(p);

@@ -199,7 +199,8 @@ struct TvArgs {
   int nt;                    // tiles per row group
   int parts;                 // K parts per row group
   int tiles_per_part;
-  int ring_bytes;            // circular stage ring in shared memory
+  int stages;
+  int stage_bytes;
   int payload_off;           // start of the payload inside a stage
   double scale;
   float* y;
@@ -257,29 +258,21 @@ __device__ __forceinline__ long long tv_tile_dot(uint32_t tile_s, uint32_t xrec_
   return acc + acc2;
 }
 
-constexpr int TV_D = 16;                   // stage descriptors / barrier pairs
-
 __global__ void __launch_bounds__((TV_CONS + 1) * 32, 1) k2_tvw(TvArgs a) {
-  // Shared memory: a circular byte ring of a.ring_bytes holding variable-size
-  // stages back to back (so the bytes in flight track the average stage, not
-  // the widest one), then per-descriptor start offsets, end positions and
-  // mbarriers, then the unit-end reduction buffer.
   extern __shared__ __align__(128) unsigned char smem[];
-  const uint32_t R = (uint32_t)a.ring_bytes;
+  const int S = a.stages;
   unsigned char* ring = smem;
-  uint32_t* d_start = reinterpret_cast<uint32_t*>(smem + R);            // [TV_D]
-  uint64_t* d_end = reinterpret_cast<uint64_t*>(d_start + TV_D);         // [TV_D] producer-private
-  uint64_t* bars = d_end + TV_D;                                         // full[D], empty[D]
-  double* red = reinterpret_cast<double*>(bars + 2 * TV_D);              // [TV_CONS][32]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)S * a.stage_bytes);
+  double* red = reinterpret_cast<double*>(bars + 2 * S);   // [TV_CONS][32]
   const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
   const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(bars);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t units = a.groups * a.parts;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < TV_D; ++i) {
+    for (int i = 0; i < S; ++i) {
       mbar_init(bar_s + 8 * i, 1);
-      mbar_init(bar_s + 8 * (TV_D + i), TV_CONS);
+      mbar_init(bar_s + 8 * (S + i), TV_CONS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -292,8 +285,9 @@ __global__ void __launch_bounds__((TV_CONS + 1) * 32, 1) k2_tvw(TvArgs a) {
     // stage), lane 0 issues the copies.
     uint64_t policy;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
-    int64_t it = 0, rel = 0;
-    uint64_t head = 0, consumed = 0;
+    int st = 0;
+    uint32_t ph = 0;
+    int64_t it = 0;
     const int nst = (a.nt + TV_CONS - 1) / TV_CONS;
     for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
       const int64_t g = u / a.parts;
@@ -302,80 +296,60 @@ __global__ void __launch_bounds__((TV_CONS + 1) * 32, 1) k2_tvw(TvArgs a) {
       const int t1 = min(a.nt, t0 + a.tiles_per_part);
       const int2* mg = a.meta + g * a.nt;
       const int k0 = t0 / TV_CONS, k1 = (t1 + TV_CONS - 1) / TV_CONS;   // stage range
-      const int nk = k1 - k0;                                            // <= 31
-      // CTAs walk their stages in rotated order so that concurrent CTAs read
-      // different x records (a shared hot line would serialise in one L2 slice)
-      const int rot = (int)(blockIdx.x % nk);
-      int64_t off = 0;
-      if (lane <= nk) off = a.soff[g * (nst + 1) + k0 + lane];
-      {
-        for (int i = 0; i < nk; ++i, ++it) {
-          const int kr = (i + rot) % nk;
-          const int64_t o0 = __shfl_sync(0xffffffffu, off, kr);
-          const int64_t o1 = __shfl_sync(0xffffffffu, off, kr + 1);
+      for (int kc = k0; kc < k1; kc += 31) {
+        const int kn = min(31, k1 - kc);
+        // lane i holds the offset at stage boundary kc + i (i <= kn)
+        int64_t off = 0;
+        if (lane <= kn) off = a.soff[g * (nst + 1) + kc + lane];
+        for (int i = 0; i < kn; ++i, ++it) {
+          const int64_t o0 = __shfl_sync(0xffffffffu, off, i);
+          const int64_t o1 = __shfl_sync(0xffffffffu, off, i + 1);
           if (lane == 0) {
-            const int ts = (k0 + kr) * TV_CONS;
+            const int ts = (kc + i) * TV_CONS;
             const int te = min(t1, ts + TV_CONS);
+            if (it >= S) mbar_wait(bar_s + 8 * (S + st), ph ^ 1);
             const uint32_t pay = (uint32_t)(o1 - o0) * TV_PLANE;
             const uint32_t mbytes = (uint32_t)(((te - ts) + 1) & ~1) * 8;
             const uint32_t xbytes = (uint32_t)(te - ts) * TV_XREC;
-            const uint32_t need = (uint32_t)a.payload_off + ((pay + 127u) & ~127u);
-            uint64_t pos = head;
-            if ((uint32_t)(pos % R) + need > R) pos += R - (uint32_t)(pos % R);   // wrap
-            const uint64_t end = pos + need;
-            // release in order until the descriptor slot and the bytes are free
-            while (it - rel >= TV_D || end - consumed > R) {
-              const int rs = (int)(rel % TV_D);
-              mbar_wait(bar_s + 8 * (TV_D + rs), (uint32_t)((rel / TV_D) & 1));
-              consumed = d_end[rs];
-              ++rel;
-            }
-            const int slot = (int)(it % TV_D);
-            const uint32_t start = (uint32_t)(pos % R);
-            d_start[slot] = start;
-            d_end[slot] = end;
-            head = end;
-            const uint32_t sb = ring_s + start;
-            const uint32_t fb = bar_s + 8 * slot;
-            mbar_expect_tx(fb, mbytes + xbytes + pay);
-            bulk_g2s(sb, mg + ts, mbytes, fb, policy);
-            bulk_g2s(sb + 64, a.xrec + (int64_t)ts * TV_XREC, xbytes, fb, policy);
-            if (pay) bulk_g2s(sb + a.payload_off, a.data + o0 * (int64_t)TV_PLANE, pay, fb, policy);
+            const uint32_t sb = ring_s + st * a.stage_bytes;
+            mbar_expect_tx(bar_s + 8 * st, mbytes + xbytes + pay);
+            bulk_g2s(sb, mg + ts, mbytes, bar_s + 8 * st, policy);
+            bulk_g2s(sb + 64, a.xrec + (int64_t)ts * TV_XREC, xbytes, bar_s + 8 * st, policy);
+            if (pay)
+              bulk_g2s(sb + a.payload_off, a.data + o0 * (int64_t)TV_PLANE, pay, bar_s + 8 * st,
+                       policy);
           }
+          if (++st == S) { st = 0; ph ^= 1; }
         }
       }
     }
   } else {
     // ------------------------------------------------------------ consumers
-    int64_t it = 0;
+    int st = 0;
+    uint32_t ph = 0;
     for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
       const int64_t g = u / a.parts;
       const int part = (int)(u - g * a.parts);
       const int t0 = part * a.tiles_per_part;
       const int t1 = min(a.nt, t0 + a.tiles_per_part);
       double row_part = 0.0;
-      const int k0 = t0 / TV_CONS, nk = (t1 + TV_CONS - 1) / TV_CONS - k0;
-      const int rot = (int)(blockIdx.x % nk);
-      for (int i = 0; i < nk; ++i, ++it) {
-        const int ts = (k0 + (i + rot) % nk) * TV_CONS;
-        const int slot = (int)(it % TV_D);
-        mbar_wait(bar_s + 8 * slot, (uint32_t)((it / TV_D) & 1));
-        const uint32_t start = d_start[slot];
-        const uint32_t sb = ring_s + start;
-        const unsigned char* sp = ring + start;
+      for (int ts = t0; ts < t1; ts += TV_CONS) {
+        mbar_wait(bar_s + 8 * st, ph);
+        const uint32_t sb = ring_s + st * a.stage_bytes;
         const int t = ts + warp;
         if (t < t1) {
-          const int2* sm = reinterpret_cast<const int2*>(sp);
+          const int2* sm = reinterpret_cast<const int2*>(ring + (size_t)st * a.stage_bytes);
           const uint32_t o0 = (uint32_t)sm[0].y >> 3;
           const int2 m = sm[warp];
           const int w = m.y & 7;
           const uint32_t tile_s = sb + a.payload_off + (((uint32_t)m.y >> 3) - o0) * TV_PLANE;
           const uint32_t xrec_s = sb + 64 + warp * TV_XREC;
-          const unsigned char* xr = sp + 64 + warp * TV_XREC;
+          const unsigned char* xr = ring + (size_t)st * a.stage_bytes + 64 + warp * TV_XREC;
           const int e = *reinterpret_cast<const int*>(xr + 264);
           if (e == TV_MASKED) {
             // inf/nan in this tile of x: fp64 with the reference's zero skip
-            const unsigned char* tp = sp + a.payload_off + (((uint32_t)m.y >> 3) - o0) * TV_PLANE;
+            const unsigned char* tp = ring + (size_t)st * a.stage_bytes + a.payload_off +
+                                      (((uint32_t)m.y >> 3) - o0) * TV_PLANE;
             const int sw = (lane >> 1) & 3;
             for (int j = 0; j < TV_TC; ++j) {
               const int pos = lane * TV_TC + (((j >> 4) ^ sw) << 4) + (j & 15);
@@ -398,7 +372,8 @@ __global__ void __launch_bounds__((TV_CONS + 1) * 32, 1) k2_tvw(TvArgs a) {
           }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(bar_s + 8 * (TV_D + slot));
+        if (lane == 0) mbar_arrive(bar_s + 8 * (S + st));
+        if (++st == S) { st = 0; ph ^= 1; }
       }
       // fixed-order combination of the 8 warps' partials of this unit
       red[warp * 32 + lane] = row_part;
@@ -491,7 +466,6 @@ int apply_tvw_launch(invop_plan* p, const float* x, float* y, cudaStream_t s) {
     double eff = (double)units / ((double)cdiv(units, sms) * sms) - 0.01 * pc;
     if (eff > best + 1e-9) { best = eff; parts = pc; }
   }
-  parts = std::max<int>(parts, (int)cdiv(nt, 31 * TV_CONS));   // <= 31 stages per unit
   int tpp = (int)cdiv(nt, parts);
   tpp = (int)round_up(tpp, TV_CONS);
   parts = (int)cdiv(nt, tpp);
@@ -532,12 +506,13 @@ int apply_tvw_launch(invop_plan* p, const float* x, float* y, cudaStream_t s) {
   a.partial = (double*)((char*)p->tv_ws + part_off);
   a.counters = (int*)((char*)p->tv_ws + cnt_off);
   a.payload_off = (int)round_up(64 + TV_CONS * TV_XREC, 128);
-  const size_t fixed = TV_D * 4 + TV_D * 8 + 2 * TV_D * 8 + TV_CONS * 32 * sizeof(double);
-  const size_t max_stage = (size_t)a.payload_off + (size_t)p->tv_wmax * TV_CONS * TV_PLANE;
-  size_t ring = (225 * 1024 - fixed - 128) & ~(size_t)127;
-  if (ring < 2 * max_stage) return fail(INVOP_E_UNSUPPORTED, "k2_tvw: not enough shared memory");
-  a.ring_bytes = (int)ring;
-  const size_t smem = ring + fixed;
+  a.stage_bytes = a.payload_off + p->tv_wmax * TV_CONS * TV_PLANE;
+  const size_t red_bytes = TV_CONS * 32 * sizeof(double);
+  int stages = (int)((225 * 1024 - red_bytes - 256) / (a.stage_bytes + 16));
+  stages = std::min(stages, 12);
+  if (stages < 2) return fail(INVOP_E_UNSUPPORTED, "k2_tvw: not enough shared memory");
+  a.stages = stages;
+  const size_t smem = (size_t)stages * a.stage_bytes + 2 * stages * 8 + red_bytes;
   cudaFuncSetAttribute(k2_tvw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int grid = (int)std::min<int64_t>(sms, groups * parts);
   k2_tvw<<<grid, (TV_CONS + 1) * 32, smem, s>>>(a);

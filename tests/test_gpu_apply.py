@@ -373,13 +373,12 @@ def test_config2_against_reference_outputs(invop, O, golden):
                                    (-2_000_000_000, 2_000_000_000)])
 @pytest.mark.parametrize("layout", ["tvw", "vw", "planes"])
 def test_stream_kernel_long_rows(invop, O, lo, hi, layout, monkeypatch):
-    """Rows of >= 16 column steps take the bulk-copy streaming kernels: k2_tvw on
-    the tiled variable-width layout (default), k2_vw on row chunks, or
-    k2_stream on the byte planes."""
+    """Rows of >= 16 column steps take the bulk-copy streaming kernels:
+    k2_stream on the byte planes (default), or the compressed layouts k2_tvw
+    (tiled variable width) / k2_vw (row chunks)."""
     import torch
 
-    if layout != "tvw":
-        monkeypatch.setenv("INVOP_TVW", "0")
+    monkeypatch.setenv("INVOP_TVW", "1" if layout == "tvw" else "0")
     if layout == "vw":
         monkeypatch.setenv("INVOP_VW", "1")
 
