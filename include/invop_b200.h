@@ -110,6 +110,15 @@ int invop_plan_counts(invop_plan* plan, int64_t* mults, int64_t* adds, void* str
 int invop_plan_column_stats(invop_plan* plan, int64_t* distinct, int64_t* nonzero,
                             void* stream);
 
+/* f1 — compressed on-disk format (reference IVOP files store int64
+   mantissas, cache.py:67-115): copy the byte planes out to host memory
+   (P planes of rows*n bytes, plane-major, row-major; synchronous) and build a
+   plan back from them. */
+int invop_plan_get_planes(const invop_plan* plan, uint8_t* host, void* stream);
+int invop_plan_from_planes(const uint8_t* host, int code_bytes, int is_signed, int64_t rows,
+                           int64_t n, int64_t row0, int scale_digits, void* stream,
+                           invop_plan** out);
+
 /* A2/A3 — expand codes back to int64 mantissas (device [rows x n], ldm). */
 int invop_plan_decode(const invop_plan* plan, int64_t* mant, int64_t ldm, void* stream);
 

@@ -23,6 +23,7 @@ from .applyplan import (
     build_plan,
     predict_direct_costs,
 )
+from .cache import CacheEntry, entry_for, read_matrix, read_vector, write_matrix, write_vector
 from .counting import OpCounters
 from .dense import PIVOT_RTOL, DenseMatrix, DeviceOperator, apply_dense, invert, residual_check
 from .errors import (
@@ -66,7 +67,8 @@ def quantized_inverse(stencil, digits: int, row0: int = 0, rows: int = None) -> 
 
 
 __all__ = [
-    "BACKEND", "ApplyPlan", "CacheError", "CapacityError", "CoefficientField", "CostPrediction",
+    "BACKEND", "ApplyPlan", "CacheEntry", "CacheError", "entry_for", "read_matrix", "read_vector",
+    "write_matrix", "write_vector", "CapacityError", "CoefficientField", "CostPrediction",
     "DegenerateProblemError", "DenseMatrix", "DeviceOperator", "Grid2D", "InvopError",
     "MANTISSA_LIMIT", "MAX_DENSE_N", "MantissaOverflowError", "OpCounters", "OperatorMatrix",
     "PIVOT_RTOL", "QuantizedMatrix", "SingularMatrixError", "SourceField", "StencilOperator",

@@ -697,3 +697,71 @@ extern "C" int invop_plan_csc(invop_plan* p, int64_t* col_ptr, int64_t* group_ab
   if (e != cudaSuccess) return cuda_fail(e, "csc tables");
   return INVOP_OK;
 }
+
+// ------------------------------------------------------------------ plane I/O
+// (next row f1 of SURVEY 8(f): the compressed on-disk format stores the byte
+// planes themselves, P bytes per entry instead of the reference's 8)
+__global__ void k_stats_planes(Planes pl, int P, int is_signed, int64_t rows, int64_t n,
+                               int64_t ld, long long* stats) {
+  int64_t mn = INT64_MAX, mx = INT64_MIN, nz = 0;
+  const int64_t total = rows * n;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = k / n, j = k - i * n;
+    const int64_t v = load_code(pl, P, is_signed, i * ld + j);
+    mn = min(mn, v); mx = max(mx, v); nz += (v != 0);
+  }
+  block_stats_commit(mn, mx, nz, stats);
+}
+
+extern "C" int invop_plan_get_planes(const invop_plan* p, uint8_t* host, void* stream) {
+  if (!p || (!host && p->rows * p->n > 0)) return fail(INVOP_E_VALUE, "NULL argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  for (int b = 0; b < p->P; ++b)
+    if (p->rows > 0 && p->n > 0)
+      INVOP_CUDA(cudaMemcpy2DAsync(host + (size_t)b * p->rows * p->n, (size_t)p->n, p->planes[b],
+                                   (size_t)p->ld, (size_t)p->n, (size_t)p->rows,
+                                   cudaMemcpyDeviceToHost, s));
+  INVOP_CUDA(cudaStreamSynchronize(s));
+  return INVOP_OK;
+}
+
+extern "C" int invop_plan_from_planes(const uint8_t* host, int P, int is_signed, int64_t rows,
+                                      int64_t n, int64_t row0, int scale_digits, void* stream,
+                                      invop_plan** out) {
+  if (!out) return fail(INVOP_E_VALUE, "out is NULL");
+  *out = nullptr;
+  if (P < 1 || P > INVOP_MAX_PLANES) return fail(INVOP_E_VALUE, "code width must be 1..8 bytes");
+  if (n < 0 || rows < 0 || row0 < 0 || row0 + rows > n) return fail(INVOP_E_VALUE, "bad plan geometry");
+  if (scale_digits < 0 || scale_digits > 22) return fail(INVOP_E_VALUE, "bad scale digits");
+  cudaStream_t s = (cudaStream_t)stream;
+  invop_plan* p = new_plan(rows, n, row0, scale_digits);
+  int rc = plan_alloc_planes(p, P);
+  if (rc) { invop_plan_destroy(p); return rc; }
+  p->is_signed = is_signed ? 1 : 0;
+  for (int b = 0; b < P; ++b) {
+    if (cudaMemsetAsync(p->planes[b], 0, (size_t)p->rows * p->ld, s) != cudaSuccess ||
+        (rows > 0 && n > 0 &&
+         cudaMemcpy2DAsync(p->planes[b], (size_t)p->ld, host + (size_t)b * rows * n, (size_t)n,
+                           (size_t)n, (size_t)rows, cudaMemcpyHostToDevice, s) != cudaSuccess)) {
+      invop_plan_destroy(p);
+      return fail(INVOP_E_CUDA, "plane upload");
+    }
+  }
+  long long* d_stats = nullptr;
+  if (cudaMalloc(&d_stats, 3 * sizeof(long long)) != cudaSuccess) {
+    invop_plan_destroy(p);
+    return fail(INVOP_E_CUDA, "cudaMalloc stats");
+  }
+  rc = init_stats(d_stats, s);
+  if (!rc && rows * n > 0)
+    k_stats_planes<<<grid_for(rows * n), 256, 0, s>>>(planes_of(p), P, p->is_signed, rows, n,
+                                                     p->ld, d_stats);
+  long long h[3] = {0, 0, 0};
+  if (!rc) rc = read_stats(d_stats, h, s);
+  cudaFree(d_stats);
+  if (rc) { invop_plan_destroy(p); return rc; }
+  plan_finalize_width(p, h[0], h[1], h[2]);
+  *out = p;
+  return INVOP_OK;
+}
