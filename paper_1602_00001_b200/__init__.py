@@ -49,6 +49,15 @@ from .grid import (
     uniform_interior,
     variable_interior,
 )
+from .harness import (
+    ErrorRow,
+    ScalingReport,
+    ScalingRow,
+    emit_csv,
+    relative_error,
+    run_scaling,
+    run_table1,
+)
 from .iterative import predict_iterations, predict_iterative_total
 from .quant import MANTISSA_LIMIT, QuantizedMatrix, dequantize, quantize, sparsity_stats
 
@@ -76,5 +85,6 @@ __all__ = [
     "assemble_rhs", "build_plan", "build_uniform", "build_variable", "dequantize", "invert",
     "predict_direct_costs", "predict_iterations", "predict_iterative_total", "quantize",
     "quantized_inverse", "residual_check", "sparsity_stats", "test_source", "uniform_interior",
-    "variable_interior",
+    "variable_interior", "ErrorRow", "ScalingReport", "ScalingRow", "emit_csv", "relative_error",
+    "run_scaling", "run_table1",
 ]
