@@ -211,6 +211,44 @@ __global__ void k_colstats_bitmap(Planes pl, int P, int is_signed, int64_t rows,
   }
 }
 
+// Global-memory bitmap path (large magnitudes, any row count): columns are
+// processed in chunks whose bitmaps fit a bounded scratch buffer.
+__global__ void k_colstats_gset(Planes pl, int P, int is_signed, int64_t rows, int64_t ld,
+                                int64_t j0, int C, int64_t words_per_col,
+                                uint32_t* __restrict__ bm, unsigned long long* __restrict__ nz) {
+  const int64_t total = rows * C;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = k / C;
+    const int c = (int)(k - i * C);
+    const int64_t v = load_code(pl, P, is_signed, i * ld + j0 + c);
+    if (v != 0) {
+      const uint64_t a = (uint64_t)(v < 0 ? -v : v);
+      atomicOr(&bm[c * words_per_col + (a >> 5)], 1u << (a & 31));
+      atomicAdd(&nz[c], 1ull);
+    }
+  }
+}
+
+__global__ void k_colstats_gcount(const uint32_t* __restrict__ bm, int64_t words_per_col,
+                                  const unsigned long long* __restrict__ nz, int64_t j0, int C,
+                                  int64_t* __restrict__ distinct, int64_t* __restrict__ nonzero) {
+  const int c = blockIdx.x;
+  if (c >= C) return;
+  int64_t cnt = 0;
+  for (int64_t w = threadIdx.x; w < words_per_col; w += blockDim.x) cnt += __popc(bm[c * words_per_col + w]);
+  __shared__ int64_t s[32];
+  cnt = warp_sum64(cnt);
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t t = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += s[i];
+    distinct[j0 + c] = t;
+    nonzero[j0 + c] = (int64_t)nz[c];
+  }
+}
+
 // Sort path (any magnitude, n <= 16384): one CTA per column sorts the
 // (|v|, row) pairs of the column with a shared-memory bitonic sort. It also
 // emits the reference CSC group tables when `emit` is set.
@@ -606,8 +644,29 @@ static int column_stats(invop_plan* p, int64_t* distinct, int64_t* nonzero, cuda
     INVOP_CHECK_LAUNCH("col_sort");
     return INVOP_OK;
   }
+  if (words * 4 <= ((int64_t)1 << 30)) {
+    // global bitmaps, <= 1 GB of scratch per pass
+    const int C = (int)std::max<int64_t>(1, std::min<int64_t>(4096, (((int64_t)1 << 30) / (words * 4))));
+    uint32_t* bm = nullptr;
+    unsigned long long* nz = nullptr;
+    INVOP_CUDA(cudaMalloc(&bm, (size_t)C * words * 4));
+    INVOP_CUDA(cudaMalloc(&nz, (size_t)C * 8));
+    for (int64_t j0 = 0; j0 < p->n; j0 += C) {
+      const int c = (int)std::min<int64_t>(C, p->n - j0);
+      INVOP_CUDA(cudaMemsetAsync(bm, 0, (size_t)c * words * 4, s));
+      INVOP_CUDA(cudaMemsetAsync(nz, 0, (size_t)c * 8, s));
+      k_colstats_gset<<<grid_for(p->rows * c), 256, 0, s>>>(planes_of(p), p->P, p->is_signed,
+                                                            p->rows, p->ld, j0, c, words, bm, nz);
+      k_colstats_gcount<<<c, 256, 0, s>>>(bm, words, nz, j0, c, distinct, nonzero);
+    }
+    cudaError_t e = cudaStreamSynchronize(s);
+    cudaFree(bm);
+    cudaFree(nz);
+    if (e != cudaSuccess) return cuda_fail(e, "colstats (global bitmaps)");
+    return INVOP_OK;
+  }
   return fail(INVOP_E_CAPACITY,
-              "distinct-value statistics need max|mantissa| < 1.6e6 or at most 16384 rows");
+              "distinct-value statistics need max|mantissa| < 2^35 or at most 16384 rows");
 }
 
 extern "C" int invop_plan_column_stats(invop_plan* p, int64_t* distinct, int64_t* nonzero,
