@@ -480,6 +480,7 @@ static int launch_stream_p(const invop_plan* p, const float* x, float* y, cudaSt
   const size_t budget = 225 * 1024;
   int stages = (int)((budget - slot_bytes - 256) / (a.stage_bytes + 16));
   stages = std::min(stages, 8);
+  if (const char* v = getenv("INVOP_ST_STAGES")) stages = std::max(2, std::min(stages, atoi(v)));
   if (stages < 2) return fail(INVOP_E_UNSUPPORTED, "k2_stream: not enough shared memory");
   a.stages = stages;
   size_t smem = (size_t)stages * a.stage_bytes + 2 * stages * 8 + slot_bytes;
