@@ -690,43 +690,75 @@ __global__ void __launch_bounds__(128) k2_ordered(OrdArgs a) {
 #pragma unroll
       for (int i = 0; i < 4; ++i) fin = fin && isfinite(xs[k * ORD_TILE + lane * 4 + i]);
     const bool masked = __any_sync(0xffffffffu, !fin);
-#pragma unroll 1
+    // All 8 chunks of the tile unrolled, so the independent decode / product
+    // work of chunk c+1 overlaps the ordered DADD chain of chunk c.
+    // For finite x, adding (0*10^-m)*x_j = +-0 leaves the accumulator bitwise
+    // unchanged (it starts at +0 and x+(-x) rounds to +0), so the reference's
+    // zero skip only matters when the tile holds inf/nan: then the product of
+    // a zero code is replaced by +0.
+#pragma unroll
     for (int c = 0; c < 8; ++c) {
-      if (c * 16 >= cend) break;
-      uint4 w[P];
+      if (c * 16 < cend) {
+        uint4 w[P];
 #pragma unroll
-      for (int b = 0; b < P; ++b)
-        w[b] = *reinterpret_cast<const uint4*>(sb + b * CODE_BYTES + sr * 128 +
-                                               ((c ^ (sr & 7)) << 4));
-      // all 16 products first (independent), then the ordered fp64 chain.
-      // For finite x, adding (0*10^-m)*x_j = +-0 leaves the accumulator
-      // bitwise unchanged (it starts at +0 and x+(-x) rounds to +0), so the
-      // reference's zero skip only matters when the tile holds inf/nan: then
-      // the product of a zero code is replaced by +0.
-      double d[16];
+        for (int b = 0; b < P; ++b)
+          w[b] = *reinterpret_cast<const uint4*>(sb + b * CODE_BYTES + sr * 128 +
+                                                 ((c ^ (sr & 7)) << 4));
+        double d[16];
+        if constexpr (P <= 4) {
+          // PRMT-assembled int32 codes, exact conversion by the 2^52 magic
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        uint8_t bytes[P];
+          for (int wd = 0; wd < 4; ++wd) {
+            uint32_t wds[4];
 #pragma unroll
-        for (int b = 0; b < P; ++b) bytes[b] = (uint8_t)(u4get(w[b], q >> 2) >> (8 * (q & 3)));
-        d[q] = __dmul_rn(code_to_double<P, SIGNED>(bytes), a.scale);
-      }
+            for (int b = 0; b < P; ++b) wds[b] = u4get(w[b], wd);
+            int32_t uv[4];
+            if (P == 4 && !SIGNED) {
+              const uint32_t t01 = prmt(wds[0], wds[1], 0x5140), t23 = prmt(wds[0], wds[1], 0x7362);
+              const uint32_t h01 = prmt(wds[P > 2 ? 2 : 0], wds[P > 3 ? 3 : 0], 0x5140);
+              const uint32_t h23 = prmt(wds[P > 2 ? 2 : 0], wds[P > 3 ? 3 : 0], 0x7362);
+              uv[0] = (int32_t)prmt(t01, h01, 0x5410); uv[1] = (int32_t)prmt(t01, h01, 0x7632);
+              uv[2] = (int32_t)prmt(t23, h23, 0x5410); uv[3] = (int32_t)prmt(t23, h23, 0x7632);
+            } else {
+              dec_int4<P, SIGNED>(wds, uv);
+            }
 #pragma unroll
-      for (int k = 0; k < KR; ++k) {
-        const double2* xk = reinterpret_cast<const double2*>(xs + k * ORD_TILE + c * 16);
-        double t[16];
+            for (int i = 0; i < 4; ++i) {
+              double v;
+              if (SIGNED)   // 2^52 + 2^51 + (s + 2^31) - (2^52 + 2^51 + 2^31)
+                v = __dadd_rn(__hiloint2double(0x43380000, (int)((uint32_t)uv[i] ^ 0x80000000u)),
+                              -6755401588539392.0);
+              else          // 2^52 + u - 2^52
+                v = __dadd_rn(__hiloint2double(0x43300000, uv[i]), -4503599627370496.0);
+              d[4 * wd + i] = __dmul_rn(v, a.scale);
+            }
+          }
+        } else {
 #pragma unroll
-        for (int q2 = 0; q2 < 8; ++q2) {
-          double2 xv = xk[q2];
-          t[2 * q2] = __dmul_rn(d[2 * q2], xv.x);
-          t[2 * q2 + 1] = __dmul_rn(d[2 * q2 + 1], xv.y);
+          for (int q = 0; q < 16; ++q) {
+            uint8_t bytes[P];
+#pragma unroll
+            for (int b = 0; b < P; ++b) bytes[b] = (uint8_t)(u4get(w[b], q >> 2) >> (8 * (q & 3)));
+            d[q] = __dmul_rn(code_to_double<P, SIGNED>(bytes), a.scale);
+          }
         }
-        if (masked) {
 #pragma unroll
-          for (int q = 0; q < 16; ++q) t[q] = d[q] != 0.0 ? t[q] : 0.0;
+        for (int k = 0; k < KR; ++k) {
+          const double2* xk = reinterpret_cast<const double2*>(xs + k * ORD_TILE + c * 16);
+          double t[16];
+#pragma unroll
+          for (int q2 = 0; q2 < 8; ++q2) {
+            double2 xv = xk[q2];
+            t[2 * q2] = __dmul_rn(d[2 * q2], xv.x);
+            t[2 * q2 + 1] = __dmul_rn(d[2 * q2 + 1], xv.y);
+          }
+          if (masked) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) t[q] = d[q] != 0.0 ? t[q] : 0.0;
+          }
+#pragma unroll
+          for (int q = 0; q < 16; ++q) acc[k] = __dadd_rn(acc[k], t[q]);
         }
-#pragma unroll
-        for (int q = 0; q < 16; ++q) acc[k] = __dadd_rn(acc[k], t[q]);
       }
     }
     __syncwarp();
