@@ -724,12 +724,8 @@ __global__ void __launch_bounds__(128) k2_ordered(OrdArgs a) {
             }
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-              double v;
-              if (SIGNED)   // 2^52 + 2^51 + (s + 2^31) - (2^52 + 2^51 + 2^31)
-                v = __dadd_rn(__hiloint2double(0x43380000, (int)((uint32_t)uv[i] ^ 0x80000000u)),
-                              -6755401588539392.0);
-              else          // 2^52 + u - 2^52
-                v = __dadd_rn(__hiloint2double(0x43300000, uv[i]), -4503599627370496.0);
+              // exact int -> double conversion (I2F.F64), off the DADD pipe
+              const double v = (SIGNED || P < 4) ? (double)uv[i] : (double)(uint32_t)uv[i];
               d[4 * wd + i] = __dmul_rn(v, a.scale);
             }
           }
