@@ -28,6 +28,7 @@
 #include "ptx.cuh"
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 namespace invop {
 
@@ -696,9 +697,16 @@ __global__ void __launch_bounds__(128) k2_ordered(OrdArgs a) {
     // unchanged (it starts at +0 and x+(-x) rounds to +0), so the reference's
     // zero skip only matters when the tile holds inf/nan: then the product of
     // a zero code is replaced by +0.
+    // Straight-line tile (8 chunks of 16 codes, no guards: the padding past n
+    // holds zero codes and zero x, whose +0 products leave the accumulator
+    // unchanged), so ptxas can overlap the decode / products of later chunks
+    // with the ordered DADD chain of earlier ones. Two instantiations: with and
+    // without the inf/nan zero-skip select, chosen once per tile.
+    auto tile_pass = [&](auto masked_tag) {
+      constexpr bool MASKED = decltype(masked_tag)::value;
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
-      if (c * 16 < cend) {
+      {
         uint4 w[P];
 #pragma unroll
         for (int b = 0; b < P; ++b)
@@ -724,8 +732,12 @@ __global__ void __launch_bounds__(128) k2_ordered(OrdArgs a) {
             }
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-              // exact int -> double conversion (I2F.F64), off the DADD pipe
-              const double v = (SIGNED || P < 4) ? (double)uv[i] : (double)(uint32_t)uv[i];
+              double v;
+              if (SIGNED)   // 2^52 + 2^51 + (s + 2^31) - (2^52 + 2^51 + 2^31)
+                v = __dadd_rn(__hiloint2double(0x43380000, (int)((uint32_t)uv[i] ^ 0x80000000u)),
+                              -6755401588539392.0);
+              else          // 2^52 + u - 2^52
+                v = __dadd_rn(__hiloint2double(0x43300000, uv[i]), -4503599627370496.0);
               d[4 * wd + i] = __dmul_rn(v, a.scale);
             }
           }
@@ -748,7 +760,7 @@ __global__ void __launch_bounds__(128) k2_ordered(OrdArgs a) {
             t[2 * q2] = __dmul_rn(d[2 * q2], xv.x);
             t[2 * q2 + 1] = __dmul_rn(d[2 * q2 + 1], xv.y);
           }
-          if (masked) {
+          if (MASKED) {
 #pragma unroll
             for (int q = 0; q < 16; ++q) t[q] = d[q] != 0.0 ? t[q] : 0.0;
           }
@@ -757,6 +769,9 @@ __global__ void __launch_bounds__(128) k2_ordered(OrdArgs a) {
         }
       }
     }
+    };
+    if (masked) tile_pass(std::true_type{});
+    else tile_pass(std::false_type{});
     __syncwarp();
   }
   cp_async_wait<0>();
