@@ -362,39 +362,44 @@ __global__ void k3_tile_planes(const uint8_t* __restrict__ in, int64_t rows, int
 }
 
 // ------------------------------------------------------------ x preparation
-// per right-hand side: e_t with max|x_t| * 2^e_t < 2^22
-__global__ void k3_exponents(const float* __restrict__ x, int64_t n, int64_t ldx, int nrhs,
-                             int* __restrict__ e, int* __restrict__ nonfinite) {
-  const int t = blockIdx.x;
+// max |x_t| for every right-hand side (as the bits of a non-negative float,
+// combined with atomicMax) plus an inf/nan flag; grid = (column chunks, RHS)
+__global__ void k3_xmax(const float* __restrict__ x, int64_t n, int64_t ldx,
+                        unsigned int* __restrict__ maxbits, int* __restrict__ nonfinite) {
+  const int t = blockIdx.y;
   float m = 0.0f;
-  if (t < nrhs)
-    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) m = fmaxf(m, fabsf(x[t * ldx + j]));
-  __shared__ float s[32];
-  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = m;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    m = threadIdx.x < (blockDim.x >> 5) ? s[threadIdx.x] : 0.0f;
-    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (threadIdx.x == 0) {
-      int ex = 0;
-      if (m > 0.0f && isfinite(m)) frexpf(m, &ex);
-      e[t] = (m > 0.0f && isfinite(m)) ? 22 - ex : 0;
-      if (!isfinite(m)) atomicOr(nonfinite, 1);
-    }
+  bool bad = false;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const float v = x[t * ldx + j];
+    bad |= !isfinite(v);
+    m = fmaxf(m, fabsf(v));
   }
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1);
+  if ((threadIdx.x & 31) == 0) atomicMax(&maxbits[t], __float_as_uint(m));
+}
+
+__device__ __forceinline__ int k3_exponent(unsigned int bits) {
+  const float m = __uint_as_float(bits);
+  int ex = 0;
+  if (m > 0.0f && isfinite(m)) frexpf(m, &ex);
+  return (m > 0.0f && isfinite(m)) ? 22 - ex : 0;   // max|x_t| * 2^e_t < 2^22
 }
 
 // balanced base-256 digits of X = rint(x * 2^e), into B[l][t][j] (int8)
 __global__ void k3_digits(const float* __restrict__ x, int64_t n, int64_t ldx, int nrhs,
-                          const int* __restrict__ e, int8_t* __restrict__ B, int64_t ldb) {
+                          const unsigned int* __restrict__ maxbits, int* __restrict__ e,
+                          int8_t* __restrict__ B, int64_t ldb) {
   const int64_t total = (int64_t)K3_NR * ldb;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
        k += (int64_t)gridDim.x * blockDim.x) {
     const int t = (int)(k / ldb);
     const int64_t j = k - (int64_t)t * ldb;
     int X = 0;
-    if (t < nrhs && j < n) X = __float2int_rn(ldexpf(x[t * ldx + j], e[t]));
+    const int et = t < nrhs ? k3_exponent(maxbits[t]) : 0;
+    if (j == 0) e[t] = et;
+    if (t < nrhs && j < n) X = __float2int_rn(ldexpf(x[t * ldx + j], et));
     const int d0 = ((X + 128) & 255) - 128;
     const int X1 = (X - d0) >> 8;
     const int d1 = ((X1 + 128) & 255) - 128;
@@ -493,19 +498,20 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
   // workspace: digits | exponents | int64 partial sums
   size_t b_bytes = (size_t)K3_ND * K3_NR * ldb;
   size_t e_off = round_up(b_bytes, 256);
-  size_t acc_off = e_off + 512;          // e[64] ints | flag | pad
+  size_t flag_off = e_off + 256;                          // e[64] ints | flag
+  size_t max_off = flag_off + 256;                        // max|x_t| bits [nrhs]
+  size_t acc_off = round_up(max_off + (size_t)nrhs * 4, 256);
   size_t acc_bytes = splits > 1 ? (size_t)K3_NR * p->rows * 8 : 0;
   int rc = ensure_scratch(&p->k3_ws, &p->k3_ws_bytes, acc_off + acc_bytes);
-  // inf/nan in x: the reference's zero-mantissa skip needs the fp32 masked
-  // kernels; checked up front (one small sync per batch)
+  if (rc) return rc;
+  unsigned int* maxbits = (unsigned int*)((char*)p->k3_ws + max_off);
+  int* flag = (int*)((char*)p->k3_ws + flag_off);
+  // max|x_t| of every right-hand side in one launch; inf/nan in x needs the
+  // reference's zero-mantissa skip (fp32 masked kernels): one small sync
   {
-    int* flag = (int*)((char*)p->k3_ws + e_off + 256);
-    int* e0 = (int*)((char*)p->k3_ws + e_off);
-    INVOP_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), s));
-    for (int64_t t0 = 0; t0 < nrhs; t0 += K3_NR) {
-      const int nr = (int)std::min<int64_t>(K3_NR, nrhs - t0);
-      k3_exponents<<<K3_NR, 256, 0, s>>>(x + t0 * ldx, p->n, ldx, nr, e0, flag);
-    }
+    INVOP_CUDA(cudaMemsetAsync((char*)p->k3_ws + flag_off, 0, max_off - flag_off + (size_t)nrhs * 4, s));
+    dim3 g((unsigned)std::min<int64_t>(cdiv(p->n, 256), 64), (unsigned)nrhs);
+    k3_xmax<<<g, 256, 0, s>>>(x, p->n, ldx, maxbits, flag);
     int h = 0;
     INVOP_CUDA(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
     INVOP_CUDA(cudaStreamSynchronize(s));
@@ -537,10 +543,8 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
   if (rc) return rc;
   for (int64_t t0 = 0; t0 < nrhs; t0 += K3_NR) {
     const int nr = (int)std::min<int64_t>(K3_NR, nrhs - t0);
-    int* flag = (int*)((char*)p->k3_ws + e_off + 256);
-    k3_exponents<<<K3_NR, 256, 0, s>>>(x + t0 * ldx, p->n, ldx, nr, e, flag);
     k3_digits<<<(unsigned)std::min<int64_t>(cdiv((int64_t)K3_NR * ldb, 256), sms * 16), 256, 0, s>>>(
-        x + t0 * ldx, p->n, ldx, nr, e, B, ldb);
+        x + t0 * ldx, p->n, ldx, nr, maxbits + t0, e, B, ldb);
     if (splits > 1) INVOP_CUDA(cudaMemsetAsync(yacc, 0, acc_bytes, s));
     K3Args a;
     a.rows = p->rows; a.n = p->n; a.P = p->P; a.hi_signed = p->is_signed;
