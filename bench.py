@@ -273,7 +273,6 @@ def run_ours(args, world, rank, local):
         if world > 1:
             torch.distributed.all_gather_into_tensor(full.view(-1), y32.view(-1))
 
-    plan_ld = (N + 511) // 512 * 512
     L.check(L.lib.invop_apply(h, x32.data_ptr(), N, y32.data_ptr(), rows, k, L.F32, L.MODE_FAST,
                               C.c_void_p(sptr)), "apply")
     for _ in range(max(args.warmup, 3)):
@@ -287,10 +286,12 @@ def run_ours(args, world, rank, local):
         torch.cuda.synchronize()
         if world > 1:
             torch.distributed.barrier()
+        lc0 = L.lib.invop_launch_count()
         ev0.record(stream)
         for _ in range(args.steps):
             step()
         ev1.record(stream)
+        launches = L.lib.invop_launch_count() - lc0
         torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
@@ -355,6 +356,7 @@ def run_ours(args, world, rank, local):
     op_bytes = C.c_int64()
     L.check(L.lib.invop_plan_apply_bytes(h, k, L.MODE_FAST, C.byref(op_bytes), C.c_void_p(sptr)))
     op_bytes = op_bytes.value
+    kname = L.lib.invop_apply_kernel(h, k, L.MODE_FAST).decode()
     alg_bytes = op_bytes + k * N * 4 + k * rows * 4
     achieved = alg_bytes / (k_ms * 1e-3) / 1e9
     int8_ops = 2.0 * rows * N * k * (code_bytes * 3) if k > 1 else None
@@ -395,9 +397,7 @@ def run_ours(args, world, rank, local):
             "roofline": {
                 "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
-                "kernel": (("k2_tvw (tiled variable-width codes, %.3f B/entry)" % (op_bytes / (rows * N)))
-                           if op_bytes != rows * plan_ld * code_bytes else "k2_stream<P=%d>" % code_bytes)
-                          if k == 1 else ("k3_batched<P=%d> (tcgen05 kind::i8)" % code_bytes),
+                "kernel": "%s (P=%d, %.3f operator B/entry)" % (kname, code_bytes, op_bytes / (rows * N)),
                 "kernel_ms": k_ms,
                 "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_src,
             },
@@ -406,7 +406,7 @@ def run_ours(args, world, rank, local):
                 "h2d_bytes_per_step": k * N * 8, "d2h_bytes_per_step": k * rows * 8,
                 "path": "invop_apply_host (C ABI, pinned host fp64 buffers)",
             },
-            "gpu_launches": args.steps * (1 if k == 1 else 3),
+            "gpu_launches": launches,
             "clocks": clk.summary(),
             "ordered_fp64": {"value": k * 1e3 / ord_ms, "unit": UNIT, "kernel_ms": ord_ms,
                              "achieved_gbs": alg_bytes / (ord_ms * 1e-3) / 1e9,

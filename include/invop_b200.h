@@ -56,12 +56,16 @@ enum { INVOP_F32 = 0, INVOP_F64 = 1 };
 /* INVOP_MODE_ORDERED: fp64, each output row accumulates (mant*10^-m)*x_j in
    ascending column order, zero mantissas skipped — bitwise equal to the
    reference apply (applyplan.py:4-8, _native.pyx:32-46).
-   INVOP_MODE_FAST: fp32 grouped-sum apply, sum_j mant_ij*x_j accumulated in
-   fp32, multiplied by 10^-m once per row. */
+   INVOP_MODE_FAST: fp32 I/O; x is split into 512-column pieces, each turned
+   into 23-bit fixed point, sum_j mant_ij*X_j accumulated exactly in integers
+   and scaled by 10^-m * 2^-e once per row (fp32 relative error <= 1e-5). */
 enum { INVOP_MODE_FAST = 0, INVOP_MODE_ORDERED = 1 };
 
 const char* invop_last_error(void);
 int invop_abi_version(void);
+/* Kernels launched so far by the apply entry points (invop_apply,
+   invop_apply_host) in this process — the benchmark's gpu_launches. */
+int64_t invop_launch_count(void);
 
 /* A1 — quantize (reference: invop.quantize, quant.py:48-65).
    entries: device fp64 [rows x cols] (leading dim ld). mant: device int64
@@ -148,6 +152,11 @@ int invop_apply_host(invop_plan* plan, const double* x, double* y, int64_t nrhs,
    of the roofline; builds the lazily created layouts first (synchronous). */
 int invop_plan_apply_bytes(invop_plan* plan, int64_t nrhs, int mode, int64_t* bytes,
                            void* stream);
+
+/* Name of the kernel an apply of `nrhs` right-hand sides in `mode` launches
+   ("k2_hl", "k2_stream", "k2_fast", "k3_batched", "k2_ordered", ...), for
+   benchmark labels; static string, "" for a NULL plan. */
+const char* invop_apply_kernel(const invop_plan* plan, int64_t nrhs, int mode);
 
 /* A8 — naive quantized apply of the reference (applyplan.py:194-209):
    identical arithmetic to ORDERED mode; provided under its own name. */

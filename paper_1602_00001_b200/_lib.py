@@ -39,7 +39,7 @@ _int = C.c_int
 _pi64 = C.POINTER(C.c_int64)
 _pint = C.POINTER(C.c_int)
 
-# name -> argtypes (restype is int for every entry point except invop_last_error)
+# name -> argtypes (restype is int except invop_last_error / invop_apply_kernel: char*)
 SIGNATURES = {
     "invop_abi_version": [],
     "invop_quantize": [_vp, _i64, _i64, _i64, _int, _vp, _i64, _pi64, _vp],
@@ -58,6 +58,7 @@ SIGNATURES = {
     "invop_apply_host": [_vp, _vp, _vp, _i64, _int, _vp],
     "invop_apply_naive": [_vp, _vp, _vp, _i64, _vp],
     "invop_plan_apply_bytes": [_vp, _i64, _int, _pi64, _vp],
+    "invop_apply_kernel": [_vp, _i64, _int],
     "invop_operator_create": [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, C.POINTER(_vp)],
     "invop_operator_factor": [_vp, _vp],
     "invop_operator_destroy": [_vp],
@@ -71,7 +72,7 @@ SIGNATURES = {
 def _load():
     if not LIB_PATH.exists():
         raise ImportError(
-            "libinvop_b200.so is not built (%s); run `python -m paper_1602_00001_b200.build` "
+            "libinvop_b200.so is not built (%s); run `python paper_1602_00001_b200/build.py` "
             "or __graft_entry__.build()" % LIB_PATH
         )
     lib = C.CDLL(str(LIB_PATH))
@@ -81,6 +82,9 @@ def _load():
         fn.restype = C.c_int
     lib.invop_last_error.argtypes = []
     lib.invop_last_error.restype = C.c_char_p
+    lib.invop_apply_kernel.restype = C.c_char_p
+    lib.invop_launch_count.argtypes = []
+    lib.invop_launch_count.restype = C.c_int64
     return lib
 
 
@@ -113,7 +117,7 @@ def check(rc: int, what: str = "") -> None:
 
 
 def exported_symbols() -> list:
-    return sorted(list(SIGNATURES) + ["invop_last_error"])
+    return sorted(list(SIGNATURES) + ["invop_last_error", "invop_launch_count"])
 
 
 def header_symbols() -> list:

@@ -1,5 +1,6 @@
 // C ABI plumbing of libinvop_b200: errors, plan lifetime, apply entry points.
 #include "common.cuh"
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -15,6 +16,9 @@ int fail(int code, const std::string& msg) {
   g_last_error = msg;
   return code;
 }
+
+static std::atomic<long long> g_launches{0};
+void count_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 int cuda_fail(cudaError_t e, const char* what) {
   g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
@@ -52,6 +56,8 @@ extern "C" const char* invop_last_error(void) { return g_last_error.c_str(); }
 
 extern "C" int invop_abi_version(void) { return 1; }
 
+extern "C" int64_t invop_launch_count(void) { return invop::g_launches.load(); }
+
 extern "C" int invop_plan_destroy(invop_plan* p) {
   if (!p) return INVOP_OK;
   for (int b = 0; b < INVOP_MAX_PLANES; ++b)
@@ -72,6 +78,8 @@ extern "C" int invop_plan_destroy(invop_plan* p) {
   if (p->tv_gptr) cudaFree(p->tv_gptr);
   if (p->tv_soff) cudaFree(p->tv_soff);
   if (p->tv_ws) cudaFree(p->tv_ws);
+  if (p->hl_data) cudaFree(p->hl_data);
+  if (p->hl_rowptr) cudaFree(p->hl_rowptr);
   if (p->host_pinned) cudaFreeHost(p->host_pinned);
   delete p;
   return INVOP_OK;
@@ -100,6 +108,35 @@ static bool layout_enabled(const char* env, bool dflt) {
   return *v != '0';
 }
 
+// Which kernel serves a fast-mode apply. Single right-hand side over long
+// rows: 3-byte codes take the HL layout (default; INVOP_HL=0 disables), TVW
+// and VW are opt-in (INVOP_TVW=1 / INVOP_VW=1); everything else streams the
+// byte planes (k2_stream / k2_fast). Many right-hand sides of <= 2-byte codes
+// go to the tensor-core kernel (K3; INVOP_NO_TC=1 disables).
+enum { ROUTE_PLANES = 0, ROUTE_K3, ROUTE_HL, ROUTE_TVW, ROUTE_VW };
+
+static int fast_route(const invop_plan* p, int64_t nrhs) {
+  if (!layout_enabled("INVOP_NO_TC", false) && batched_supported(p, nrhs)) return ROUTE_K3;
+  if (nrhs != 1 || p->ld / 512 < 16) return ROUTE_PLANES;
+  if (p->P == 3 && p->ld <= 16384 && p->hl_ready >= 0 && layout_enabled("INVOP_HL", true))
+    return ROUTE_HL;
+  if (p->tv_ready >= 0 && layout_enabled("INVOP_TVW", false)) return ROUTE_TVW;
+  if (p->vw_ready >= 0 && layout_enabled("INVOP_VW", false)) return ROUTE_VW;
+  return ROUTE_PLANES;
+}
+
+extern "C" const char* invop_apply_kernel(const invop_plan* p, int64_t nrhs, int mode) {
+  if (!p) return "";
+  if (mode == INVOP_MODE_ORDERED) return "k2_ordered";
+  switch (fast_route(p, nrhs)) {
+    case ROUTE_K3: return "k3_batched";
+    case ROUTE_HL: return "k2_hl";
+    case ROUTE_TVW: return "k2_tvw";
+    case ROUTE_VW: return "k2_vw";
+    default: return stream_selected(p, nrhs) ? "k2_stream" : "k2_fast";
+  }
+}
+
 extern "C" int invop_apply(const invop_plan* p, const void* x, int64_t ldx, void* y,
                            int64_t ldy, int64_t nrhs, int dtype, int mode, void* stream) {
   if (!p) return fail(INVOP_E_VALUE, "plan is NULL");
@@ -123,27 +160,22 @@ extern "C" int invop_apply(const invop_plan* p, const void* x, int64_t ldx, void
   }
   if (mode == INVOP_MODE_FAST) {
     if (dtype != INVOP_F32) return fail(INVOP_E_VALUE, "fast mode computes in fp32: dtype F32");
-    // many right-hand sides: tensor-core batched apply (K3)
-    const char* no_tc = getenv("INVOP_NO_TC");
-    if (!(no_tc && *no_tc && *no_tc != '0') && batched_supported(p, nrhs))
-      return apply_batched_launch(const_cast<invop_plan*>(p), (const float*)x,
-                                  nrhs > 1 ? ldx : p->n, (float*)y, nrhs > 1 ? ldy : p->rows,
-                                  nrhs, s);
-    // one right-hand side over long rows: tiled variable-width layout (TVW)
-    // (opt-in: INVOP_TVW=1; the byte-plane stream kernel is faster today)
-    if (nrhs == 1 && p->ld / 512 >= 16 && layout_enabled("INVOP_TVW", false)) {
-      invop_plan* mp = const_cast<invop_plan*>(p);
-      int rc = tvw_build(mp, s);
-      if (rc == INVOP_OK) return apply_tvw_launch(mp, (const float*)x, (float*)y, s);
+    invop_plan* mp = const_cast<invop_plan*>(p);
+    const int route = fast_route(p, nrhs);
+    if (route == ROUTE_K3)
+      return apply_batched_launch(mp, (const float*)x, nrhs > 1 ? ldx : p->n, (float*)y,
+                                  nrhs > 1 ? ldy : p->rows, nrhs, s);
+    if (route != ROUTE_PLANES) {
+      int rc = route == ROUTE_HL ? hl_build(mp, s) : route == ROUTE_TVW ? tvw_build(mp, s)
+                                                                        : vw_build(mp, s);
+      if (rc == INVOP_OK) {
+        rc = route == ROUTE_HL ? apply_hl_launch(mp, (const float*)x, (float*)y, s)
+           : route == ROUTE_TVW ? apply_tvw_launch(mp, (const float*)x, (float*)y, s)
+                                : apply_vw_launch(mp, (const float*)x, (float*)y, s);
+      }
       if (rc != INVOP_E_UNSUPPORTED) return rc;
-    }
-    // row-chunk variable-width layout (VW), opt-in (INVOP_VW=1)
-    const char* use_vw = getenv("INVOP_VW");
-    if (nrhs == 1 && p->ld / 512 >= 16 && use_vw && *use_vw && *use_vw != '0') {
-      invop_plan* mp = const_cast<invop_plan*>(p);
-      int rc = vw_build(mp, s);
-      if (rc == INVOP_OK) return apply_vw_launch(mp, (const float*)x, (float*)y, s);
-      if (rc != INVOP_E_UNSUPPORTED) return rc;
+      if (route == ROUTE_HL) mp->hl_ready = -1;
+      // layout not applicable to this plan: plain byte planes below
     }
     return apply_fast_launch(p, (const float*)x, nrhs > 1 ? ldx : p->n, (float*)y,
                              nrhs > 1 ? ldy : p->rows, nrhs, s);
@@ -157,23 +189,22 @@ extern "C" int invop_plan_apply_bytes(invop_plan* p, int64_t nrhs, int mode, int
   // roofline numerator), building the lazily created layouts first
   if (!p || !bytes) return fail(INVOP_E_VALUE, "NULL argument");
   cudaStream_t s = (cudaStream_t)stream;
-  if (mode == INVOP_MODE_FAST && nrhs == 1 && p->ld / 512 >= 16 &&
-      layout_enabled("INVOP_TVW", false)) {
-    int rc = tvw_build(p, s);
+  if (mode == INVOP_MODE_FAST) {
+    const int route = fast_route(p, nrhs);
+    int rc = route == ROUTE_HL ? hl_build(p, s) : route == ROUTE_TVW ? tvw_build(p, s)
+           : route == ROUTE_VW ? vw_build(p, s) : INVOP_E_UNSUPPORTED;
     if (rc == INVOP_OK) {
-      *bytes = tvw_stream_bytes(p);
+      if (route == ROUTE_HL) {
+        *bytes = p->hl_bytes + (p->rows + 1) * 8;
+      } else if (route == ROUTE_TVW) {
+        *bytes = tvw_stream_bytes(p);
+      } else {
+        const int64_t nch = p->ld / 512, nchp = (nch + 1) & ~1;
+        *bytes = p->vw_bytes + p->rows * nchp * 8 + (p->rows + 1) * 8;
+      }
       return INVOP_OK;
     }
-  }
-  const char* use_vw = getenv("INVOP_VW");
-  if (mode == INVOP_MODE_FAST && nrhs == 1 && p->ld / 512 >= 16 && use_vw && *use_vw &&
-      *use_vw != '0') {
-    int rc = vw_build(p, s);
-    if (rc == INVOP_OK) {
-      const int64_t nch = p->ld / 512, nchp = (nch + 1) & ~1;
-      *bytes = p->vw_bytes + p->rows * nchp * 8 + (p->rows + 1) * 8;
-      return INVOP_OK;
-    }
+    if (rc != INVOP_E_UNSUPPORTED) return rc;
   }
   *bytes = (int64_t)p->P * p->rows * p->ld;
   return INVOP_OK;
@@ -213,6 +244,7 @@ extern "C" int invop_apply_host(invop_plan* p, const double* x, double* y, int64
     float* fy = (float*)((char*)p->dev_y + ((yb + 15) & ~(size_t)15));
     int64_t nx = nrhs * p->n, ny = nrhs * p->rows;
     k_f64_to_f32<<<(unsigned)std::min<int64_t>(cdiv(nx, 256), 4096), 256, 0, s>>>(dx, fx, nx);
+    INVOP_LAUNCHED(2);   // + k_f32_to_f64 below
     rc = invop_apply(p, fx, p->n, fy, p->rows, nrhs, INVOP_F32, mode, stream);
     if (rc) return rc;
     k_f32_to_f64<<<(unsigned)std::min<int64_t>(cdiv(ny, 256), 4096), 256, 0, s>>>(fy, dy, ny);

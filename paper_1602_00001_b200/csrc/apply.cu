@@ -227,6 +227,7 @@ static int launch_fast_t(FastArgs a, int grid, cudaStream_t s) {
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   kern<<<grid, 512, smem, s>>>(a);
+  INVOP_LAUNCHED(1);
   INVOP_CHECK_LAUNCH("k2_fast");
   return INVOP_OK;
 }
@@ -489,6 +490,7 @@ static int launch_stream_p(const invop_plan* p, const float* x, float* y, cudaSt
   auto kern = k2_stream<P, SIGNED>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   kern<<<grid, (ST_CONSUMERS + 1) * 32, smem, s>>>(a);
+  INVOP_LAUNCHED(1);
   INVOP_CHECK_LAUNCH("k2_stream");
   return INVOP_OK;
 }
@@ -506,15 +508,19 @@ static int apply_stream(const invop_plan* p, const float* x, float* y, cudaStrea
   }
 }
 
+bool stream_selected(const invop_plan* p, int64_t nrhs) {
+  if (nrhs != 1 || p->ld / 512 < ST_CONSUMERS || getenv_flag("INVOP_NO_STREAM") || p->rows == 0)
+    return false;
+  const int64_t rows_per_cta = cdiv(p->rows, std::min<int64_t>(num_sms(), p->rows));
+  return rows_per_cta * ST_CONSUMERS * 8 <= 64 * 1024;
+}
+
 int apply_fast_launch(const invop_plan* p, const float* x, int64_t ldx, float* y, int64_t ldy,
                       int64_t nrhs, cudaStream_t s) {
   if (p->P > 4) return fail(INVOP_E_UNSUPPORTED, "fast mode needs codes of at most 4 bytes");
   if (p->rows == 0 || nrhs == 0) return INVOP_OK;
   // long rows, one right-hand side: stream rows through shared memory
-  if (nrhs == 1 && p->ld / 512 >= ST_CONSUMERS && !getenv_flag("INVOP_NO_STREAM")) {
-    int64_t rows_per_cta = cdiv(p->rows, std::min<int64_t>(num_sms(), p->rows));
-    if (rows_per_cta * ST_CONSUMERS * 8 <= 64 * 1024) return apply_stream(p, x, y, s);
-  }
+  if (stream_selected(p, nrhs)) return apply_stream(p, x, y, s);
   const int warps = 16;
   const int sms = num_sms();
   int Cp = (int)(p->ld / 512);
@@ -794,6 +800,7 @@ static int launch_ord_t(OrdArgs a, cudaStream_t s) {
   int64_t warps = cdiv(a.rows, 32);
   int64_t grid = cdiv(warps, wpb);
   kern<<<(unsigned)grid, wpb * 32, smem, s>>>(a);
+  INVOP_LAUNCHED(1);
   INVOP_CHECK_LAUNCH("k2_ordered");
   return INVOP_OK;
 }

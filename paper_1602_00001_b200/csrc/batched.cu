@@ -512,6 +512,7 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
     INVOP_CUDA(cudaMemsetAsync((char*)p->k3_ws + flag_off, 0, max_off - flag_off + (size_t)nrhs * 4, s));
     dim3 g((unsigned)std::min<int64_t>(cdiv(p->n, 256), 64), (unsigned)nrhs);
     k3_xmax<<<g, 256, 0, s>>>(x, p->n, ldx, maxbits, flag);
+    INVOP_LAUNCHED(1);
     int h = 0;
     INVOP_CUDA(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
     INVOP_CUDA(cudaStreamSynchronize(s));
@@ -528,6 +529,7 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
       if (!p->k3_tiles[b]) INVOP_CUDA(cudaMalloc(&p->k3_tiles[b], tile_bytes));
       k3_tile_planes<<<(unsigned)std::min<int64_t>(cdiv(tile_bytes / 16, 256), sms * 16), 256, 0, s>>>(
           p->planes[b], p->rows, p->ld, p->k3_tiles[b], rtiles);
+      INVOP_LAUNCHED(1);
       INVOP_CHECK_LAUNCH("k3_tile_planes");
     }
     const uint64_t trows = (uint64_t)rtiles * (p->ld / K3_BK) * K3_BM;
@@ -545,6 +547,7 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
     const int nr = (int)std::min<int64_t>(K3_NR, nrhs - t0);
     k3_digits<<<(unsigned)std::min<int64_t>(cdiv((int64_t)K3_NR * ldb, 256), sms * 16), 256, 0, s>>>(
         x + t0 * ldx, p->n, ldx, nr, maxbits + t0, e, B, ldb);
+    INVOP_LAUNCHED(2);   // k3_digits + k3_batched
     if (splits > 1) INVOP_CUDA(cudaMemsetAsync(yacc, 0, acc_bytes, s));
     K3Args a;
     a.rows = p->rows; a.n = p->n; a.P = p->P; a.hi_signed = p->is_signed;
@@ -570,6 +573,7 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
       int64_t tot = (int64_t)nr * p->rows;
       k3_finalize<<<(unsigned)std::min<int64_t>(cdiv(tot, 256), sms * 8), 256, 0, s>>>(
           yacc, p->rows, nr, e, p->scale, y + t0 * ldy, ldy);
+      INVOP_LAUNCHED(1);
     }
   }
   INVOP_CHECK_LAUNCH("k3 epilogue");

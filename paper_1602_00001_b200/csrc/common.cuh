@@ -52,6 +52,11 @@ struct invop_plan {
   int64_t tv_bytes = 0;
   int tv_ready = 0, tv_wmax = 0;
   void* tv_ws = nullptr; size_t tv_ws_bytes = 0; int64_t tv_ws_cnt_off = -1;
+  // HL layout (hl.cu): two low byte planes + top plane only where a chunk needs it
+  uint8_t* hl_data = nullptr;
+  int64_t* hl_rowptr = nullptr;     // [rows+1] byte offsets
+  int64_t hl_bytes = 0;
+  int hl_ready = 0;
   alignas(64) unsigned char k3_mapA[2][128];
   int k3_maps_ready = 0;
 };
@@ -83,6 +88,11 @@ int cuda_fail(cudaError_t e, const char* what);
 
 #define INVOP_CHECK_LAUNCH(what) INVOP_CUDA(cudaGetLastError())
 
+// kernels launched by the apply entry points (invop_apply / invop_apply_host),
+// cumulative; read through invop_launch_count() by the benchmark
+void count_launches(int n);
+#define INVOP_LAUNCHED(n) ::invop::count_launches(n)
+
 __host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 __host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
@@ -97,6 +107,7 @@ int plan_finalize_width(invop_plan* p, int64_t mn, int64_t mx, int64_t nnz);
 int apply_fast_launch(const invop_plan* p, const float* x, int64_t ldx, float* y,
                       int64_t ldy, int64_t nrhs, cudaStream_t s);
 bool batched_supported(const invop_plan* p, int64_t nrhs);
+bool stream_selected(const invop_plan* p, int64_t nrhs);
 int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, int64_t ldy,
                          int64_t nrhs, cudaStream_t s);
 int vw_build(invop_plan* p, cudaStream_t s);
@@ -104,6 +115,8 @@ int tvw_build(invop_plan* p, cudaStream_t s);
 int64_t tvw_stream_bytes(const invop_plan* p);
 int apply_tvw_launch(invop_plan* p, const float* x, float* y, cudaStream_t s);
 int apply_vw_launch(invop_plan* p, const float* x, float* y, cudaStream_t s);
+int hl_build(invop_plan* p, cudaStream_t s);
+int apply_hl_launch(invop_plan* p, const float* x, float* y, cudaStream_t s);
 int apply_ordered_launch(const invop_plan* p, const double* x, int64_t ldx, double* y,
                          int64_t ldy, int64_t nrhs, cudaStream_t s);
 

@@ -39,6 +39,14 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 
 // PRMT with the full selector nibble (bit 3 = replicate the sign of the
 // selected byte); __byte_perm only honours the low 3 bits of each nibble.
+// acc + (int64)a * b as one IMAD.WIDE (keeps the compiler from hoisting a
+// sign-extended 64-bit copy of a loop-invariant operand and multiplying 64x64)
+__device__ __forceinline__ long long madw(int32_t a, int32_t b, long long c) {
+  long long r;
+  asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(r) : "r"(a), "r"(b), "l"(c));
+  return r;
+}
+
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   uint32_t r;
   asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));

@@ -248,10 +248,10 @@ __device__ __forceinline__ long long tv_tile_dot(uint32_t tile_s, uint32_t xrec_
       } else {
         int32_t uv[4];
         dec_int4<W, false>(wds, uv);
-        acc += (long long)uv[0] * Xc[4 * wd + 0];
-        acc2 += (long long)uv[1] * Xc[4 * wd + 1];
-        acc += (long long)uv[2] * Xc[4 * wd + 2];
-        acc2 += (long long)uv[3] * Xc[4 * wd + 3];
+        acc = madw(uv[0], Xc[4 * wd + 0], acc);
+        acc2 = madw(uv[1], Xc[4 * wd + 1], acc2);
+        acc = madw(uv[2], Xc[4 * wd + 2], acc);
+        acc2 = madw(uv[3], Xc[4 * wd + 3], acc2);
       }
     }
   }
@@ -516,6 +516,7 @@ int apply_tvw_launch(invop_plan* p, const float* x, float* y, cudaStream_t s) {
   cudaFuncSetAttribute(k2_tvw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int grid = (int)std::min<int64_t>(sms, groups * parts);
   k2_tvw<<<grid, (TV_CONS + 1) * 32, smem, s>>>(a);
+  INVOP_LAUNCHED(2);   // + k_tv_xprep
   INVOP_CHECK_LAUNCH("k2_tvw");
   return INVOP_OK;
 }

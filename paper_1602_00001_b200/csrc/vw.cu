@@ -181,10 +181,10 @@ __device__ __forceinline__ long long vw_chunk_dot(uint32_t cp, const int32_t* X)
     } else {
       int32_t uv[4];
       dec_int4<W, false>(wds, uv);
-      acc += (long long)uv[0] * X[4 * w + 0];
-      acc2 += (long long)uv[1] * X[4 * w + 1];
-      acc += (long long)uv[2] * X[4 * w + 2];
-      acc2 += (long long)uv[3] * X[4 * w + 3];
+      acc = madw(uv[0], X[4 * w + 0], acc);
+      acc2 = madw(uv[1], X[4 * w + 1], acc2);
+      acc = madw(uv[2], X[4 * w + 2], acc);
+      acc2 = madw(uv[3], X[4 * w + 3], acc2);
     }
   }
   return acc + acc2;
@@ -440,6 +440,7 @@ int apply_vw_launch(invop_plan* p, const float* x, float* y, cudaStream_t s) {
   const size_t smem = (size_t)stages * a.stage_bytes + 2 * stages * 8 + slot_bytes;
   cudaFuncSetAttribute(k2_vw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k2_vw<<<grid, (VW_CONS + 1) * 32, smem, s>>>(a);
+  INVOP_LAUNCHED(1);
   INVOP_CHECK_LAUNCH("k2_vw");
   return INVOP_OK;
 }

@@ -371,7 +371,7 @@ def test_config2_against_reference_outputs(invop, O, golden):
 @pytest.mark.parametrize("lo,hi", [(0, 250), (-120, 120), (0, 60000), (-30000, 30000),
                                    (0, 9_000_000), (-4_000_000, 4_000_000), (0, 16_000_000),
                                    (-2_000_000_000, 2_000_000_000)])
-@pytest.mark.parametrize("layout", ["tvw", "vw", "planes"])
+@pytest.mark.parametrize("layout", ["tvw", "vw", "hl", "planes"])
 def test_stream_kernel_long_rows(invop, O, lo, hi, layout, monkeypatch):
     """Rows of >= 16 column steps take the bulk-copy streaming kernels:
     k2_stream on the byte planes (default), or the compressed layouts k2_tvw
@@ -379,6 +379,7 @@ def test_stream_kernel_long_rows(invop, O, lo, hi, layout, monkeypatch):
     import torch
 
     monkeypatch.setenv("INVOP_TVW", "1" if layout == "tvw" else "0")
+    monkeypatch.setenv("INVOP_HL", "1" if layout == "hl" else "0")
     if layout == "vw":
         monkeypatch.setenv("INVOP_VW", "1")
 
@@ -467,3 +468,56 @@ def test_row_shards_reassemble_exactly(invop, O, key, shards):
         parts32.append(sh.apply_device(x.float(), mode=0))
     assert torch.equal(torch.cat(parts64), y64)
     assert torch.equal(torch.cat(parts32), y32)
+
+
+@pytest.mark.parametrize("cons", [8, 16])
+@pytest.mark.parametrize("signed", [False, True])
+@pytest.mark.parametrize("N", [8192, 9000, 16384])
+def test_hl_sparse_top_plane(invop, O, signed, N, cons, monkeypatch):
+    """3-byte codes whose top byte is needed only in some 512-column chunks
+    (config 4's shape): the HL layout keeps the top plane for those chunks
+    only; results match the plain byte-plane kernel and the oracle."""
+    import torch
+
+    rows = 333
+    rng = np.random.default_rng(N + signed)
+    lo = -30000 if signed else 0
+    mant = rng.integers(lo, 30001, size=(rows, N))
+    # large values in ~30% of the chunks, row-dependent
+    for r in range(rows):
+        for c in range((N + 511) // 512):
+            if rng.random() < 0.3:
+                j = c * 512 + rng.integers(0, 512)
+                if j < N:
+                    mant[r, j] = rng.integers(70000, 500000) * (-1 if signed and rng.random() < 0.5 else 1)
+    mant[5] = 0                             # an all-zero row
+    mant[7, :] = 40000                      # every chunk needs the top byte (signed: 40000 > 32767)
+    if not signed:
+        mant[9, 3] = 9_000_000              # > 2^23: forces unsigned 3-byte codes
+    dplan = invop._plan.DevicePlan.from_mantissas(mant, 4, row0=0, n=N)
+    assert dplan.code_bytes == 3 and dplan.is_signed == signed
+    x = rng.standard_normal(N)
+    xt = torch.tensor(x, device="cuda", dtype=torch.float32)
+    monkeypatch.setenv("INVOP_HL", "0")
+    y_planes = dplan.apply_device(xt, mode=0).cpu().numpy()
+    monkeypatch.setenv("INVOP_HL", "1")
+    monkeypatch.setenv("INVOP_HL_CONS", str(cons))
+    y_hl = dplan.apply_device(xt, mode=0).cpu().numpy()
+    yo = O.ordered_apply(mant, 4, x.astype(np.float32).astype(np.float64))
+    assert relerr(y_hl, yo) <= F32_TOL
+    assert relerr(y_planes, yo) <= F32_TOL
+    if cons == 8:
+        # same x pieces per warp as k2_stream: same exact integer sums, same bits
+        assert y_hl.tobytes() == y_planes.tobytes()
+    # non-finite x: the reference's zero skip
+    col = 1000
+    mant2 = mant.copy()
+    mant2[::2, col] = 0
+    dplan2 = invop._plan.DevicePlan.from_mantissas(mant2, 4, row0=0, n=N)
+    xb = x.copy()
+    xb[col] = np.inf
+    y = dplan2.apply_device(torch.tensor(xb, device="cuda", dtype=torch.float32), mode=0).cpu().numpy()
+    yo2 = O.ordered_apply(mant2, 4, xb.astype(np.float32).astype(np.float64))
+    assert np.array_equal(np.isinf(y), np.isinf(yo2)) and np.array_equal(np.isnan(y), np.isnan(yo2))
+    fin = np.isfinite(yo2)
+    assert relerr(y[fin], yo2[fin]) <= F32_TOL

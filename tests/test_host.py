@@ -104,3 +104,18 @@ def test_device_path_fails_loudly_without_gpu():
     q = invop.QuantizedMatrix(n=2, scale_digits=1, mantissas=np.eye(2, dtype=np.int64))
     with pytest.raises(invop.InvopError):
         invop.build_plan(q).planned_additions
+
+
+def test_builder_loads_without_the_library(tmp_path):
+    """__graft_entry__.build() must work on a fresh checkout, where importing
+    the package fails because the library is not built yet: the builder
+    module loads standalone."""
+    import subprocess
+    import sys
+
+    code = ("import sys, __graft_entry__ as g; b = g._builder(); "
+            "assert 'paper_1602_00001_b200' not in sys.modules; "
+            "assert b.LIB.name == 'libinvop_b200.so' and b.sources(); print('ok')")
+    out = subprocess.run([sys.executable, "-c", code], cwd=str(_lib.LIB_PATH.parent.parent),
+                         capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0 and out.stdout.strip() == "ok", out.stderr
