@@ -254,6 +254,9 @@ def run_ours(args, world, rank, local):
     del dop
 
     X = cfg.rhs()
+    if args.nrhs:
+        reps = -(-args.nrhs // X.shape[0])
+        X = np.ascontiguousarray(np.tile(X, (reps, 1))[:args.nrhs])
     k = X.shape[0]
     x64 = torch.tensor(X, dtype=torch.float64, device=dev)      # [k, N]
     x32 = x64.float().contiguous()
@@ -361,7 +364,7 @@ def run_ours(args, world, rank, local):
     achieved = alg_bytes / (k_ms * 1e-3) / 1e9
     int8_ops = 2.0 * rows * N * k * (code_bytes * 3) if k > 1 else None
     traffic = None
-    prof = ROOT / "profiles" / ("ncu_cfg%d_k2_fast.json" % cfg.key)
+    prof = ROOT / "profiles" / ("ncu_cfg%d_%s.json" % (cfg.key, kname))
     if prof.exists():
         try:
             traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
@@ -434,6 +437,8 @@ def main():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--nrhs", type=int, default=0,
+                    help="right-hand sides per step (default: the config's own count)")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     args = ap.parse_args()
     world, rank, local = dist_init(args)

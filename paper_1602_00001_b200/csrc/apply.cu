@@ -264,9 +264,14 @@ static int fast_SW(int KR) { return KR == 1 ? 2 : 1; }
 // the result is deterministic and independent of summation order.
 // A warp whose x piece holds inf/nan falls back to fp32 decoding with the
 // reference's zero-mantissa skip.
-constexpr int ST_CONSUMERS = 8;      // consumer warps (one column piece each)
-constexpr int ST_SW = 4;             // 512-column steps per consumer warp per slab
-constexpr int ST_SLAB = ST_CONSUMERS * ST_SW * 512;   // 16384 columns
+// CONS consumer warps (one column piece of ST_SLAB / CONS columns each); codes
+// of at most 3 bytes (4-byte codes take k2_fast: their int64 sums could overflow)
+constexpr int ST_SLAB = 16384;       // columns per slab (stage)
+static int stream_consumers() {
+  // 16 x 2 chunks: config 4 0.124 ms (8 x 4: 0.127), config 5 one RHS 1.50 ms (1.76)
+  const char* v = getenv("INVOP_ST_CONS");
+  return v && atoi(v) == 8 ? 8 : 16;
+}
 
 struct StreamArgs {
   const uint8_t* planes[4];
@@ -280,8 +285,9 @@ struct StreamArgs {
   int slot_rows;
 };
 
-template <int P, bool SIGNED>
-__global__ void __launch_bounds__((ST_CONSUMERS + 1) * 32, 1) k2_stream(StreamArgs a) {
+template <int P, bool SIGNED, int CONS>
+__global__ void __launch_bounds__((CONS + 1) * 32, 1) k2_stream(StreamArgs a) {
+  constexpr int ST_CONSUMERS = CONS, ST_SW = ST_SLAB / (CONS * 512);
   constexpr bool TWO = (P >= 3);
   extern __shared__ __align__(128) unsigned char smem[];
   // layout: [stages][P][ST_SLAB] codes | full[stages] | empty[stages] | slot
@@ -398,18 +404,20 @@ __global__ void __launch_bounds__((ST_CONSUMERS + 1) * 32, 1) k2_stream(StreamAr
             for (int b = 0; b < P; ++b) wds[b] = u4get(cw[b], w);
             int32_t uv[4];
             dec_int4<P, SIGNED>(wds, uv);
-            acc += (long long)uv[0] * X[t][4 * w + 0];
-            acc2 += (long long)uv[1] * X[t][4 * w + 1];
-            acc += (long long)uv[2] * X[t][4 * w + 2];
-            acc2 += (long long)uv[3] * X[t][4 * w + 3];
+            acc = madw(uv[0], X[t][4 * w + 0], acc);
+            acc2 = madw(uv[1], X[t][4 * w + 1], acc2);
+            acc = madw(uv[2], X[t][4 * w + 2], acc);
+            acc2 = madw(uv[3], X[t][4 * w + 3], acc2);
           }
         }
         acc += acc2;
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_s + 8 * (S + st));   // stage consumed by this warp
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        part = (double)acc * inv2e;
+        // exact warp sum with two REDUX (P <= 3): |acc| < 64 * 2^24 * 2^22 = 2^52,
+        // so the 27-bit low parts sum below 2^32 and the high parts below 2^30
+        const uint32_t slo = __reduce_add_sync(0xffffffffu, (uint32_t)acc & 0x7FFFFFFu);
+        const int32_t shi = __reduce_add_sync(0xffffffffu, (int32_t)(acc >> 27));
+        part = (double)(((long long)shi << 27) + (long long)slo) * inv2e;
       } else {
         float acc = 0.0f;
 #pragma unroll
@@ -467,8 +475,8 @@ __global__ void __launch_bounds__((ST_CONSUMERS + 1) * 32, 1) k2_stream(StreamAr
   }
 }
 
-template <int P, bool SIGNED>
-static int launch_stream_p(const invop_plan* p, const float* x, float* y, cudaStream_t s) {
+template <int P, bool SIGNED, int CONS>
+static int launch_stream_t(const invop_plan* p, const float* x, float* y, cudaStream_t s) {
   StreamArgs a;
   for (int b = 0; b < 4; ++b) a.planes[b] = p->planes[b < p->P ? b : 0];
   a.rows = p->rows; a.n = p->n; a.ld = p->ld;
@@ -478,7 +486,7 @@ static int launch_stream_p(const invop_plan* p, const float* x, float* y, cudaSt
   a.stage_bytes = P * ST_SLAB;
   int grid = (int)std::min<int64_t>(num_sms(), p->rows);
   a.slot_rows = (int)cdiv(p->rows, grid);
-  size_t slot_bytes = (size_t)a.slot_rows * ST_CONSUMERS * sizeof(double);
+  size_t slot_bytes = (size_t)a.slot_rows * CONS * sizeof(double);
   const size_t budget = 225 * 1024;
   int stages = (int)((budget - slot_bytes - 256) / (a.stage_bytes + 16));
   // 3 stages measured best at config 4 (0.123 ms vs 0.126 with 4, 0.133 with 2)
@@ -487,12 +495,18 @@ static int launch_stream_p(const invop_plan* p, const float* x, float* y, cudaSt
   if (stages < 2) return fail(INVOP_E_UNSUPPORTED, "k2_stream: not enough shared memory");
   a.stages = stages;
   size_t smem = (size_t)stages * a.stage_bytes + 2 * stages * 8 + slot_bytes;
-  auto kern = k2_stream<P, SIGNED>;
+  auto kern = k2_stream<P, SIGNED, CONS>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<grid, (ST_CONSUMERS + 1) * 32, smem, s>>>(a);
+  kern<<<grid, (CONS + 1) * 32, smem, s>>>(a);
   INVOP_LAUNCHED(1);
   INVOP_CHECK_LAUNCH("k2_stream");
   return INVOP_OK;
+}
+
+template <int P, bool SIGNED>
+static int launch_stream_p(const invop_plan* p, const float* x, float* y, cudaStream_t s) {
+  return stream_consumers() == 8 ? launch_stream_t<P, SIGNED, 8>(p, x, y, s)
+                                 : launch_stream_t<P, SIGNED, 16>(p, x, y, s);
 }
 
 static int apply_stream(const invop_plan* p, const float* x, float* y, cudaStream_t s) {
@@ -502,17 +516,15 @@ static int apply_stream(const invop_plan* p, const float* x, float* y, cudaStrea
     case 4: return launch_stream_p<2, false>(p, x, y, s);
     case 5: return launch_stream_p<2, true>(p, x, y, s);
     case 6: return launch_stream_p<3, false>(p, x, y, s);
-    case 7: return launch_stream_p<3, true>(p, x, y, s);
-    case 8: return launch_stream_p<4, false>(p, x, y, s);
-    default: return launch_stream_p<4, true>(p, x, y, s);
+    default: return launch_stream_p<3, true>(p, x, y, s);
   }
 }
 
 bool stream_selected(const invop_plan* p, int64_t nrhs) {
-  if (nrhs != 1 || p->ld / 512 < ST_CONSUMERS || getenv_flag("INVOP_NO_STREAM") || p->rows == 0)
+  if (nrhs != 1 || p->P > 3 || p->ld / 512 < 16 || getenv_flag("INVOP_NO_STREAM") || p->rows == 0)
     return false;
   const int64_t rows_per_cta = cdiv(p->rows, std::min<int64_t>(num_sms(), p->rows));
-  return rows_per_cta * ST_CONSUMERS * 8 <= 64 * 1024;
+  return rows_per_cta * stream_consumers() * 8 <= 64 * 1024;
 }
 
 int apply_fast_launch(const invop_plan* p, const float* x, int64_t ldx, float* y, int64_t ldy,
