@@ -112,6 +112,10 @@ class DevicePlan:
         h = d.cpu().numpy()
         return h[: self.n].copy(), h[max(self.n, 1): max(self.n, 1) + self.n].copy()
 
+    def apply_kernel(self, nrhs: int = 1, mode: int = 0) -> str:
+        """Name of the kernel an apply of `nrhs` right-hand sides launches."""
+        return L.lib.invop_apply_kernel(self._h, nrhs, mode).decode()
+
     def decode(self):
         """int64 mantissas as a device tensor [rows x n]."""
         t = dev.require_cuda()

@@ -80,6 +80,8 @@ extern "C" int invop_plan_destroy(invop_plan* p) {
   if (p->tv_ws) cudaFree(p->tv_ws);
   if (p->hl_data) cudaFree(p->hl_data);
   if (p->hl_rowptr) cudaFree(p->hl_rowptr);
+  if (p->dl_data) cudaFree(p->dl_data);
+  if (p->dl_uoff) cudaFree(p->dl_uoff);
   if (p->host_pinned) cudaFreeHost(p->host_pinned);
   delete p;
   return INVOP_OK;
@@ -113,11 +115,12 @@ static bool layout_enabled(const char* env, bool dflt) {
 // and VW are opt-in (INVOP_TVW=1 / INVOP_VW=1); everything else streams the
 // byte planes (k2_stream / k2_fast). Many right-hand sides of <= 2-byte codes
 // go to the tensor-core kernel (K3; INVOP_NO_TC=1 disables).
-enum { ROUTE_PLANES = 0, ROUTE_K3, ROUTE_HL, ROUTE_TVW, ROUTE_VW };
+enum { ROUTE_PLANES = 0, ROUTE_K3, ROUTE_DL, ROUTE_HL, ROUTE_TVW, ROUTE_VW };
 
 static int fast_route(const invop_plan* p, int64_t nrhs) {
   if (!layout_enabled("INVOP_NO_TC", false) && batched_supported(p, nrhs)) return ROUTE_K3;
   if (nrhs != 1 || p->ld / 512 < 16) return ROUTE_PLANES;
+  if (p->P <= 3 && p->dl_ready >= 0 && layout_enabled("INVOP_DL", true)) return ROUTE_DL;
   if (p->P == 3 && p->ld <= 16384 && p->hl_ready >= 0 && layout_enabled("INVOP_HL", true))
     return ROUTE_HL;
   if (p->tv_ready >= 0 && layout_enabled("INVOP_TVW", false)) return ROUTE_TVW;
@@ -130,6 +133,7 @@ extern "C" const char* invop_apply_kernel(const invop_plan* p, int64_t nrhs, int
   if (mode == INVOP_MODE_ORDERED) return "k2_ordered";
   switch (fast_route(p, nrhs)) {
     case ROUTE_K3: return "k3_batched";
+    case ROUTE_DL: return "k2_dl";
     case ROUTE_HL: return "k2_hl";
     case ROUTE_TVW: return "k2_tvw";
     case ROUTE_VW: return "k2_vw";
@@ -166,15 +170,19 @@ extern "C" int invop_apply(const invop_plan* p, const void* x, int64_t ldx, void
       return apply_batched_launch(mp, (const float*)x, nrhs > 1 ? ldx : p->n, (float*)y,
                                   nrhs > 1 ? ldy : p->rows, nrhs, s);
     if (route != ROUTE_PLANES) {
-      int rc = route == ROUTE_HL ? hl_build(mp, s) : route == ROUTE_TVW ? tvw_build(mp, s)
-                                                                        : vw_build(mp, s);
+      int rc = route == ROUTE_DL ? dl_build(mp, s) : route == ROUTE_HL ? hl_build(mp, s)
+             : route == ROUTE_TVW ? tvw_build(mp, s) : vw_build(mp, s);
       if (rc == INVOP_OK) {
-        rc = route == ROUTE_HL ? apply_hl_launch(mp, (const float*)x, (float*)y, s)
+        rc = route == ROUTE_DL ? apply_dl_launch(mp, (const float*)x, (float*)y, s)
+           : route == ROUTE_HL ? apply_hl_launch(mp, (const float*)x, (float*)y, s)
            : route == ROUTE_TVW ? apply_tvw_launch(mp, (const float*)x, (float*)y, s)
                                 : apply_vw_launch(mp, (const float*)x, (float*)y, s);
       }
       if (rc != INVOP_E_UNSUPPORTED) return rc;
       if (route == ROUTE_HL) mp->hl_ready = -1;
+      if (route == ROUTE_DL) mp->dl_ready = -1;
+      if (route == ROUTE_DL || route == ROUTE_HL)
+        return invop_apply(p, x, ldx, y, ldy, nrhs, dtype, mode, stream);   // next route
       // layout not applicable to this plan: plain byte planes below
     }
     return apply_fast_launch(p, (const float*)x, nrhs > 1 ? ldx : p->n, (float*)y,
@@ -191,10 +199,15 @@ extern "C" int invop_plan_apply_bytes(invop_plan* p, int64_t nrhs, int mode, int
   cudaStream_t s = (cudaStream_t)stream;
   if (mode == INVOP_MODE_FAST) {
     const int route = fast_route(p, nrhs);
-    int rc = route == ROUTE_HL ? hl_build(p, s) : route == ROUTE_TVW ? tvw_build(p, s)
-           : route == ROUTE_VW ? vw_build(p, s) : INVOP_E_UNSUPPORTED;
+    int rc = route == ROUTE_DL ? dl_build(p, s) : route == ROUTE_HL ? hl_build(p, s)
+           : route == ROUTE_TVW ? tvw_build(p, s) : route == ROUTE_VW ? vw_build(p, s)
+           : INVOP_E_UNSUPPORTED;
+    if (rc == INVOP_E_UNSUPPORTED && (route == ROUTE_DL || route == ROUTE_HL))
+      return invop_plan_apply_bytes(p, nrhs, mode, bytes, stream);   // next route
     if (rc == INVOP_OK) {
-      if (route == ROUTE_HL) {
+      if (route == ROUTE_DL) {
+        *bytes = p->dl_bytes + (p->rows * p->dl_nslabs + 1) * 8;
+      } else if (route == ROUTE_HL) {
         *bytes = p->hl_bytes + (p->rows + 1) * 8;
       } else if (route == ROUTE_TVW) {
         *bytes = tvw_stream_bytes(p);

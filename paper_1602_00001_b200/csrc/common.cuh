@@ -57,6 +57,11 @@ struct invop_plan {
   int64_t* hl_rowptr = nullptr;     // [rows+1] byte offsets
   int64_t hl_bytes = 0;
   int hl_ready = 0;
+  // DL layout (dl.cu): second-order row residuals, per-chunk byte width
+  uint8_t* dl_data = nullptr;
+  int64_t* dl_uoff = nullptr;       // [units+1] byte offsets, units in (CTA, slab, row) order
+  int64_t dl_bytes = 0, dl_maxunit = 0;
+  int dl_ready = 0, dl_grid = 0, dl_nslabs = 0;
   alignas(64) unsigned char k3_mapA[2][128];
   int k3_maps_ready = 0;
 };
@@ -116,6 +121,8 @@ int64_t tvw_stream_bytes(const invop_plan* p);
 int apply_tvw_launch(invop_plan* p, const float* x, float* y, cudaStream_t s);
 int apply_vw_launch(invop_plan* p, const float* x, float* y, cudaStream_t s);
 int hl_build(invop_plan* p, cudaStream_t s);
+int dl_build(invop_plan* p, cudaStream_t s);
+int apply_dl_launch(invop_plan* p, const float* x, float* y, cudaStream_t s);
 int apply_hl_launch(invop_plan* p, const float* x, float* y, cudaStream_t s);
 int apply_ordered_launch(const invop_plan* p, const double* x, int64_t ldx, double* y,
                          int64_t ldy, int64_t nrhs, cudaStream_t s);

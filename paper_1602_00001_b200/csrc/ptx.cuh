@@ -37,8 +37,6 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
       : "memory");
 }
 
-// PRMT with the full selector nibble (bit 3 = replicate the sign of the
-// selected byte); __byte_perm only honours the low 3 bits of each nibble.
 // acc + (int64)a * b as one IMAD.WIDE (keeps the compiler from hoisting a
 // sign-extended 64-bit copy of a loop-invariant operand and multiplying 64x64)
 __device__ __forceinline__ long long madw(int32_t a, int32_t b, long long c) {
@@ -47,6 +45,39 @@ __device__ __forceinline__ long long madw(int32_t a, int32_t b, long long c) {
   return r;
 }
 
+// 4-way byte dot products with int32 accumulate: signed x signed and
+// unsigned (a) x signed (b)
+__device__ __forceinline__ int32_t dp4a_ss(uint32_t a, uint32_t b, int32_t c) {
+  int32_t r;
+  asm("dp4a.s32.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
+__device__ __forceinline__ int32_t dp4a_us(uint32_t a, uint32_t b, int32_t c) {
+  int32_t r;
+  asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
+
+// balanced base-256 digits of |X| <= 2^22: X = d0 + 256 d1 + 65536 d2, each
+// digit in [-128, 127]; 4 consecutive values' digit d packed into word d
+__device__ __forceinline__ void x_digits4(const int32_t* X, uint32_t* w) {
+  uint32_t p0 = 0, p1 = 0, p2 = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int32_t x = X[i];
+    const int32_t d0 = ((x + 128) & 255) - 128;
+    const int32_t x1 = (x - d0) >> 8;
+    const int32_t d1 = ((x1 + 128) & 255) - 128;
+    const int32_t d2 = (x1 - d1) >> 8;
+    p0 |= (uint32_t)(d0 & 255) << (8 * i);
+    p1 |= (uint32_t)(d1 & 255) << (8 * i);
+    p2 |= (uint32_t)(d2 & 255) << (8 * i);
+  }
+  w[0] = p0; w[1] = p1; w[2] = p2;
+}
+
+// PRMT with the full selector nibble (bit 3 = replicate the sign of the
+// selected byte); __byte_perm only honours the low 3 bits of each nibble.
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   uint32_t r;
   asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));

@@ -522,3 +522,73 @@ def test_hl_sparse_top_plane(invop, O, signed, N, cons, monkeypatch):
     assert np.array_equal(np.isinf(y), np.isinf(yo2)) and np.array_equal(np.isnan(y), np.isnan(yo2))
     fin = np.isfinite(yo2)
     assert relerr(y[fin], yo2[fin]) <= F32_TOL
+
+
+def _smooth_rows(rng, rows, N, amp, signed):
+    """Rows that vary smoothly with the row index (like inverse-operator rows)."""
+    r = np.arange(rows)[:, None].astype(np.float64)
+    j = np.arange(N)[None, :].astype(np.float64)
+    base = amp * np.exp(-np.abs(j / N * rows - r) / (0.1 * rows)) * (1 + 0.3 * np.sin(j / 37.0))
+    if signed:
+        base *= np.cos(j / 501.0)
+    return np.rint(base + rng.integers(-2, 3, size=(rows, N))).astype(np.int64)
+
+
+@pytest.mark.parametrize("amp,signed", [(100, False), (100, True), (20000, False),
+                                        (20000, True), (3_000_000, False), (3_000_000, True)])
+@pytest.mark.parametrize("N", [8192, 9000, 20000])
+def test_dl_row_residuals(invop, O, amp, signed, N, monkeypatch):
+    """DL layout (second-order row residuals, per-chunk byte widths): same bits
+    as k2_stream on the plain byte planes, oracle parity, inf/nan zero skip."""
+    import torch
+
+    rows = 400
+    rng = np.random.default_rng(amp + N + signed)
+    mant = _smooth_rows(rng, rows, N, amp, signed)
+    mant[17, ::3] = 0
+    mant[18] = 0                       # rows with zeros and an all-zero row
+    if not signed:
+        mant = np.abs(mant)
+    dplan = invop._plan.DevicePlan.from_mantissas(mant, 4, row0=0, n=N)
+    x = rng.standard_normal(N)
+    xt = torch.tensor(x, device="cuda", dtype=torch.float32)
+    monkeypatch.setenv("INVOP_DL", "1")
+    assert dplan.apply_kernel(1) == "k2_dl"
+    y_dl = dplan.apply_device(xt, mode=0).cpu().numpy()
+    # built and used; 1-byte codes cannot shrink, the layout is declined
+    assert dplan.apply_kernel(1) == ("k2_dl" if dplan.code_bytes > 1 else "k2_stream")
+    monkeypatch.setenv("INVOP_DL", "0")
+    monkeypatch.setenv("INVOP_HL", "0")
+    y_st = dplan.apply_device(xt, mode=0).cpu().numpy()
+    assert dplan.apply_kernel(1) == "k2_stream"
+    yo = O.ordered_apply(mant, 4, x.astype(np.float32).astype(np.float64))
+    assert relerr(y_dl, yo) <= F32_TOL
+    assert y_dl.tobytes() == y_st.tobytes()
+    # non-finite x in one warp piece: that piece reads the plain codes
+    monkeypatch.setenv("INVOP_DL", "1")
+    col = 1000
+    mant2 = mant.copy()
+    mant2[::2, col] = 0
+    dplan2 = invop._plan.DevicePlan.from_mantissas(mant2, 4, row0=0, n=N)
+    xb = x.copy()
+    xb[col] = np.inf
+    y = dplan2.apply_device(torch.tensor(xb, device="cuda", dtype=torch.float32), mode=0).cpu().numpy()
+    assert dplan2.apply_kernel(1) == ("k2_dl" if dplan.code_bytes > 1 else "k2_stream")
+    yo2 = O.ordered_apply(mant2, 4, xb.astype(np.float32).astype(np.float64))
+    assert np.array_equal(np.isinf(y), np.isinf(yo2)) and np.array_equal(np.isnan(y), np.isnan(yo2))
+    fin = np.isfinite(yo2)
+    assert relerr(y[fin], yo2[fin]) <= F32_TOL
+
+
+def test_dl_rejects_rough_rows(invop, monkeypatch):
+    """Random (non-smooth) rows: residuals are wider than the codes, so the
+    DL layout is not built and the byte-plane kernel runs."""
+    import torch
+
+    rng = np.random.default_rng(7)
+    mant = rng.integers(-30000, 30000, size=(300, 9000))
+    dplan = invop._plan.DevicePlan.from_mantissas(mant, 3, row0=0, n=9000)
+    monkeypatch.setenv("INVOP_DL", "1")
+    monkeypatch.setenv("INVOP_HL", "0")
+    dplan.apply_device(torch.zeros(9000, device="cuda"), mode=0)
+    assert dplan.apply_kernel(1) == "k2_stream"
