@@ -22,8 +22,9 @@
 //   [48 B header: u8 start[33], start of chunk c in 512-byte blocks after the
 //    header; chunk c has w = start[c+1] - start[c] byte planes]
 //   [chunk 0: w_0 planes of 512 B][chunk 1] ...
-// Residuals are two's complement; a chunk of width w decodes as a w-byte
-// signed code. Codes of at most 3 bytes (|e| < 2^25).
+// A residual is stored as balanced base-256 digits, e = sum_b 256^b s_b with
+// every s_b in [-128, 127] (plane b holds s_b); a chunk keeps as many planes
+// as its largest residual needs. Codes of at most 3 bytes (|e| < 2^25).
 //
 // A consumer warp whose x piece holds inf/nan cannot use residuals (the
 // reference skips zero mantissas): it reads that row piece's codes from the
@@ -60,9 +61,24 @@ __device__ __forceinline__ void dl_load16(const uint8_t* const* planes, int P, i
   }
 }
 
+// balanced base-256 digit b of e
+__host__ __device__ inline int32_t dl_digit(int32_t e, int b) {
+  for (int i = 0; i < b; ++i) {
+    const int32_t d = ((e + 128) & 255) - 128;
+    e = (e - d) >> 8;
+  }
+  return ((e + 128) & 255) - 128;
+}
+
+// number of balanced digits of e (>= 1)
 __device__ __forceinline__ uint32_t dl_width(int32_t e) {
-  const uint32_t a = (uint32_t)(e < 0 ? ~e : e);     // magnitude in two's complement terms
-  return a < 0x80u ? 1u : a < 0x8000u ? 2u : a < 0x800000u ? 3u : 4u;
+  uint32_t w = 1;
+  for (;;) {
+    const int32_t d = ((e + 128) & 255) - 128;
+    e = (e - d) >> 8;
+    if (e == 0) return w;
+    ++w;
+  }
 }
 
 struct DlBuild {
@@ -164,7 +180,7 @@ __device__ __forceinline__ uint4 dl_bytes16(const int32_t* e, int b) {
   for (int k = 0; k < 4; ++k) {
     uint32_t x = 0;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) x |= (((uint32_t)e[4 * k + i] >> (8 * b)) & 0xffu) << (8 * i);
+    for (int i = 0; i < 4; ++i) x |= ((uint32_t)dl_digit(e[4 * k + i], b) & 0xffu) << (8 * i);
     w[k] = x;
   }
   return make_uint4(w[0], w[1], w[2], w[3]);
@@ -200,40 +216,45 @@ struct DlArgs {
   double scale;
   const float* x;
   float* y;
-  int stages, stage_bytes;
+  int ring_bytes;               // variable-size unit ring (FIFO) in shared memory
 };
 
-// sum_q e_q X_q over a lane's 16 codes of a chunk of width W, with byte dot
-// products: e = sum_b 256^b e_b (bytes 0..W-2 unsigned, byte W-1 signed) and
-// X = sum_d 256^d x_d (balanced digits, xd[d][k] packs codes 4k..4k+3), so the
-// (b, d) partial lands in S[b + d] with weight 256^(b+d). Exact in int32: one
-// DP4A adds at most 4 * 255 * 128 < 2^17.
-template <int W>
-__device__ __forceinline__ void dl_mac(const unsigned char* p, const uint32_t (*xd)[4],
-                                       int32_t* S) {
-  uint4 cw[4];
+constexpr int DL_NS = 8;         // units in flight at most (barrier pairs)
+
+__device__ __forceinline__ uint4 dl_lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint32_t dl_lds_u8(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+
+// plane b of a lane's 16 residual digits times the 3 digit words of X: the
+// (b, d) partial lands in S[b + d] (weight 256^(b+d)). Exact in int32: one
+// DP4A adds at most 4 * 128 * 128 = 2^16.
+template <int B>
+__device__ __forceinline__ void dl_plane(const uint4& cw, const uint32_t (*xd)[4], int32_t* S) {
 #pragma unroll
-  for (int b = 0; b < W; ++b) cw[b] = *reinterpret_cast<const uint4*>(p + b * 512);
+  for (int k = 0; k < 4; ++k)
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-#pragma unroll
-    for (int b = 0; b < W; ++b) {
-      const uint32_t a = u4get(cw[b], k);
-#pragma unroll
-      for (int d = 0; d < 3; ++d)
-        S[b + d] = (b == W - 1) ? dp4a_ss(a, xd[d][k], S[b + d]) : dp4a_us(a, xd[d][k], S[b + d]);
-    }
-  }
+    for (int d = 0; d < 3; ++d) S[B + d] = dp4a_ss(u4get(cw, k), xd[d][k], S[B + d]);
 }
 
 template <int CONS>
 __global__ void __launch_bounds__((CONS + 1) * 32, 1) k2_dl(DlArgs a) {
   constexpr int SW = DL_SLAB / (CONS * 512);
   extern __shared__ __align__(128) unsigned char smem[];
-  const int S = a.stages;
+  // [ring][full[NS], empty[NS]][unit pos[NS]][slot: nrows x CONS doubles][unit offsets]
+  constexpr int S = DL_NS;
+  const uint32_t R = (uint32_t)a.ring_bytes;
   unsigned char* ring = smem;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)S * a.stage_bytes);
-  double* slot = reinterpret_cast<double*>(bars + 2 * S);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + R);
+  uint32_t* s_pos = reinterpret_cast<uint32_t*>(bars + 2 * S);
+  double* slot = reinterpret_cast<double*>(s_pos + 2 * S);
   const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
   const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(bars);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -255,16 +276,35 @@ __global__ void __launch_bounds__((CONS + 1) * 32, 1) k2_dl(DlArgs a) {
 
   if (warp == CONS) {
     if (lane == 0) {
+      // FIFO of variable-size units: a unit goes at the ring head (or at 0 when
+      // it would run past the end); the oldest units are retired (all consumer
+      // warps arrived on their empty barrier) until it fits and a slot is free
       uint64_t policy;
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
-      int st = 0;
-      uint32_t ph = 0;
-      for (int64_t u = 0; u < units; ++u) {
-        if (u >= S) mbar_wait(bar_s + 8 * (S + st), ph ^ 1);
+      uint32_t* s_alloc = s_pos + S;
+      uint32_t head = 0, used = 0;
+      int oldest = 0;
+      for (int u = 0; u < (int)units; ++u) {
         const uint32_t bytes = (uint32_t)(s_off[u + 1] - s_off[u]);
-        mbar_expect_tx(bar_s + 8 * st, bytes);
-        bulk_g2s(ring_s + st * a.stage_bytes, a.data + s_off[u], bytes, bar_s + 8 * st, policy);
-        if (++st == S) { st = 0; ph ^= 1; }
+        uint32_t pos, gap;
+        for (;;) {
+          pos = head;
+          gap = 0;
+          if (head + bytes > R) { gap = R - head; pos = 0; }
+          if (used + gap + bytes <= R && u - oldest < S) break;
+          const int so = oldest % S;
+          mbar_wait(bar_s + 8 * (S + so), (uint32_t)(oldest / S) & 1u);
+          used -= s_alloc[so];
+          ++oldest;
+          if (used == 0) head = 0;
+        }
+        const int sl = u % S;
+        s_pos[sl] = pos;
+        s_alloc[sl] = gap + bytes;
+        used += gap + bytes;
+        head = pos + bytes;
+        mbar_expect_tx(bar_s + 8 * sl, bytes);
+        bulk_g2s(ring_s + pos, a.data + s_off[u], bytes, bar_s + 8 * sl, policy);
       }
     }
   } else {
@@ -276,8 +316,8 @@ __global__ void __launch_bounds__((CONS + 1) * 32, 1) k2_dl(DlArgs a) {
     long long Y1 = 0, Y2 = 0;
     int st = 0, slab = 0;
     uint32_t ph = 0;
-    int64_t lr = 0;
-    for (int64_t u = 0; u < units; ++u) {
+    int lr = 0;
+    for (int u = 0; u < (int)units; ++u) {
       if (lr == 0) {
         // new slab: x piece of this warp -> 23-bit fixed point (as k2_stream)
         bool finite = true;
@@ -324,20 +364,34 @@ __global__ void __launch_bounds__((CONS + 1) * 32, 1) k2_dl(DlArgs a) {
         Y2 = 0;
       }
       mbar_wait(bar_s + 8 * st, ph);
-      const unsigned char* sb = ring + (size_t)st * a.stage_bytes;
+      const uint32_t sbs = ring_s + s_pos[st];
       double part;
       if (!masked) {
         int32_t Sk[6] = {0, 0, 0, 0, 0, 0};
+        // chunk starts and plane 0 of every chunk first (independent loads)
+        uint32_t cs[SW], cw_[SW];
+#pragma unroll
+        for (int t = 0; t < SW; ++t) {
+          const int c = wc + t * CONS;
+          cs[t] = dl_lds_u8(sbs + c);
+          cw_[t] = dl_lds_u8(sbs + c + 1) - cs[t];
+        }
+        uint4 pl0[SW];
+#pragma unroll
+        for (int t = 0; t < SW; ++t)
+          pl0[t] = stepv[t] ? dl_lds128(sbs + DL_HDR + cs[t] * 512 + lane * 16) : make_uint4(0, 0, 0, 0);
 #pragma unroll
         for (int t = 0; t < SW; ++t) {
           if (!stepv[t]) continue;                      // warp-uniform
-          const int c = wc + t * CONS;
-          const int s0 = sb[c], w = sb[c + 1] - s0;
-          const unsigned char* p = sb + DL_HDR + s0 * 512 + lane * 16;
-          if (w == 1) dl_mac<1>(p, xd[t], Sk);
-          else if (w == 2) dl_mac<2>(p, xd[t], Sk);
-          else if (w == 3) dl_mac<3>(p, xd[t], Sk);
-          else dl_mac<4>(p, xd[t], Sk);
+          dl_plane<0>(pl0[t], xd[t], Sk);
+          const uint32_t pb = sbs + DL_HDR + cs[t] * 512 + lane * 16;
+          if (cw_[t] >= 2) {
+            dl_plane<1>(dl_lds128(pb + 512), xd[t], Sk);
+            if (cw_[t] >= 3) {
+              dl_plane<2>(dl_lds128(pb + 1024), xd[t], Sk);
+              if (cw_[t] >= 4) dl_plane<3>(dl_lds128(pb + 1536), xd[t], Sk);
+            }
+          }
         }
         long long acc = (long long)Sk[0] + ((long long)Sk[1] << 8) + ((long long)Sk[2] << 16) +
                         ((long long)Sk[3] << 24) + ((long long)Sk[4] << 32) + ((long long)Sk[5] << 40);
@@ -376,7 +430,7 @@ __global__ void __launch_bounds__((CONS + 1) * 32, 1) k2_dl(DlArgs a) {
         *sp = (slab == 0) ? part : (*sp + part);
       }
       if (++st == S) { st = 0; ph ^= 1; }
-      if (++lr == nrows) { lr = 0; ++slab; }
+      if (++lr == (int)nrows) { lr = 0; ++slab; }
     }
   }
   __syncthreads();
@@ -437,7 +491,7 @@ int dl_build(invop_plan* p, cudaStream_t s) {
   p->dl_bytes = total;
   p->dl_maxunit = (int64_t)mx;
   int rc = INVOP_OK;
-  const size_t need = 2 * (size_t)mx + dl_side_bytes(p, dl_consumers()) + 64;
+  const size_t need = 2 * (size_t)mx + dl_side_bytes(p, dl_consumers()) + DL_NS * 24 + 128;
   if (total >= (int64_t)p->P * p->rows * p->ld || need > 225 * 1024) {
     rc = INVOP_E_UNSUPPORTED;          // no gain over the byte planes / does not fit
   } else {
@@ -470,16 +524,13 @@ int apply_dl_launch(invop_plan* p, const float* x, float* y, cudaStream_t s) {
   a.nslabs = p->dl_nslabs;
   a.scale = p->scale;
   a.x = x; a.y = y;
-  a.stage_bytes = (int)round_up(p->dl_maxunit, 128);
   const int cons = dl_consumers();
-  const size_t side = dl_side_bytes(p, cons);
-  const int fit = (int)((225 * 1024 - (int64_t)side) / (a.stage_bytes + 16));
-  int stages = 3;
-  if (const char* v = getenv("INVOP_DL_STAGES")) stages = std::max(2, atoi(v));
-  stages = std::min(stages, fit);
-  if (stages < 2) return fail(INVOP_E_UNSUPPORTED, "k2_dl: not enough shared memory");
-  a.stages = stages;
-  const size_t smem = (size_t)stages * a.stage_bytes + 2 * stages * 8 + side;
+  const size_t side = dl_side_bytes(p, cons) + DL_NS * 24;
+  int64_t ring = (225 * 1024 - (int64_t)side) / 128 * 128;
+  if (const char* v = getenv("INVOP_DL_RING_KB")) ring = std::min<int64_t>(ring, atoi(v) * 1024);
+  if (ring < 2 * p->dl_maxunit) return fail(INVOP_E_UNSUPPORTED, "k2_dl: not enough shared memory");
+  a.ring_bytes = (int)ring;
+  const size_t smem = (size_t)ring + side;
   auto kern = cons == 8 ? k2_dl<8> : k2_dl<16>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   kern<<<p->dl_grid, (cons + 1) * 32, smem, s>>>(a);
