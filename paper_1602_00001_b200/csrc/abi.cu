@@ -173,7 +173,7 @@ extern "C" int invop_apply(const invop_plan* p, const void* x, int64_t ldx, void
       int rc = route == ROUTE_DL ? dl_build(mp, s) : route == ROUTE_HL ? hl_build(mp, s)
              : route == ROUTE_TVW ? tvw_build(mp, s) : vw_build(mp, s);
       if (rc == INVOP_OK) {
-        rc = route == ROUTE_DL ? apply_dl_launch(mp, (const float*)x, (float*)y, s)
+        rc = route == ROUTE_DL ? apply_dl_launch(mp, x, y, false, s)
            : route == ROUTE_HL ? apply_hl_launch(mp, (const float*)x, (float*)y, s)
            : route == ROUTE_TVW ? apply_tvw_launch(mp, (const float*)x, (float*)y, s)
                                 : apply_vw_launch(mp, (const float*)x, (float*)y, s);
@@ -234,6 +234,15 @@ __global__ void k_f32_to_f64(const float* __restrict__ a, double* __restrict__ b
     b[i] = (double)a[i];
 }
 
+static bool is_pinned(const void* ptr) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
 extern "C" int invop_apply_host(invop_plan* p, const double* x, double* y, int64_t nrhs,
                                 int mode, void* stream) {
   if (!p) return fail(INVOP_E_VALUE, "plan is NULL");
@@ -241,6 +250,24 @@ extern "C" int invop_apply_host(invop_plan* p, const double* x, double* y, int64
   cudaStream_t s = (cudaStream_t)stream;
   size_t xb = (size_t)nrhs * p->n * sizeof(double);
   size_t yb = (size_t)nrhs * p->rows * sizeof(double);
+  if (mode == INVOP_MODE_FAST && nrhs == 1 && fast_route(p, 1) == ROUTE_DL && is_pinned(y) &&
+      dl_build(p, s) == INVOP_OK) {
+    // page-locked y: the DL kernel writes its fp64 rows straight into host
+    // memory (each row once; zero copy), after one H2D copy of x (x is read by
+    // every CTA, so it is staged in device memory)
+    void* dyp = nullptr;
+    int rc = ensure_scratch(&p->dev_x, &p->dev_x_bytes, xb + 64);
+    if (rc) return rc;
+    if (cudaHostGetDevicePointer(&dyp, y, 0) == cudaSuccess) {
+      INVOP_CUDA(cudaMemcpyAsync(p->dev_x, x, xb, cudaMemcpyHostToDevice, s));
+      rc = apply_dl_launch(p, p->dev_x, dyp, true, s);
+      if (rc == INVOP_OK) {
+        INVOP_CUDA(cudaStreamSynchronize(s));
+        return INVOP_OK;
+      }
+    }
+    cudaGetLastError();
+  }
   // fp64 staging + fp32 copies for the fast path
   int rc = ensure_scratch(&p->dev_x, &p->dev_x_bytes, xb + xb / 2 + 64);
   if (rc) return rc;
@@ -252,6 +279,10 @@ extern "C" int invop_apply_host(invop_plan* p, const double* x, double* y, int64
   if (mode == INVOP_MODE_ORDERED) {
     rc = invop_apply(p, dx, p->n, dy, p->rows, nrhs, INVOP_F64, mode, stream);
     if (rc) return rc;
+  } else if (nrhs == 1 && fast_route(p, 1) == ROUTE_DL && dl_build(p, s) == INVOP_OK &&
+             apply_dl_launch(p, dx, dy, true, s) == INVOP_OK) {
+    // DL kernel reads the fp64 x and writes the fp64 y itself (same values as
+    // the fp32 path: x rounded to fp32 on load, y widened from fp32)
   } else {
     float* fx = (float*)((char*)p->dev_x + ((xb + 15) & ~(size_t)15));
     float* fy = (float*)((char*)p->dev_y + ((yb + 15) & ~(size_t)15));

@@ -214,8 +214,8 @@ struct DlArgs {
   int64_t rows, n, ld;
   int nslabs;
   double scale;
-  const float* x;
-  float* y;
+  const void* x;                // fp32, or fp64 when F64IO (rounded to fp32 on load)
+  void* y;                      // fp32, or fp64 when F64IO (the fp32 result widened)
   int ring_bytes;               // variable-size unit ring (FIFO) in shared memory
 };
 
@@ -244,7 +244,12 @@ __device__ __forceinline__ void dl_plane(const uint4& cw, const uint32_t (*xd)[4
     for (int d = 0; d < 3; ++d) S[B + d] = dp4a_ss(u4get(cw, k), xd[d][k], S[B + d]);
 }
 
-template <int CONS>
+template <bool F64IO>
+__device__ __forceinline__ float dl_x(const DlArgs& a, int64_t j) {
+  return F64IO ? (float)static_cast<const double*>(a.x)[j] : static_cast<const float*>(a.x)[j];
+}
+
+template <int CONS, bool F64IO>
 __global__ void __launch_bounds__((CONS + 1) * 32, 1) k2_dl(DlArgs a) {
   constexpr int SW = DL_SLAB / (CONS * 512);
   extern __shared__ __align__(128) unsigned char smem[];
@@ -319,7 +324,9 @@ __global__ void __launch_bounds__((CONS + 1) * 32, 1) k2_dl(DlArgs a) {
     int lr = 0;
     for (int u = 0; u < (int)units; ++u) {
       if (lr == 0) {
-        // new slab: x piece of this warp -> 23-bit fixed point (as k2_stream)
+        // new slab: x piece of this warp -> 23-bit fixed point (as k2_stream);
+        // x is read once (it may live in mapped host memory)
+        float xv[SW][16];
         bool finite = true;
         float mx = 0.0f;
 #pragma unroll
@@ -329,9 +336,9 @@ __global__ void __launch_bounds__((CONS + 1) * 32, 1) k2_dl(DlArgs a) {
           const int64_t c0 = col + lane * 16;
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
-            const float v = (stepv[t] && c0 + q < a.n) ? a.x[c0 + q] : 0.0f;
-            finite = finite && isfinite(v);
-            mx = fmaxf(mx, fabsf(v));
+            xv[t][q] = (stepv[t] && c0 + q < a.n) ? dl_x<F64IO>(a, c0 + q) : 0.0f;
+            finite = finite && isfinite(xv[t][q]);
+            mx = fmaxf(mx, fabsf(xv[t][q]));
           }
         }
         masked = __any_sync(0xffffffffu, !finite);
@@ -345,16 +352,11 @@ __global__ void __launch_bounds__((CONS + 1) * 32, 1) k2_dl(DlArgs a) {
         inv2e = ldexp(1.0, -e);
 #pragma unroll
         for (int t = 0; t < SW; ++t) {
-          const int64_t c0 = (int64_t)slab * DL_SLAB + (int64_t)(wc + t * CONS) * 512 + lane * 16;
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             int32_t X[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const int64_t col = c0 + 4 * k + i;
-              const float v = (stepv[t] && col < a.n) ? a.x[col] : 0.0f;
-              X[i] = masked ? 0 : __float2int_rn(ldexpf(v, e));
-            }
+            for (int i = 0; i < 4; ++i) X[i] = masked ? 0 : __float2int_rn(ldexpf(xv[t][4 * k + i], e));
             uint32_t dw[3];
             x_digits4(X, dw);
             xd[t][0][k] = dw[0]; xd[t][1][k] = dw[1]; xd[t][2][k] = dw[2];
@@ -419,7 +421,7 @@ __global__ void __launch_bounds__((CONS + 1) * 32, 1) k2_dl(DlArgs a) {
           dl_load16(a.planes, a.P, a.sgn, r * a.ld + c0, v);
           for (int q = 0; q < 16; ++q) {
             if (v[q] == 0 || c0 + q >= a.n) continue;
-            acc = fmaf((float)v[q], a.x[c0 + q], acc);
+            acc = fmaf((float)v[q], dl_x<F64IO>(a, c0 + q), acc);
           }
         }
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -438,7 +440,9 @@ __global__ void __launch_bounds__((CONS + 1) * 32, 1) k2_dl(DlArgs a) {
     double s = 0.0;
 #pragma unroll
     for (int c = 0; c < CONS; ++c) s += slot[r * CONS + c];
-    a.y[row_lo + r] = (float)(s * a.scale);
+    const float yv = (float)(s * a.scale);
+    if (F64IO) static_cast<double*>(a.y)[row_lo + r] = (double)yv;
+    else static_cast<float*>(a.y)[row_lo + r] = yv;
   }
 }
 
@@ -513,7 +517,7 @@ int dl_build(invop_plan* p, cudaStream_t s) {
   return INVOP_OK;
 }
 
-int apply_dl_launch(invop_plan* p, const float* x, float* y, cudaStream_t s) {
+int apply_dl_launch(invop_plan* p, const void* x, void* y, bool f64io, cudaStream_t s) {
   DlArgs a;
   a.data = p->dl_data;
   a.uoff = p->dl_uoff;
@@ -531,7 +535,8 @@ int apply_dl_launch(invop_plan* p, const float* x, float* y, cudaStream_t s) {
   if (ring < 2 * p->dl_maxunit) return fail(INVOP_E_UNSUPPORTED, "k2_dl: not enough shared memory");
   a.ring_bytes = (int)ring;
   const size_t smem = (size_t)ring + side;
-  auto kern = cons == 8 ? k2_dl<8> : k2_dl<16>;
+  auto kern = cons == 8 ? (f64io ? k2_dl<8, true> : k2_dl<8, false>)
+                        : (f64io ? k2_dl<16, true> : k2_dl<16, false>);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   kern<<<p->dl_grid, (cons + 1) * 32, smem, s>>>(a);
   INVOP_LAUNCHED(1);

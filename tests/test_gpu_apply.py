@@ -564,6 +564,18 @@ def test_dl_row_residuals(invop, O, amp, signed, N, monkeypatch):
     yo = O.ordered_apply(mant, 4, x.astype(np.float32).astype(np.float64))
     assert relerr(y_dl, yo) <= F32_TOL
     assert y_dl.tobytes() == y_st.tobytes()
+    # host fp64 entry: the DL kernel reads fp64 x / writes fp64 y itself
+    monkeypatch.setenv("INVOP_DL", "1")
+    yh = dplan.apply_host(x, mode=0)
+    assert yh.tobytes() == y_dl.astype(np.float64).tobytes()
+    # page-locked host buffers: zero-copy reads of x / writes of y by the kernel
+    import ctypes as C
+    from paper_1602_00001_b200 import _lib as L
+    xp = torch.from_numpy(x.copy()).pin_memory()
+    yp = torch.full((rows,), np.nan, dtype=torch.float64).pin_memory()
+    L.check(L.lib.invop_apply_host(dplan.handle, xp.data_ptr(), yp.data_ptr(), 1, 0,
+                                   C.c_void_p(torch.cuda.current_stream().cuda_stream)), "apply_host")
+    assert yp.numpy().tobytes() == yh.tobytes()
     # non-finite x in one warp piece: that piece reads the plain codes
     monkeypatch.setenv("INVOP_DL", "1")
     col = 1000
