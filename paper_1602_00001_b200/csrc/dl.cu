@@ -322,7 +322,7 @@ __global__ void __launch_bounds__((CONS + 1) * 32, 1) k2_dl(DlArgs a) {
     int st = 0, slab = 0;
     uint32_t ph = 0;
     int lr = 0;
-    for (int u = 0; u < (int)units; ++u) {
+    for (int u = 0; u < (int)units;) {
       if (lr == 0) {
         // new slab: x piece of this warp -> 23-bit fixed point (as k2_stream);
         // x is read once (it may live in mapped host memory)
@@ -365,48 +365,89 @@ __global__ void __launch_bounds__((CONS + 1) * 32, 1) k2_dl(DlArgs a) {
         Y1 = 0;
         Y2 = 0;
       }
+      // two rows per iteration when both are in this slab: their loads, DP4As
+      // and warp sums interleave (the per-row chain is latency bound)
+      const bool two = !masked && lr + 1 < (int)nrows;
+      const int stB = st + 1 == S ? 0 : st + 1;
+      const uint32_t phB = st + 1 == S ? ph ^ 1u : ph;
       mbar_wait(bar_s + 8 * st, ph);
-      const uint32_t sbs = ring_s + s_pos[st];
-      double part;
+      if (two) mbar_wait(bar_s + 8 * stB, phB);
       if (!masked) {
-        int32_t Sk[6] = {0, 0, 0, 0, 0, 0};
-        // chunk starts and plane 0 of every chunk first (independent loads)
-        uint32_t cs[SW], cw_[SW];
+        const uint32_t sbA = ring_s + s_pos[st];
+        const uint32_t sbB = ring_s + s_pos[two ? stB : st];
+        uint32_t csA[SW], wA[SW], csB[SW], wB[SW];
 #pragma unroll
         for (int t = 0; t < SW; ++t) {
           const int c = wc + t * CONS;
-          cs[t] = dl_lds_u8(sbs + c);
-          cw_[t] = dl_lds_u8(sbs + c + 1) - cs[t];
+          csA[t] = dl_lds_u8(sbA + c);
+          wA[t] = dl_lds_u8(sbA + c + 1) - csA[t];
+          csB[t] = dl_lds_u8(sbB + c);
+          wB[t] = dl_lds_u8(sbB + c + 1) - csB[t];
         }
-        uint4 pl0[SW];
+        uint4 pA[SW], pB[SW];
 #pragma unroll
-        for (int t = 0; t < SW; ++t)
-          pl0[t] = stepv[t] ? dl_lds128(sbs + DL_HDR + cs[t] * 512 + lane * 16) : make_uint4(0, 0, 0, 0);
+        for (int t = 0; t < SW; ++t) {
+          pA[t] = stepv[t] ? dl_lds128(sbA + DL_HDR + csA[t] * 512 + lane * 16) : make_uint4(0, 0, 0, 0);
+          pB[t] = stepv[t] ? dl_lds128(sbB + DL_HDR + csB[t] * 512 + lane * 16) : make_uint4(0, 0, 0, 0);
+        }
+        int32_t SA[6] = {0, 0, 0, 0, 0, 0}, SB[6] = {0, 0, 0, 0, 0, 0};
+#pragma unroll
+        for (int t = 0; t < SW; ++t) {
+          dl_plane<0>(pA[t], xd[t], SA);
+          dl_plane<0>(pB[t], xd[t], SB);
+        }
 #pragma unroll
         for (int t = 0; t < SW; ++t) {
           if (!stepv[t]) continue;                      // warp-uniform
-          dl_plane<0>(pl0[t], xd[t], Sk);
-          const uint32_t pb = sbs + DL_HDR + cs[t] * 512 + lane * 16;
-          if (cw_[t] >= 2) {
-            dl_plane<1>(dl_lds128(pb + 512), xd[t], Sk);
-            if (cw_[t] >= 3) {
-              dl_plane<2>(dl_lds128(pb + 1024), xd[t], Sk);
-              if (cw_[t] >= 4) dl_plane<3>(dl_lds128(pb + 1536), xd[t], Sk);
+          const uint32_t pa = sbA + DL_HDR + csA[t] * 512 + lane * 16;
+          if (wA[t] >= 2) {
+            dl_plane<1>(dl_lds128(pa + 512), xd[t], SA);
+            if (wA[t] >= 3) {
+              dl_plane<2>(dl_lds128(pa + 1024), xd[t], SA);
+              if (wA[t] >= 4) dl_plane<3>(dl_lds128(pa + 1536), xd[t], SA);
+            }
+          }
+          const uint32_t pbb = sbB + DL_HDR + csB[t] * 512 + lane * 16;
+          if (wB[t] >= 2) {
+            dl_plane<1>(dl_lds128(pbb + 512), xd[t], SB);
+            if (wB[t] >= 3) {
+              dl_plane<2>(dl_lds128(pbb + 1024), xd[t], SB);
+              if (wB[t] >= 4) dl_plane<3>(dl_lds128(pbb + 1536), xd[t], SB);
             }
           }
         }
-        long long acc = (long long)Sk[0] + ((long long)Sk[1] << 8) + ((long long)Sk[2] << 16) +
-                        ((long long)Sk[3] << 24) + ((long long)Sk[4] << 32) + ((long long)Sk[5] << 40);
         __syncwarp();
-        if (lane == 0) mbar_arrive(bar_s + 8 * (S + st));
-        // exact warp sum: |e| < 2^25, |X| <= 2^22, 32 codes per lane -> |acc| < 2^52
-        const uint32_t slo = __reduce_add_sync(0xffffffffu, (uint32_t)acc & 0x7FFFFFFu);
-        const int32_t shi = __reduce_add_sync(0xffffffffu, (int32_t)(acc >> 27));
-        const long long D = ((long long)shi << 27) + (long long)slo;
-        const long long Y = D + (lr >= 2 ? 2 * Y1 - Y2 : (lr == 1 ? Y1 : 0));
+        if (lane == 0) {
+          mbar_arrive(bar_s + 8 * (S + st));
+          if (two) mbar_arrive(bar_s + 8 * (S + stB));
+        }
+        const long long accA = (long long)SA[0] + ((long long)SA[1] << 8) + ((long long)SA[2] << 16) +
+                               ((long long)SA[3] << 24) + ((long long)SA[4] << 32) + ((long long)SA[5] << 40);
+        const long long accB = (long long)SB[0] + ((long long)SB[1] << 8) + ((long long)SB[2] << 16) +
+                               ((long long)SB[3] << 24) + ((long long)SB[4] << 32) + ((long long)SB[5] << 40);
+        // exact warp sums: |e| < 2^25, |X| <= 2^22, 32 codes per lane -> |acc| < 2^52
+        const uint32_t loA = __reduce_add_sync(0xffffffffu, (uint32_t)accA & 0x7FFFFFFu);
+        const int32_t hiA = __reduce_add_sync(0xffffffffu, (int32_t)(accA >> 27));
+        const uint32_t loB = __reduce_add_sync(0xffffffffu, (uint32_t)accB & 0x7FFFFFFu);
+        const int32_t hiB = __reduce_add_sync(0xffffffffu, (int32_t)(accB >> 27));
+        const long long DA = ((long long)hiA << 27) + (long long)loA;
+        const long long DB = ((long long)hiB << 27) + (long long)loB;
+        const long long YA = DA + (lr >= 2 ? 2 * Y1 - Y2 : (lr == 1 ? Y1 : 0));
         Y2 = Y1;
-        Y1 = Y;
-        part = (double)Y * inv2e;
+        Y1 = YA;
+        if (lane == 0) {
+          double* sp = &slot[lr * CONS + wc];
+          *sp = (slab == 0) ? (double)YA * inv2e : (*sp + (double)YA * inv2e);
+        }
+        if (two) {
+          const long long YB = DB + (lr + 1 >= 2 ? 2 * Y1 - Y2 : Y1);
+          Y2 = Y1;
+          Y1 = YB;
+          if (lane == 0) {
+            double* sp = &slot[(lr + 1) * CONS + wc];
+            *sp = (slab == 0) ? (double)YB * inv2e : (*sp + (double)YB * inv2e);
+          }
+        }
       } else {
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_s + 8 * (S + st));
@@ -425,14 +466,22 @@ __global__ void __launch_bounds__((CONS + 1) * 32, 1) k2_dl(DlArgs a) {
           }
         }
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        part = (double)acc;
+        if (lane == 0) {
+          double* sp = &slot[lr * CONS + wc];
+          *sp = (slab == 0) ? (double)acc : (*sp + (double)acc);
+        }
       }
-      if (lane == 0) {
-        double* sp = &slot[lr * CONS + wc];
-        *sp = (slab == 0) ? part : (*sp + part);
+      if (two) {
+        st = stB == S - 1 ? 0 : stB + 1;
+        ph = stB == S - 1 ? phB ^ 1u : phB;
+        u += 2;
+        lr += 2;
+      } else {
+        if (++st == S) { st = 0; ph ^= 1; }
+        u += 1;
+        lr += 1;
       }
-      if (++st == S) { st = 0; ph ^= 1; }
-      if (++lr == (int)nrows) { lr = 0; ++slab; }
+      if (lr == (int)nrows) { lr = 0; ++slab; }
     }
   }
   __syncthreads();
@@ -495,7 +544,7 @@ int dl_build(invop_plan* p, cudaStream_t s) {
   p->dl_bytes = total;
   p->dl_maxunit = (int64_t)mx;
   int rc = INVOP_OK;
-  const size_t need = 2 * (size_t)mx + dl_side_bytes(p, dl_consumers()) + DL_NS * 24 + 128;
+  const size_t need = 3 * (size_t)mx + dl_side_bytes(p, dl_consumers()) + DL_NS * 24 + 128;
   if (total >= (int64_t)p->P * p->rows * p->ld || need > 225 * 1024) {
     rc = INVOP_E_UNSUPPORTED;          // no gain over the byte planes / does not fit
   } else {
@@ -532,7 +581,9 @@ int apply_dl_launch(invop_plan* p, const void* x, void* y, bool f64io, cudaStrea
   const size_t side = dl_side_bytes(p, cons) + DL_NS * 24;
   int64_t ring = (225 * 1024 - (int64_t)side) / 128 * 128;
   if (const char* v = getenv("INVOP_DL_RING_KB")) ring = std::min<int64_t>(ring, atoi(v) * 1024);
-  if (ring < 2 * p->dl_maxunit) return fail(INVOP_E_UNSUPPORTED, "k2_dl: not enough shared memory");
+  // consumers take two consecutive units at once: with a ring of >= 3 max
+  // units, any two consecutive units fit side by side after a wrap
+  if (ring < 3 * p->dl_maxunit) return fail(INVOP_E_UNSUPPORTED, "k2_dl: not enough shared memory");
   a.ring_bytes = (int)ring;
   const size_t smem = (size_t)ring + side;
   auto kern = cons == 8 ? (f64io ? k2_dl<8, true> : k2_dl<8, false>)
