@@ -80,6 +80,9 @@ extern "C" int invop_plan_destroy(invop_plan* p) {
   if (p->tv_ws) cudaFree(p->tv_ws);
   if (p->hl_data) cudaFree(p->hl_data);
   if (p->hl_rowptr) cudaFree(p->hl_rowptr);
+  for (int b = 0; b < 2; ++b)
+    if (p->k3d_tiles[b]) cudaFree(p->k3d_tiles[b]);
+  if (p->k3d_idx1) cudaFree(p->k3d_idx1);
   if (p->dl_data) cudaFree(p->dl_data);
   if (p->dl_uoff) cudaFree(p->dl_uoff);
   if (p->host_pinned) cudaFreeHost(p->host_pinned);
@@ -132,7 +135,7 @@ extern "C" const char* invop_apply_kernel(const invop_plan* p, int64_t nrhs, int
   if (!p) return "";
   if (mode == INVOP_MODE_ORDERED) return "k2_ordered";
   switch (fast_route(p, nrhs)) {
-    case ROUTE_K3: return "k3_batched";
+    case ROUTE_K3: return p->k3d_ready > 0 ? "k3_batched_dl" : "k3_batched";
     case ROUTE_DL: return "k2_dl";
     case ROUTE_HL: return "k2_hl";
     case ROUTE_TVW: return "k2_tvw";
@@ -199,6 +202,10 @@ extern "C" int invop_plan_apply_bytes(invop_plan* p, int64_t nrhs, int mode, int
   cudaStream_t s = (cudaStream_t)stream;
   if (mode == INVOP_MODE_FAST) {
     const int route = fast_route(p, nrhs);
+    if (route == ROUTE_K3 && k3d_bytes(p) > 0) {
+      *bytes = k3d_bytes(p);
+      return INVOP_OK;
+    }
     int rc = route == ROUTE_DL ? dl_build(p, s) : route == ROUTE_HL ? hl_build(p, s)
            : route == ROUTE_TVW ? tvw_build(p, s) : route == ROUTE_VW ? vw_build(p, s)
            : INVOP_E_UNSUPPORTED;

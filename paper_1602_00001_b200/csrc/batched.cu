@@ -36,6 +36,12 @@
 
 namespace invop {
 
+static bool layout_flag(const char* env, bool dflt) {
+  const char* v = getenv(env);
+  if (!v || !*v) return dflt;
+  return *v != '0';
+}
+
 constexpr int K3_BM = 128;            // rows per MMA tile
 constexpr int K3_TILES = 2;           // row tiles per work unit (share B)
 constexpr int K3_BK = 64;             // K bytes per stage (SWIZZLE_64B row)
@@ -61,7 +67,8 @@ struct K3Args {
   double scale;
   float* y;
   int64_t ldy;
-  long long* yacc;         // [64][rows] when splits > 1
+  long long* yacc;         // [64][rows] when splits > 1 (DL: always; holds D)
+  const int* idx1;         // DL: compact index of a tile's digit-1 plane, -1 if absent
 };
 
 // ------------------------------------------------------------ PTX helpers
@@ -165,7 +172,11 @@ __host__ __device__ constexpr uint32_t idesc_i8(int a_signed) {
 }
 
 // ------------------------------------------------------------ main kernel
-template <int P, int TILES, int STAGES>
+// DL = true: A holds the balanced base-256 digits of second-order row
+// residuals (both planes signed; the digit-1 plane of a tile is present only
+// where a residual needs it, idx1 >= 0), and the epilogue writes the exact
+// int64 D = E X for the double prefix sum along rows (k3d_scan).
+template <int P, int TILES, int STAGES, bool DL>
 __global__ void __launch_bounds__(K3_THREADS, 1)
     k3_batched(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapA1,
                const __grid_constant__ CUtensorMap mapB, K3Args a) {
@@ -176,6 +187,15 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
   unsigned char* base = (unsigned char*)(((uintptr_t)k3s + 1023) & ~(uintptr_t)1023);
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], tfull, tempty;
   __shared__ uint32_t tmem_slot;
+  __shared__ uint32_t s_mask[STAGES];                       // DL: tiles whose digit-1 plane is loaded
+  // DL: an all-zero A tile after the stages (initialises the accumulator that
+  // only digit-1 planes feed when the unit's first K block has none)
+  unsigned char* zero_tile = base + (size_t)STAGES * STAGE;
+  if (DL) {
+    for (int i = threadIdx.x; i < K3_A_TILE / 16; i += blockDim.x)
+      reinterpret_cast<uint4*>(zero_tile)[i] = make_uint4(0, 0, 0, 0);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -223,13 +243,31 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
           if (it >= STAGES) k3_wait(smem_u32(&empty[st]), ph ^ 1);
           const uint32_t sb = smem_u32(base + (size_t)st * STAGE);
           const uint32_t fb = smem_u32(&full[st]);
-          k3_expect_tx(fb, STAGE);
+          if (DL) {
+            int i1[TILES];
+            uint32_t mask = 0, bytes = TILES * K3_A_TILE + K3_ND * K3_B_TILE;
 #pragma unroll
-          for (int ti = 0; ti < TILES; ++ti) {
-            // tiled planes: tile (rt, kb) starts at tensor row (rt*kblocks + kb)*128
-            const int trow = (int)(((int64_t)(row0 / K3_BM + ti) * a.kb_stride + kb) * K3_BM);
-            tma_2d(sb + (ti * P + 0) * K3_A_TILE, &mapA0, 0, trow, fb, pol_a);
-            if (P > 1) tma_2d(sb + (ti * P + 1) * K3_A_TILE, &mapA1, 0, trow, fb, pol_a);
+            for (int ti = 0; ti < TILES; ++ti) {
+              i1[ti] = a.idx1[(int64_t)(row0 / K3_BM + ti) * a.kb_stride + kb];
+              if (i1[ti] >= 0) { mask |= 1u << ti; bytes += K3_A_TILE; }
+            }
+            s_mask[st] = mask;
+            k3_expect_tx(fb, bytes);
+#pragma unroll
+            for (int ti = 0; ti < TILES; ++ti) {
+              const int trow = (int)(((int64_t)(row0 / K3_BM + ti) * a.kb_stride + kb) * K3_BM);
+              tma_2d(sb + (ti * P + 0) * K3_A_TILE, &mapA0, 0, trow, fb, pol_a);
+              if (i1[ti] >= 0) tma_2d(sb + (ti * P + 1) * K3_A_TILE, &mapA1, 0, i1[ti] * K3_BM, fb, pol_a);
+            }
+          } else {
+            k3_expect_tx(fb, STAGE);
+#pragma unroll
+            for (int ti = 0; ti < TILES; ++ti) {
+              // tiled planes: tile (rt, kb) starts at tensor row (rt*kblocks + kb)*128
+              const int trow = (int)(((int64_t)(row0 / K3_BM + ti) * a.kb_stride + kb) * K3_BM);
+              tma_2d(sb + (ti * P + 0) * K3_A_TILE, &mapA0, 0, trow, fb, pol_a);
+              if (P > 1) tma_2d(sb + (ti * P + 1) * K3_A_TILE, &mapA1, 0, trow, fb, pol_a);
+            }
           }
 #pragma unroll
           for (int l = 0; l < K3_ND; ++l)
@@ -258,11 +296,14 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
           // descriptors: one base per stage plus compile-time offsets (>> 4)
           const uint32_t sb = smem_u32(base + (size_t)st * STAGE);
           const uint64_t dbase = desc_sw64(sb);
-          const uint32_t id_lo = idesc_i8(0), id_hi = idesc_i8(a.hi_signed);
+          const uint64_t dzero = desc_sw64(smem_u32(zero_tile));
+          const uint32_t id_lo = idesc_i8(DL ? 1 : 0), id_hi = idesc_i8(DL ? 1 : a.hi_signed);
+          const uint32_t mask = DL ? s_mask[st] : 0xffffffffu;
 #pragma unroll
           for (int kk = 0; kk < K3_BK / 32; ++kk) {
 #pragma unroll
             for (int ti = 0; ti < TILES; ++ti) {
+              const bool have1 = (mask >> ti) & 1u;          // warp-uniform
 #pragma unroll
               for (int w = 0; w < NACC; ++w) {
 #pragma unroll
@@ -272,7 +313,12 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
                   // first product of weight w at the unit's first K step starts the accumulator
                   const bool first_pair = (p == (w < K3_ND ? 0 : w - K3_ND + 1));
                   const uint32_t acc = (i > 0 || kk > 0 || !first_pair) ? 1u : 0u;
-                  const uint64_t da = dbase + (uint64_t)(((ti * P + p) * K3_A_TILE + kk * 32) >> 4);
+                  uint64_t da = dbase + (uint64_t)(((ti * P + p) * K3_A_TILE + kk * 32) >> 4);
+                  if (DL && p == 1 && !have1) {
+                    // plane absent: only the accumulator start it owns is needed
+                    if (acc) continue;
+                    da = dzero + (uint64_t)((kk * 32) >> 4);
+                  }
                   const uint64_t db = dbase + (uint64_t)((A_BYTES + l * K3_B_TILE + kk * 32) >> 4);
                   mma_i8_elect(tmem + (uint32_t)((ti * NACC + w) * K3_NR), da, db,
                                (p == P - 1) ? id_hi : id_lo, acc);
@@ -315,7 +361,9 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
               long long v = 0;
 #pragma unroll
               for (int w = 0; w < NACC; ++w) v += (long long)r[w][j] * (1LL << (8 * w));
-              if (a.splits == 1) {
+              if (DL && a.splits == 1) {
+                a.yacc[(int64_t)t * a.rows + row] = v;
+              } else if (a.splits == 1) {
                 a.y[(int64_t)t * a.ldy + row] = (float)((double)v * ldexp(a.scale, -a.e[t]));
               } else {
                 atomicAdd((unsigned long long*)&a.yacc[(int64_t)t * a.rows + row],
@@ -422,6 +470,223 @@ __global__ void k3_finalize(const long long* __restrict__ yacc, int64_t rows, in
   }
 }
 
+// ------------------------------------------------------------ K3 on row residuals
+// Residual of plan row r (plan-local): e_r = v_r - 2 v_{r-1} + v_{r-2} for
+// r >= 2; rows 0 and 1 are stored as zero and their sums computed exactly from
+// the codes (k3d_rows01), so D_0 = Y_0, D_1 = Y_1 - 2 Y_0 and Y is the double
+// prefix sum of D along rows (k3d_scan). Digits are balanced base-256.
+__device__ __forceinline__ int32_t k3d_code(const uint8_t* const* planes, int P, int sgn,
+                                            int64_t off) {
+  uint32_t u = 0;
+  for (int b = 0; b < P; ++b) u |= (uint32_t)planes[b][off] << (8 * b);
+  const int sh = 32 - 8 * P;
+  return sgn ? ((int32_t)(u << sh) >> sh) : (int32_t)u;
+}
+
+struct K3DBuild {
+  const uint8_t* planes[2];
+  int P, sgn;
+  int64_t rows, ld;
+  int64_t kbs, rtiles;
+};
+
+__device__ __forceinline__ int32_t k3d_resid(const K3DBuild& a, int64_t r, int64_t j) {
+  if (r < 2 || r >= a.rows) return 0;
+  const int64_t off = r * a.ld + j;
+  return k3d_code(a.planes, a.P, a.sgn, off) - 2 * k3d_code(a.planes, a.P, a.sgn, off - a.ld) +
+         k3d_code(a.planes, a.P, a.sgn, off - 2 * a.ld);
+}
+
+// one thread per (row, K block): digit count of its 64 residuals -> tile max
+__global__ void k3d_width(K3DBuild a, int* __restrict__ tilew, int* __restrict__ wmax) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= a.rows * a.kbs) return;
+  const int64_t r = t / a.kbs, kb = t - r * a.kbs;
+  int w = 1;
+  for (int q = 0; q < K3_BK; ++q) {
+    int32_t e = k3d_resid(a, r, kb * K3_BK + q);
+    int n = 1;
+    for (;;) {
+      const int32_t d = ((e + 128) & 255) - 128;
+      e = (e - d) >> 8;
+      if (e == 0) break;
+      ++n;
+    }
+    w = max(w, n);
+  }
+  atomicMax(&tilew[(r / K3_BM) * a.kbs + kb], w);
+  atomicMax(wmax, w);
+}
+
+// compact index of the tiles that need a digit-1 plane (one block)
+__global__ void k3d_index(int64_t tiles, const int* __restrict__ tilew, int* __restrict__ idx1,
+                          int64_t* __restrict__ n1) {
+  __shared__ int64_t part[1024];
+  const int t = threadIdx.x, T = blockDim.x;
+  const int64_t per = (tiles + T - 1) / T;
+  const int64_t a0 = t * per, a1 = min(tiles, a0 + per);
+  int64_t c = 0;
+  for (int64_t i = a0; i < a1; ++i) c += tilew[i] >= 2;
+  part[t] = c;
+  __syncthreads();
+  if (t == 0) {
+    int64_t acc = 0;
+    for (int i = 0; i < T; ++i) { const int64_t v = part[i]; part[i] = acc; acc += v; }
+    *n1 = acc;
+  }
+  __syncthreads();
+  int64_t acc = part[t];
+  for (int64_t i = a0; i < a1; ++i) idx1[i] = tilew[i] >= 2 ? (int)acc++ : -1;
+}
+
+// one thread per (row, K block): write the residual digits into the tiles
+__global__ void k3d_write(K3DBuild a, const int* __restrict__ idx1, uint8_t* __restrict__ t0,
+                          uint8_t* __restrict__ t1) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= a.rows * a.kbs) return;
+  const int64_t r = t / a.kbs, kb = t - r * a.kbs;
+  const int64_t tile = (r / K3_BM) * a.kbs + kb;
+  const int i1 = idx1[tile];
+  uint8_t* d0 = t0 + tile * K3_A_TILE + (r % K3_BM) * K3_BK;
+  uint8_t* d1 = i1 >= 0 ? t1 + (int64_t)i1 * K3_A_TILE + (r % K3_BM) * K3_BK : nullptr;
+  for (int q0 = 0; q0 < K3_BK; q0 += 16) {
+    uint32_t w0[4] = {0, 0, 0, 0}, w1[4] = {0, 0, 0, 0};
+    for (int q = 0; q < 16; ++q) {
+      const int32_t e = k3d_resid(a, r, kb * K3_BK + q0 + q);
+      const int32_t g0 = ((e + 128) & 255) - 128;
+      const int32_t g1 = (e - g0) >> 8;
+      w0[q >> 2] |= ((uint32_t)g0 & 255u) << (8 * (q & 3));
+      w1[q >> 2] |= ((uint32_t)g1 & 255u) << (8 * (q & 3));
+    }
+    *reinterpret_cast<uint4*>(d0 + q0) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
+    if (d1) *reinterpret_cast<uint4*>(d1 + q0) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
+  }
+}
+
+// exact Y_0, Y_1 from the plain codes and the same x digits, added as
+// D_0 += Y_0, D_1 += Y_1 - 2 Y_0 (linear, so column pieces add atomically;
+// the tensor-core pass left 0 in both rows). grid = (column pieces, RHS),
+// 16 columns per thread
+__global__ void k3d_rows01(const uint8_t* p0, const uint8_t* p1, int P, int sgn, int64_t n,
+                           int64_t ld, int64_t rows, const int8_t* __restrict__ B, int64_t ldb,
+                           long long* __restrict__ yacc) {
+  const int t = blockIdx.y;
+  const int64_t j0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 16;
+  long long s0 = 0, s1 = 0;
+  if (j0 < n) {
+    const uint4 g0 = *reinterpret_cast<const uint4*>(B + (0 * K3_NR + t) * ldb + j0);
+    const uint4 g1 = *reinterpret_cast<const uint4*>(B + (1 * K3_NR + t) * ldb + j0);
+    const uint4 g2 = *reinterpret_cast<const uint4*>(B + (2 * K3_NR + t) * ldb + j0);
+    const uint4 a0 = *reinterpret_cast<const uint4*>(p0 + j0);
+    const uint4 a1 = P > 1 ? *reinterpret_cast<const uint4*>(p1 + j0) : make_uint4(0, 0, 0, 0);
+    const uint4 b0 = rows > 1 ? *reinterpret_cast<const uint4*>(p0 + ld + j0) : make_uint4(0, 0, 0, 0);
+    const uint4 b1 = (rows > 1 && P > 1) ? *reinterpret_cast<const uint4*>(p1 + ld + j0)
+                                         : make_uint4(0, 0, 0, 0);
+    const uint32_t G0[4] = {g0.x, g0.y, g0.z, g0.w}, G1[4] = {g1.x, g1.y, g1.z, g1.w},
+                   G2[4] = {g2.x, g2.y, g2.z, g2.w}, A0[4] = {a0.x, a0.y, a0.z, a0.w},
+                   A1[4] = {a1.x, a1.y, a1.z, a1.w}, B0[4] = {b0.x, b0.y, b0.z, b0.w},
+                   B1[4] = {b1.x, b1.y, b1.z, b1.w};
+    const int sh = 32 - 8 * P;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int w = q >> 2, bb = 8 * (q & 3);
+      const long long X = (long long)(int8_t)(G0[w] >> bb) + 256LL * (int8_t)(G1[w] >> bb) +
+                          65536LL * (int8_t)(G2[w] >> bb);
+      uint32_t u0 = ((A0[w] >> bb) & 255u) | (((A1[w] >> bb) & 255u) << 8);
+      uint32_t u1 = ((B0[w] >> bb) & 255u) | (((B1[w] >> bb) & 255u) << 8);
+      const int32_t v0 = sgn ? ((int32_t)(u0 << sh) >> sh) : (int32_t)u0;
+      const int32_t v1 = sgn ? ((int32_t)(u1 << sh) >> sh) : (int32_t)u1;
+      s0 += (long long)v0 * X;
+      s1 += (long long)v1 * X;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd((unsigned long long*)&yacc[(int64_t)t * rows], (unsigned long long)s0);
+    if (rows > 1)
+      atomicAdd((unsigned long long*)&yacc[(int64_t)t * rows + 1], (unsigned long long)(s1 - 2 * s0));
+  }
+}
+
+// Y = double prefix sum of D along rows, exact in int64, in segments of
+// K3D_SEG rows: pass 1 gives per segment (sum D, sum z_local) with z_local the
+// segment-local first prefix; the carries (Z_in, Y_in) follow sequentially per
+// RHS; pass 2 rebuilds y_r = y_local + (r - r0 + 1) Z_in + Y_in and scales.
+constexpr int K3D_SEG = 1024;
+
+__device__ __forceinline__ long long k3d_block_incl(long long v, long long* sh) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  long long inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long u = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += u;
+  }
+  if (lane == 31) sh[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    long long s = sh[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long u = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += u;
+    }
+    sh[lane] = s;
+  }
+  __syncthreads();
+  const long long r = inc + (w > 0 ? sh[w - 1] : 0);
+  __syncthreads();
+  return r;
+}
+
+// grid = (segments, RHS), 1024 threads: one row per thread
+__global__ void __launch_bounds__(K3D_SEG) k3d_seg_sums(const long long* __restrict__ yacc,
+                                                        int64_t rows, long long* __restrict__ seg) {
+  __shared__ long long sh[32];
+  const int t = blockIdx.y;
+  const int64_t r = (int64_t)blockIdx.x * K3D_SEG + threadIdx.x;
+  const long long d = r < rows ? yacc[(int64_t)t * rows + r] : 0;
+  const long long z = k3d_block_incl(d, sh);          // local first prefix
+  const long long zs = k3d_block_incl(z, sh);         // its prefix: local y
+  if (threadIdx.x == K3D_SEG - 1) {
+    seg[((int64_t)t * gridDim.x + blockIdx.x) * 2 + 0] = z;    // sum of D
+    seg[((int64_t)t * gridDim.x + blockIdx.x) * 2 + 1] = zs;   // sum of z_local
+  }
+}
+
+// one thread per RHS: segment carries in place, (sum D, sum z) -> (Z_in, Y_in)
+__global__ void k3d_seg_carry(long long* __restrict__ seg, int nseg, int nrhs) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nrhs) return;
+  long long Z = 0, Y = 0;
+  for (int k = 0; k < nseg; ++k) {
+    long long* p = seg + ((int64_t)t * nseg + k) * 2;
+    const long long sd = p[0], sz = p[1];
+    p[0] = Z;
+    p[1] = Y;
+    Y += (long long)K3D_SEG * Z + sz;   // y at segment end
+    Z += sd;
+  }
+}
+
+__global__ void __launch_bounds__(K3D_SEG) k3d_seg_apply(const long long* __restrict__ yacc,
+                                                         int64_t rows, const long long* __restrict__ seg,
+                                                         const int* __restrict__ e, double scale,
+                                                         float* __restrict__ y, int64_t ldy) {
+  __shared__ long long sh[32];
+  const int t = blockIdx.y;
+  const int64_t r = (int64_t)blockIdx.x * K3D_SEG + threadIdx.x;
+  const long long d = r < rows ? yacc[(int64_t)t * rows + r] : 0;
+  const long long z = k3d_block_incl(d, sh);
+  const long long yl = k3d_block_incl(z, sh);
+  const long long* c = seg + ((int64_t)t * gridDim.x + blockIdx.x) * 2;
+  const long long Y = yl + (long long)(threadIdx.x + 1) * c[0] + c[1];
+  if (r < rows) y[(int64_t)t * ldy + r] = (float)((double)Y * ldexp(scale, -e[t]));
+}
+
 // ------------------------------------------------------------ host side
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                     const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -460,16 +725,85 @@ bool batched_supported(const invop_plan* p, int64_t nrhs) {
   return p->P <= 2 && nrhs >= 8 && p->n >= K3_BK && p->rows >= 1 && encode_fn() != nullptr;
 }
 
-template <int P, int TILES, int STAGES>
+template <int P, int TILES, int STAGES, bool DL = false>
 static int launch_k3(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b,
                      const K3Args& args, int grid, cudaStream_t s) {
   constexpr int STAGE = TILES * P * K3_A_TILE + K3_ND * K3_B_TILE;
-  size_t smem = (size_t)STAGES * STAGE + 1024;
-  auto kern = k3_batched<P, TILES, STAGES>;
+  size_t smem = (size_t)STAGES * STAGE + 1024 + (DL ? K3_A_TILE : 0);
+  auto kern = k3_batched<P, TILES, STAGES, DL>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   kern<<<grid, K3_THREADS, smem, s>>>(a0, a1, b, args);
   INVOP_CHECK_LAUNCH("k3_batched");
   return INVOP_OK;
+}
+
+// residual tiles for the K3 DL path; declined (k3d_ready = -1) when some
+// residual needs a third digit or the layout would not be smaller
+static int k3d_build(invop_plan* p, cudaStream_t s) {
+  if (p->k3d_ready) return p->k3d_ready > 0 ? INVOP_OK : INVOP_E_UNSUPPORTED;
+  p->k3d_ready = -1;
+  if (p->P > 2 || p->rows < 4 || !layout_flag("INVOP_K3_DL", true)) return INVOP_E_UNSUPPORTED;
+  K3DBuild a;
+  a.planes[0] = p->planes[0];
+  a.planes[1] = p->planes[p->P > 1 ? 1 : 0];
+  a.P = p->P;
+  a.sgn = p->is_signed;
+  a.rows = p->rows;
+  a.ld = p->ld;
+  a.kbs = p->ld / K3_BK;
+  a.rtiles = round_up(cdiv(p->rows, K3_BM), 2);
+  const int64_t tiles = a.rtiles * a.kbs;
+  int* tilew = nullptr;
+  int64_t* n1d = nullptr;
+  INVOP_CUDA(cudaMalloc(&tilew, (size_t)tiles * 4 + 16));
+  INVOP_CUDA(cudaMalloc(&n1d, 16));
+  int* wmaxd = tilew + tiles;
+  INVOP_CUDA(cudaMemsetAsync(tilew, 0, (size_t)tiles * 4 + 16, s));
+  const int64_t thr = p->rows * a.kbs;
+  k3d_width<<<(unsigned)cdiv(thr, 256), 256, 0, s>>>(a, tilew, wmaxd);
+  int wmax = 0;
+  INVOP_CUDA(cudaMemcpyAsync(&wmax, wmaxd, 4, cudaMemcpyDeviceToHost, s));
+  INVOP_CUDA(cudaStreamSynchronize(s));
+  int rc = INVOP_E_UNSUPPORTED;
+  if (wmax <= 2) {
+    INVOP_CUDA(cudaMalloc(&p->k3d_idx1, (size_t)tiles * 4));
+    k3d_index<<<1, 1024, 0, s>>>(tiles, tilew, p->k3d_idx1, n1d);
+    INVOP_CUDA(cudaMemcpyAsync(&p->k3d_n1, n1d, 8, cudaMemcpyDeviceToHost, s));
+    INVOP_CUDA(cudaStreamSynchronize(s));
+    if (tiles + p->k3d_n1 < (int64_t)p->P * tiles) {
+      INVOP_CUDA(cudaMalloc(&p->k3d_tiles[0], (size_t)tiles * K3_A_TILE));
+      INVOP_CUDA(cudaMalloc(&p->k3d_tiles[1], (size_t)std::max<int64_t>(p->k3d_n1, 1) * K3_A_TILE));
+      INVOP_CUDA(cudaMemsetAsync(p->k3d_tiles[0], 0, (size_t)tiles * K3_A_TILE, s));
+      k3d_write<<<(unsigned)cdiv(thr, 256), 256, 0, s>>>(a, p->k3d_idx1, p->k3d_tiles[0],
+                                                         p->k3d_tiles[1]);
+      rc = make_map_u8((CUtensorMap*)p->k3d_mapA[0], p->k3d_tiles[0], K3_BK,
+                       (uint64_t)tiles * K3_BM, K3_BK, K3_BK, K3_BM);
+      if (!rc)
+        rc = make_map_u8((CUtensorMap*)p->k3d_mapA[1], p->k3d_tiles[1], K3_BK,
+                         (uint64_t)std::max<int64_t>(p->k3d_n1, 1) * K3_BM, K3_BK, K3_BK, K3_BM);
+      cudaError_t ce = cudaStreamSynchronize(s);
+      if (!rc && ce != cudaSuccess) rc = cuda_fail(ce, "k3d build");
+      if (!rc) p->k3d_ready = 1;
+    }
+  }
+  cudaFree(tilew);
+  cudaFree(n1d);
+  if (p->k3d_ready < 0) {
+    for (int b = 0; b < 2; ++b) {
+      if (p->k3d_tiles[b]) cudaFree(p->k3d_tiles[b]);
+      p->k3d_tiles[b] = nullptr;
+    }
+    if (p->k3d_idx1) cudaFree(p->k3d_idx1);
+    p->k3d_idx1 = nullptr;
+    return rc ? rc : INVOP_E_UNSUPPORTED;
+  }
+  return INVOP_OK;
+}
+
+int64_t k3d_bytes(const invop_plan* p) {
+  if (p->k3d_ready <= 0) return -1;
+  const int64_t tiles = round_up(cdiv(p->rows, K3_BM), 2) * (p->ld / K3_BK);
+  return (tiles + p->k3d_n1) * K3_A_TILE + tiles * 4;
 }
 
 int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, int64_t ldy,
@@ -501,7 +835,12 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
   size_t flag_off = e_off + 256;                          // e[64] ints | flag
   size_t max_off = flag_off + 256;                        // max|x_t| bits [nrhs]
   size_t acc_off = round_up(max_off + (size_t)nrhs * 4, 256);
+  int krc = k3d_build(p, s);
+  if (krc != INVOP_OK && krc != INVOP_E_UNSUPPORTED) return krc;
+  const bool dl = p->k3d_ready > 0 && tiles == 2 && stages == 4;
   size_t acc_bytes = splits > 1 ? (size_t)K3_NR * p->rows * 8 : 0;
+  if (dl)   // + segment carries of the row prefix sums
+    acc_bytes = (size_t)K3_NR * p->rows * 8 + (size_t)K3_NR * cdiv(p->rows, K3D_SEG) * 16;
   int rc = ensure_scratch(&p->k3_ws, &p->k3_ws_bytes, acc_off + acc_bytes);
   if (rc) return rc;
   unsigned int* maxbits = (unsigned int*)((char*)p->k3_ws + max_off);
@@ -522,7 +861,7 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
   int8_t* B = (int8_t*)p->k3_ws;
   int* e = (int*)((char*)p->k3_ws + e_off);
   long long* yacc = (long long*)((char*)p->k3_ws + acc_off);
-  if (!p->k3_maps_ready) {
+  if (!dl && !p->k3_maps_ready) {
     const int64_t rtiles = round_up(cdiv(p->rows, K3_BM), 2);   // row tiles (even)
     const int64_t tile_bytes = rtiles * (p->ld / K3_BK) * K3_A_TILE;
     for (int b = 0; b < p->P; ++b) {
@@ -550,16 +889,18 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
     INVOP_LAUNCHED(2);   // k3_digits + k3_batched
     if (splits > 1) INVOP_CUDA(cudaMemsetAsync(yacc, 0, acc_bytes, s));
     K3Args a;
+    a.idx1 = p->k3d_idx1;
     a.rows = p->rows; a.n = p->n; a.P = p->P; a.hi_signed = p->is_signed;
     a.kblocks_total = kblocks; a.kblocks_per_unit = kpu; a.splits = splits;
     a.kb_stride = (int)(p->ld / K3_BK);
     a.pairs = pairs; a.nrhs = nr; a.e = e; a.scale = p->scale;
     a.y = y + t0 * ldy; a.ldy = ldy; a.yacc = yacc;
     int grid = (int)std::min<int64_t>(sms, pairs * splits);
-    const CUtensorMap* A0 = (const CUtensorMap*)p->k3_mapA[0];
-    const CUtensorMap* A1 = (const CUtensorMap*)p->k3_mapA[1];
-    const int key = p->P * 100 + tiles * 10 + stages;
+    const CUtensorMap* A0 = (const CUtensorMap*)(dl ? p->k3d_mapA[0] : p->k3_mapA[0]);
+    const CUtensorMap* A1 = (const CUtensorMap*)(dl ? p->k3d_mapA[1] : p->k3_mapA[1]);
+    const int key = dl ? 999 : p->P * 100 + tiles * 10 + stages;
     switch (key) {
+      case 999: rc = launch_k3<2, 2, 4, true>(*A0, *A1, mapB, a, grid, s); break;
       case 124: rc = launch_k3<1, 2, 4>(*A0, *A1, mapB, a, grid, s); break;
       case 116: rc = launch_k3<1, 1, 6>(*A0, *A1, mapB, a, grid, s); break;
       case 224: rc = launch_k3<2, 2, 4>(*A0, *A1, mapB, a, grid, s); break;
@@ -569,7 +910,19 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
       default: return fail(INVOP_E_VALUE, "unsupported INVOP_K3_CFG");
     }
     if (rc) return rc;
-    if (splits > 1) {
+    if (dl) {
+      // rows 0/1 from the codes, then the double prefix sum along rows
+      dim3 g01((unsigned)cdiv(cdiv(p->n, 16), 256), (unsigned)nr);
+      k3d_rows01<<<g01, 256, 0, s>>>(p->planes[0], p->planes[p->P > 1 ? 1 : 0], p->P, p->is_signed,
+                                     p->n, p->ld, p->rows, B, ldb, yacc);
+      const int nseg = (int)cdiv(p->rows, K3D_SEG);
+      long long* seg = yacc + (size_t)K3_NR * p->rows;
+      dim3 gs((unsigned)nseg, (unsigned)nr);
+      k3d_seg_sums<<<gs, K3D_SEG, 0, s>>>(yacc, p->rows, seg);
+      k3d_seg_carry<<<1, 64, 0, s>>>(seg, nseg, nr);
+      k3d_seg_apply<<<gs, K3D_SEG, 0, s>>>(yacc, p->rows, seg, e, p->scale, y + t0 * ldy, ldy);
+      INVOP_LAUNCHED(4);
+    } else if (splits > 1) {
       int64_t tot = (int64_t)nr * p->rows;
       k3_finalize<<<(unsigned)std::min<int64_t>(cdiv(tot, 256), sms * 8), 256, 0, s>>>(
           yacc, p->rows, nr, e, p->scale, y + t0 * ldy, ldy);

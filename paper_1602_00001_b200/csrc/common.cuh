@@ -64,6 +64,13 @@ struct invop_plan {
   int dl_ready = 0, dl_grid = 0, dl_nslabs = 0;
   alignas(64) unsigned char k3_mapA[2][128];
   int k3_maps_ready = 0;
+  // K3 on row residuals (batched.cu): digit-0 tiles for every (row tile, K
+  // block), digit-1 tiles only where needed (compact, indexed by k3d_idx1)
+  alignas(64) unsigned char k3d_mapA[2][128];
+  uint8_t* k3d_tiles[2] = {nullptr, nullptr};
+  int* k3d_idx1 = nullptr;
+  int64_t k3d_n1 = 0;
+  int k3d_ready = 0;
 };
 
 struct invop_operator {
@@ -118,6 +125,7 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
 int vw_build(invop_plan* p, cudaStream_t s);
 int tvw_build(invop_plan* p, cudaStream_t s);
 int64_t tvw_stream_bytes(const invop_plan* p);
+int64_t k3d_bytes(const invop_plan* p);
 int apply_tvw_launch(invop_plan* p, const float* x, float* y, cudaStream_t s);
 int apply_vw_launch(invop_plan* p, const float* x, float* y, cudaStream_t s);
 int hl_build(invop_plan* p, cudaStream_t s);

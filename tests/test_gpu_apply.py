@@ -604,3 +604,35 @@ def test_dl_rejects_rough_rows(invop, monkeypatch):
     monkeypatch.setenv("INVOP_HL", "0")
     dplan.apply_device(torch.zeros(9000, device="cuda"), mode=0)
     assert dplan.apply_kernel(1) == "k2_stream"
+
+
+@pytest.mark.parametrize("rows,N,k,splits", [(400, 9000, 16, 0), (1000, 40000, 70, 0),
+                                              (333, 2048, 8, 3), (130, 5000, 64, 2)])
+def test_k3_row_residuals(invop, O, rows, N, k, splits, monkeypatch):
+    """Tensor-core batched apply on second-order row residuals (digit-1 tiles
+    only where needed, rows 0/1 from the codes, double prefix sum): same bits
+    as the byte-plane K3, oracle parity."""
+    import torch
+
+    rng = np.random.default_rng(rows + N + k)
+    mant = np.abs(_smooth_rows(rng, rows, N, 10000, False))
+    mant[17, ::3] = 0                   # residuals up to ~2 * 13000: two digits
+    dplan = invop._plan.DevicePlan.from_mantissas(mant, 4, row0=0, n=N)
+    assert dplan.code_bytes == 2
+    X = rng.standard_normal((k, N))
+    X[:, ::11] *= 1e-3
+    Xt = torch.tensor(X, device="cuda", dtype=torch.float32)
+    if splits:
+        monkeypatch.setenv("INVOP_K3_SPLITS", str(splits))
+    monkeypatch.setenv("INVOP_K3_DL", "1")
+    Y_dl = dplan.apply_device(Xt, mode=0).cpu().numpy()
+    assert dplan.apply_kernel(k) == "k3_batched_dl"
+    dplan2 = invop._plan.DevicePlan.from_mantissas(mant, 4, row0=0, n=N)
+    monkeypatch.setenv("INVOP_K3_DL", "0")
+    Y_pl = dplan2.apply_device(Xt, mode=0).cpu().numpy()
+    assert dplan2.apply_kernel(k) == "k3_batched"
+    assert Y_dl.tobytes() == Y_pl.tobytes()
+    Xr = X.astype(np.float32).astype(np.float64)
+    for t in (0, k // 2, k - 1):
+        yo = O.ordered_apply(mant, 4, Xr[t])
+        assert relerr(Y_dl[t], yo) <= F32_TOL
