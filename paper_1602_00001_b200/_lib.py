@@ -18,7 +18,10 @@ from .errors import (
     SingularMatrixError,
 )
 
-LIB_PATH = Path(__file__).resolve().parent / "libinvop_b200.so"
+# INVOP_LIB_PATH: another build of the same library (A/B timing of kernel
+# revisions on one box); the default is the in-tree build
+LIB_PATH = Path(os.environ.get("INVOP_LIB_PATH") or
+                Path(__file__).resolve().parent / "libinvop_b200.so").resolve()
 
 OK = 0
 E_VALUE = 1

@@ -61,7 +61,7 @@ struct invop_plan {
   uint8_t* dl_data = nullptr;
   int64_t* dl_uoff = nullptr;       // [units+1] byte offsets, units in (CTA, slab, row) order
   int64_t dl_bytes = 0, dl_maxunit = 0;
-  int dl_ready = 0, dl_grid = 0, dl_nslabs = 0;
+  int dl_ready = 0, dl_grid = 0, dl_nslabs = 0, dl_groups = 1;
   alignas(64) unsigned char k3_mapA[2][128];
   int k3_maps_ready = 0;
   // K3 on row residuals (batched.cu): digit-0 tiles for every (row tile, K

@@ -45,6 +45,31 @@ __host__ __device__ inline int dl_cta_of(int64_t r, int64_t rows, int grid) {
   return b;
 }
 
+// A CTA's rows [lo, lo + n) are split into G segments of consecutive rows
+// (the first n % G one row longer), one per consumer group. Residual orders
+// restart at every segment start; the units of a slab are interleaved across
+// segments: row i of segment g is unit i*G + g of the slab.
+struct DlPos {
+  int64_t lo, n;       // CTA row range
+  int g;               // segment
+  int64_t i;           // row index within the segment
+};
+__host__ __device__ inline DlPos dl_pos(int64_t r, int64_t rows, int grid, int G) {
+  DlPos p;
+  const int b = dl_cta_of(r, rows, grid);
+  p.lo = (int64_t)b * rows / grid;
+  p.n = (int64_t)(b + 1) * rows / grid - p.lo;
+  const int64_t l = r - p.lo, base = p.n / G, rem = p.n % G;
+  if (l < rem * (base + 1)) {
+    p.g = (int)(l / (base + 1));
+    p.i = l - p.g * (base + 1);
+  } else {
+    p.g = (int)(rem + (l - rem * (base + 1)) / base);
+    p.i = l - rem * (base + 1) - (p.g - rem) * base;
+  }
+  return p;
+}
+
 // code j of a lane's 16 (bytes from up to 3 planes) -> int32
 __device__ __forceinline__ void dl_load16(const uint8_t* const* planes, int P, int sgn,
                                           int64_t off, int32_t* v) {
@@ -85,14 +110,13 @@ struct DlBuild {
   const uint8_t* planes[3];
   int P, sgn;
   int64_t rows, n, ld;
-  int nch, nslabs, grid;
+  int nch, nslabs, grid, groups;
 };
 
 __device__ __forceinline__ void dl_residual16(const DlBuild& a, int64_t r, int c, int lane,
                                               int32_t* e) {
-  const int b = dl_cta_of(r, a.rows, a.grid);
-  const int64_t lo = (int64_t)b * a.rows / a.grid;
-  const int order = (int)(r - lo < 2 ? r - lo : 2);
+  const DlPos ps = dl_pos(r, a.rows, a.grid, a.groups);
+  const int order = (int)(ps.i < 2 ? ps.i : 2);
   const int64_t off = r * a.ld + (int64_t)c * 512 + lane * 16;
   dl_load16(a.planes, a.P, a.sgn, off, e);
   if (order >= 1) {
@@ -126,11 +150,12 @@ __global__ void k_dl_width(DlBuild a, uint8_t* __restrict__ width) {
   if (lane == 0) width[gw] = (uint8_t)w;
 }
 
-// unit index of (row r, slab s) in processing order (CTA, slab, row)
-__host__ __device__ inline int64_t dl_unit(int64_t r, int s, int64_t rows, int nslabs, int grid) {
-  const int b = dl_cta_of(r, rows, grid);
-  const int64_t lo = (int64_t)b * rows / grid, hi = (int64_t)(b + 1) * rows / grid;
-  return lo * nslabs + (int64_t)s * (hi - lo) + (r - lo);
+// unit index of (row r, slab s) in processing order (CTA, slab, segment row,
+// segment)
+__host__ __device__ inline int64_t dl_unit(int64_t r, int s, int64_t rows, int nslabs, int grid,
+                                           int G) {
+  const DlPos p = dl_pos(r, rows, grid, G);
+  return p.lo * nslabs + (int64_t)s * p.n + p.i * G + p.g;
 }
 
 // one thread per (row, slab): header (chunk starts) and byte size of the unit
@@ -147,7 +172,7 @@ __global__ void k_dl_units(DlBuild a, const uint8_t* __restrict__ width, uint4* 
     h[c >> 2] |= start << (8 * (c & 3));
     if (c < cn) start += width[r * a.nch + c0 + c];
   }
-  const int64_t u = dl_unit(r, s, a.rows, a.nslabs, a.grid);
+  const int64_t u = dl_unit(r, s, a.rows, a.nslabs, a.grid, a.groups);
   for (int k = 0; k < 3; ++k) hdrs[3 * u + k] = make_uint4(h[4 * k], h[4 * k + 1], h[4 * k + 2], h[4 * k + 3]);
   const int64_t bytes = DL_HDR + 512 * (int64_t)start;
   size[u] = bytes;
@@ -195,7 +220,7 @@ __global__ void k_dl_write(DlBuild a, const uint4* __restrict__ hdrs,
   const int64_t r = gw / a.nch;
   const int c = (int)(gw - r * a.nch);
   const int s = c / 32, cl = c % 32;
-  const int64_t u = dl_unit(r, s, a.rows, a.nslabs, a.grid);
+  const int64_t u = dl_unit(r, s, a.rows, a.nslabs, a.grid, a.groups);
   uint8_t* unit = data + off[u];
   const uint8_t* h = reinterpret_cast<const uint8_t*>(hdrs + 3 * u);
   if (cl == 0 && lane < 3) reinterpret_cast<uint4*>(unit)[lane] = hdrs[3 * u + lane];
@@ -219,7 +244,11 @@ struct DlArgs {
   int ring_bytes;               // variable-size unit ring (FIFO) in shared memory
 };
 
-constexpr int DL_NS = 8;         // units in flight at most (barrier pairs)
+#ifndef DL_NS_OVERRIDE
+constexpr int DL_NS = 16;        // units in flight at most (barrier pairs)
+#else
+constexpr int DL_NS = DL_NS_OVERRIDE;
+#endif
 
 __device__ __forceinline__ uint4 dl_lds128(uint32_t addr) {
   uint4 v;
@@ -244,16 +273,142 @@ __device__ __forceinline__ void dl_plane(const uint4& cw, const uint32_t (*xd)[4
     for (int d = 0; d < 3; ++d) S[B + d] = dp4a_ss(u4get(cw, k), xd[d][k], S[B + d]);
 }
 
+// planes 1.. of one chunk (width w >= 2), warp-uniform branches
+__device__ __forceinline__ void dl_upper(uint32_t pa, uint32_t w, const uint32_t (*xd)[4], int32_t* S) {
+  if (w >= 2) {
+    dl_plane<1>(dl_lds128(pa + 512), xd, S);
+    if (w >= 3) {
+      dl_plane<2>(dl_lds128(pa + 1024), xd, S);
+      if (w >= 4) dl_plane<3>(dl_lds128(pa + 1536), xd, S);
+    }
+  }
+}
+
+__device__ __forceinline__ long long dl_warp_sum(const int32_t* S) {
+  const long long acc = (long long)S[0] + ((long long)S[1] << 8) + ((long long)S[2] << 16) +
+                        ((long long)S[3] << 24) + ((long long)S[4] << 32) + ((long long)S[5] << 40);
+  // exact warp sum: |e| < 2^25, |X| <= 2^22, 16 SW codes per lane -> |acc| < 2^54
+  const uint32_t lo = __reduce_add_sync(0xffffffffu, (uint32_t)acc & 0x7FFFFFFu);
+  const int32_t hi = __reduce_add_sync(0xffffffffu, (int32_t)(acc >> 27));
+  return ((long long)hi << 27) + (long long)lo;
+}
+
+__device__ __forceinline__ void dl_slot(double* sp, bool first, long long Y, double inv2e, int lane) {
+  const double v = (double)Y * inv2e;
+  if (lane == 0) *sp = first ? v : (*sp + v);
+}
+
 template <bool F64IO>
 __device__ __forceinline__ float dl_x(const DlArgs& a, int64_t j) {
   return F64IO ? (float)static_cast<const double*>(a.x)[j] : static_cast<const float*>(a.x)[j];
 }
 
-template <int CONS, bool F64IO>
+// the rows of one consumer iteration: headers of all (row, chunk), then the
+// plane-0 words, then the DP4As of all rows (independent chains); upper planes
+// last (warp-uniform branches on the chunk widths)
+template <int SW, int ROWS, int WPG>
+__device__ __forceinline__ void dl_rows_phased(const uint32_t* sb, int q, uint32_t stepv,
+                                               const uint32_t (*xd)[3][4], int lane,
+                                               int32_t (*Sa)[6]) {
+  uint32_t h[ROWS][SW], w[ROWS][SW];
+#pragma unroll
+  for (int r = 0; r < ROWS; ++r)
+#pragma unroll
+    for (int t = 0; t < SW; ++t) {
+      const int c = q + t * WPG;
+      h[r][t] = dl_lds_u8(sb[r] + c);
+      w[r][t] = dl_lds_u8(sb[r] + c + 1) - h[r][t];
+    }
+  uint4 cw[ROWS][SW];
+#pragma unroll
+  for (int r = 0; r < ROWS; ++r)
+#pragma unroll
+    for (int t = 0; t < SW; ++t) {
+      h[r][t] = sb[r] + DL_HDR + h[r][t] * 512 + lane * 16;      // chunk address
+      cw[r][t] = ((stepv >> t) & 1u) ? dl_lds128(h[r][t]) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+  for (int r = 0; r < ROWS; ++r)
+#pragma unroll
+    for (int k = 0; k < 6; ++k) Sa[r][k] = 0;
+#pragma unroll
+  for (int t = 0; t < SW; ++t)
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) dl_plane<0>(cw[r][t], xd[t], Sa[r]);
+#pragma unroll
+  for (int t = 0; t < SW; ++t) {
+    if (!((stepv >> t) & 1u)) continue;                      // warp-uniform
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) dl_upper(h[r][t], w[r][t], xd[t], Sa[r]);
+  }
+}
+
+// chunk by chunk (fewer live registers for many chunks per warp)
+template <int SW, int ROWS, int WPG>
+__device__ __forceinline__ void dl_rows_lazy(const uint32_t* sb, int q, uint32_t stepv,
+                                             const uint32_t (*xd)[3][4], int lane,
+                                             int32_t (*Sa)[6]) {
+#pragma unroll
+  for (int r = 0; r < ROWS; ++r)
+#pragma unroll
+    for (int k = 0; k < 6; ++k) Sa[r][k] = 0;
+#pragma unroll
+  for (int t = 0; t < SW; ++t) {
+    if (!((stepv >> t) & 1u)) continue;                      // warp-uniform
+    const int c = q + t * WPG;
+    uint32_t pa[ROWS], wd[ROWS];
+    uint4 cw[ROWS];
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) {
+      const uint32_t h = dl_lds_u8(sb[r] + c);
+      wd[r] = dl_lds_u8(sb[r] + c + 1) - h;
+      pa[r] = sb[r] + DL_HDR + h * 512 + lane * 16;
+      cw[r] = dl_lds128(pa[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) dl_plane<0>(cw[r], xd[t], Sa[r]);
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) dl_upper(pa[r], wd[r], xd[t], Sa[r]);
+  }
+}
+
+// 16 consecutive x values from column c0 (zero past n): 128-bit loads when the
+// run is inside x and aligned
+template <bool F64IO>
+__device__ __forceinline__ void dl_x16(const DlArgs& a, int64_t c0, bool inside, float* v) {
+  if (inside && c0 + 16 <= a.n &&
+      ((reinterpret_cast<uintptr_t>(a.x) + (uintptr_t)c0 * (F64IO ? 8 : 4)) & 15) == 0) {
+    if (F64IO) {
+      const double2* p = reinterpret_cast<const double2*>(static_cast<const double*>(a.x) + c0);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const double2 d = __ldg(p + k);
+        v[2 * k] = (float)d.x;
+        v[2 * k + 1] = (float)d.y;
+      }
+    } else {
+      const float4* p = reinterpret_cast<const float4*>(static_cast<const float*>(a.x) + c0);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float4 f = __ldg(p + k);
+        v[4 * k] = f.x; v[4 * k + 1] = f.y; v[4 * k + 2] = f.z; v[4 * k + 3] = f.w;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = (inside && c0 + k < a.n) ? dl_x<F64IO>(a, c0 + k) : 0.0f;
+  }
+}
+
+// CONS consumer warps in G groups. Group g walks segment g of the CTA's rows
+// (ROWS rows per iteration); warp q of a group owns chunks q + t*(CONS/G) of
+// every slab, its x piece held in registers as balanced digits.
+template <int CONS, int G, int ROWS, bool F64IO>
 __global__ void __launch_bounds__((CONS + 1) * 32, 1) k2_dl(DlArgs a) {
-  constexpr int SW = DL_SLAB / (CONS * 512);
+  constexpr int WPG = CONS / G;
+  constexpr int SW = DL_SLAB / (WPG * 512);
   extern __shared__ __align__(128) unsigned char smem[];
-  // [ring][full[NS], empty[NS]][unit pos[NS]][slot: nrows x CONS doubles][unit offsets]
+  // [ring][full[NS], empty[NS]][unit pos[NS], alloc[NS]][slot: nrows x WPG doubles][unit offsets]
   constexpr int S = DL_NS;
   const uint32_t R = (uint32_t)a.ring_bytes;
   unsigned char* ring = smem;
@@ -268,12 +423,12 @@ __global__ void __launch_bounds__((CONS + 1) * 32, 1) k2_dl(DlArgs a) {
   const int64_t nrows = row_hi - row_lo;
   const int64_t units = nrows * a.nslabs;
   const int64_t ubase = row_lo * a.nslabs;
-  int64_t* s_off = reinterpret_cast<int64_t*>(slot + nrows * CONS);
+  int64_t* s_off = reinterpret_cast<int64_t*>(slot + nrows * WPG);
   for (int64_t i = threadIdx.x; i <= units; i += blockDim.x) s_off[i] = a.uoff[ubase + i];
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
       mbar_init(bar_s + 8 * i, 1);
-      mbar_init(bar_s + 8 * (S + i), CONS);
+      mbar_init(bar_s + 8 * (S + i), WPG);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -282,8 +437,8 @@ __global__ void __launch_bounds__((CONS + 1) * 32, 1) k2_dl(DlArgs a) {
   if (warp == CONS) {
     if (lane == 0) {
       // FIFO of variable-size units: a unit goes at the ring head (or at 0 when
-      // it would run past the end); the oldest units are retired (all consumer
-      // warps arrived on their empty barrier) until it fits and a slot is free
+      // it would run past the end); the oldest units are retired (all warps of
+      // their group arrived on the empty barrier) until it fits and a slot is free
       uint64_t policy;
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
       uint32_t* s_alloc = s_pos + S;
@@ -313,32 +468,34 @@ __global__ void __launch_bounds__((CONS + 1) * 32, 1) k2_dl(DlArgs a) {
       }
     }
   } else {
-    const int wc = warp;
+    const int g = warp / WPG, q = warp - g * WPG;
+    const int64_t sbase = nrows / G, srem = nrows % G;
+    const int segn = (int)(sbase + (g < srem ? 1 : 0));
+    const int seglo = (int)(g * sbase + (g < srem ? g : srem));
     uint32_t xd[SW][3][4];          // balanced base-256 digits of the fixed-point x piece
-    bool stepv[SW];
-    bool masked = false;
-    double inv2e = 1.0;
-    long long Y1 = 0, Y2 = 0;
-    int st = 0, slab = 0;
-    uint32_t ph = 0;
-    int lr = 0;
-    for (int u = 0; u < (int)units;) {
-      if (lr == 0) {
-        // new slab: x piece of this warp -> 23-bit fixed point (as k2_stream);
-        // x is read once (it may live in mapped host memory)
-        float xv[SW][16];
+    uint32_t stepv = 0;             // bit t: chunk t of this warp lies inside the operator
+    for (int slab = 0; slab < a.nslabs; ++slab) {
+      stepv = 0;
+      // x piece of this warp -> 23-bit fixed point (warp-wide exponent):
+      // one pass for max|x| and finiteness, one for the digits (SW > 2; the
+      // values stay in registers for SW <= 2)
+      bool masked;
+      double inv2e;
+      {
+        constexpr int KEEP = SW <= 2 ? SW : 1;
+        float xk[KEEP][16];
         bool finite = true;
         float mx = 0.0f;
 #pragma unroll
         for (int t = 0; t < SW; ++t) {
-          const int64_t col = (int64_t)slab * DL_SLAB + (int64_t)(wc + t * CONS) * 512;
-          stepv[t] = col < a.n;
-          const int64_t c0 = col + lane * 16;
+          const int64_t col = (int64_t)slab * DL_SLAB + (int64_t)(q + t * WPG) * 512;
+          if (col < a.n) stepv |= 1u << t;
+          float* v = xk[SW <= 2 ? t : 0];
+          dl_x16<F64IO>(a, col + lane * 16, col < a.n, v);
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            xv[t][q] = (stepv[t] && c0 + q < a.n) ? dl_x<F64IO>(a, c0 + q) : 0.0f;
-            finite = finite && isfinite(xv[t][q]);
-            mx = fmaxf(mx, fabsf(xv[t][q]));
+          for (int k = 0; k < 16; ++k) {
+            finite = finite && isfinite(v[k]);
+            mx = fmaxf(mx, fabsf(v[k]));
           }
         }
         masked = __any_sync(0xffffffffu, !finite);
@@ -352,143 +509,89 @@ __global__ void __launch_bounds__((CONS + 1) * 32, 1) k2_dl(DlArgs a) {
         inv2e = ldexp(1.0, -e);
 #pragma unroll
         for (int t = 0; t < SW; ++t) {
+          const int64_t c0 = (int64_t)slab * DL_SLAB + (int64_t)(q + t * WPG) * 512 + lane * 16;
+          float* v = xk[SW <= 2 ? t : 0];
+          if (SW > 2) dl_x16<F64IO>(a, c0, (stepv >> t) & 1u, v);
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             int32_t X[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) X[i] = masked ? 0 : __float2int_rn(ldexpf(xv[t][4 * k + i], e));
+            for (int i = 0; i < 4; ++i) X[i] = masked ? 0 : __float2int_rn(ldexpf(v[4 * k + i], e));
             uint32_t dw[3];
             x_digits4(X, dw);
             xd[t][0][k] = dw[0]; xd[t][1][k] = dw[1]; xd[t][2][k] = dw[2];
           }
         }
-        Y1 = 0;
-        Y2 = 0;
       }
-      // two rows per iteration when both are in this slab: their loads, DP4As
-      // and warp sums interleave (the per-row chain is latency bound)
-      const bool two = !masked && lr + 1 < (int)nrows;
-      const int stB = st + 1 == S ? 0 : st + 1;
-      const uint32_t phB = st + 1 == S ? ph ^ 1u : ph;
-      mbar_wait(bar_s + 8 * st, ph);
-      if (two) mbar_wait(bar_s + 8 * stB, phB);
-      if (!masked) {
-        const uint32_t sbA = ring_s + s_pos[st];
-        const uint32_t sbB = ring_s + s_pos[two ? stB : st];
-        uint32_t csA[SW], wA[SW], csB[SW], wB[SW];
+      long long Y1 = 0, Y2 = 0;
+      const uint32_t ub = slab * (uint32_t)nrows + g;
+      for (int i = 0; i < segn;) {
+        // ROWS rows per iteration (their loads, DP4As and warp sums interleave)
+        const int nr = masked ? 1 : min(ROWS, segn - i);
+        uint32_t st[ROWS];
 #pragma unroll
-        for (int t = 0; t < SW; ++t) {
-          const int c = wc + t * CONS;
-          csA[t] = dl_lds_u8(sbA + c);
-          wA[t] = dl_lds_u8(sbA + c + 1) - csA[t];
-          csB[t] = dl_lds_u8(sbB + c);
-          wB[t] = dl_lds_u8(sbB + c + 1) - csB[t];
+        for (int r = 0; r < ROWS; ++r) {
+          const uint32_t u = ub + (i + r) * G;
+          st[r] = u % S;
+          if (r < nr) mbar_wait(bar_s + 8 * st[r], (u / S) & 1u);
         }
-        uint4 pA[SW], pB[SW];
+        const uint32_t stA = st[0];
+        const int lr = seglo + i;
+        if (!masked) {
+          uint32_t sb[ROWS];
 #pragma unroll
-        for (int t = 0; t < SW; ++t) {
-          pA[t] = stepv[t] ? dl_lds128(sbA + DL_HDR + csA[t] * 512 + lane * 16) : make_uint4(0, 0, 0, 0);
-          pB[t] = stepv[t] ? dl_lds128(sbB + DL_HDR + csB[t] * 512 + lane * 16) : make_uint4(0, 0, 0, 0);
-        }
-        int32_t SA[6] = {0, 0, 0, 0, 0, 0}, SB[6] = {0, 0, 0, 0, 0, 0};
-#pragma unroll
-        for (int t = 0; t < SW; ++t) {
-          dl_plane<0>(pA[t], xd[t], SA);
-          dl_plane<0>(pB[t], xd[t], SB);
-        }
-#pragma unroll
-        for (int t = 0; t < SW; ++t) {
-          if (!stepv[t]) continue;                      // warp-uniform
-          const uint32_t pa = sbA + DL_HDR + csA[t] * 512 + lane * 16;
-          if (wA[t] >= 2) {
-            dl_plane<1>(dl_lds128(pa + 512), xd[t], SA);
-            if (wA[t] >= 3) {
-              dl_plane<2>(dl_lds128(pa + 1024), xd[t], SA);
-              if (wA[t] >= 4) dl_plane<3>(dl_lds128(pa + 1536), xd[t], SA);
-            }
-          }
-          const uint32_t pbb = sbB + DL_HDR + csB[t] * 512 + lane * 16;
-          if (wB[t] >= 2) {
-            dl_plane<1>(dl_lds128(pbb + 512), xd[t], SB);
-            if (wB[t] >= 3) {
-              dl_plane<2>(dl_lds128(pbb + 1024), xd[t], SB);
-              if (wB[t] >= 4) dl_plane<3>(dl_lds128(pbb + 1536), xd[t], SB);
-            }
-          }
-        }
-        __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(bar_s + 8 * (S + st));
-          if (two) mbar_arrive(bar_s + 8 * (S + stB));
-        }
-        const long long accA = (long long)SA[0] + ((long long)SA[1] << 8) + ((long long)SA[2] << 16) +
-                               ((long long)SA[3] << 24) + ((long long)SA[4] << 32) + ((long long)SA[5] << 40);
-        const long long accB = (long long)SB[0] + ((long long)SB[1] << 8) + ((long long)SB[2] << 16) +
-                               ((long long)SB[3] << 24) + ((long long)SB[4] << 32) + ((long long)SB[5] << 40);
-        // exact warp sums: |e| < 2^25, |X| <= 2^22, 32 codes per lane -> |acc| < 2^52
-        const uint32_t loA = __reduce_add_sync(0xffffffffu, (uint32_t)accA & 0x7FFFFFFu);
-        const int32_t hiA = __reduce_add_sync(0xffffffffu, (int32_t)(accA >> 27));
-        const uint32_t loB = __reduce_add_sync(0xffffffffu, (uint32_t)accB & 0x7FFFFFFu);
-        const int32_t hiB = __reduce_add_sync(0xffffffffu, (int32_t)(accB >> 27));
-        const long long DA = ((long long)hiA << 27) + (long long)loA;
-        const long long DB = ((long long)hiB << 27) + (long long)loB;
-        const long long YA = DA + (lr >= 2 ? 2 * Y1 - Y2 : (lr == 1 ? Y1 : 0));
-        Y2 = Y1;
-        Y1 = YA;
-        if (lane == 0) {
-          double* sp = &slot[lr * CONS + wc];
-          *sp = (slab == 0) ? (double)YA * inv2e : (*sp + (double)YA * inv2e);
-        }
-        if (two) {
-          const long long YB = DB + (lr + 1 >= 2 ? 2 * Y1 - Y2 : Y1);
-          Y2 = Y1;
-          Y1 = YB;
+          for (int r = 0; r < ROWS; ++r) sb[r] = ring_s + s_pos[r < nr ? st[r] : st[0]];
+          int32_t Sa[ROWS][6];
+          if (G == 1) dl_rows_phased<SW, ROWS, WPG>(sb, q, stepv, xd, lane, Sa);
+          else dl_rows_lazy<SW, ROWS, WPG>(sb, q, stepv, xd, lane, Sa);
+          __syncwarp();
           if (lane == 0) {
-            double* sp = &slot[(lr + 1) * CONS + wc];
-            *sp = (slab == 0) ? (double)YB * inv2e : (*sp + (double)YB * inv2e);
+#pragma unroll
+            for (int r = 0; r < ROWS; ++r)
+              if (r < nr) mbar_arrive(bar_s + 8 * (S + st[r]));
+          }
+#pragma unroll
+          for (int r = 0; r < ROWS; ++r) {
+            if (r < nr) {
+              const int ir = i + r;
+              const long long Y = dl_warp_sum(Sa[r]) + (ir >= 2 ? 2 * Y1 - Y2 : (ir == 1 ? Y1 : 0));
+              Y2 = Y1;
+              Y1 = Y;
+              dl_slot(&slot[(lr + r) * WPG + q], slab == 0, Y, inv2e, lane);
+            }
+          }
+        } else {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar_s + 8 * (S + stA));
+          // inf/nan in this warp's x: plain codes from the byte planes, the
+          // reference's zero skip, fp32 accumulation (as k2_stream)
+          float acc = 0.0f;
+          const int64_t r = row_lo + lr;
+          for (int t = 0; t < SW; ++t) {
+            if (!((stepv >> t) & 1u)) continue;
+            const int64_t c0 = (int64_t)slab * DL_SLAB + (int64_t)(q + t * WPG) * 512 + lane * 16;
+            int32_t v[16];
+            dl_load16(a.planes, a.P, a.sgn, r * a.ld + c0, v);
+            for (int k = 0; k < 16; ++k) {
+              if (v[k] == 0 || c0 + k >= a.n) continue;
+              acc = fmaf((float)v[k], dl_x<F64IO>(a, c0 + k), acc);
+            }
+          }
+          for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+          if (lane == 0) {
+            double* sp = &slot[lr * WPG + q];
+            *sp = (slab == 0) ? (double)acc : (*sp + (double)acc);
           }
         }
-      } else {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar_s + 8 * (S + st));
-        // inf/nan in this warp's x: plain codes from the byte planes, the
-        // reference's zero skip, fp32 accumulation (as k2_stream)
-        float acc = 0.0f;
-        const int64_t r = row_lo + lr;
-        for (int t = 0; t < SW; ++t) {
-          if (!stepv[t]) continue;
-          const int64_t c0 = (int64_t)slab * DL_SLAB + (int64_t)(wc + t * CONS) * 512 + lane * 16;
-          int32_t v[16];
-          dl_load16(a.planes, a.P, a.sgn, r * a.ld + c0, v);
-          for (int q = 0; q < 16; ++q) {
-            if (v[q] == 0 || c0 + q >= a.n) continue;
-            acc = fmaf((float)v[q], dl_x<F64IO>(a, c0 + q), acc);
-          }
-        }
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) {
-          double* sp = &slot[lr * CONS + wc];
-          *sp = (slab == 0) ? (double)acc : (*sp + (double)acc);
-        }
+        i += nr;
       }
-      if (two) {
-        st = stB == S - 1 ? 0 : stB + 1;
-        ph = stB == S - 1 ? phB ^ 1u : phB;
-        u += 2;
-        lr += 2;
-      } else {
-        if (++st == S) { st = 0; ph ^= 1; }
-        u += 1;
-        lr += 1;
-      }
-      if (lr == (int)nrows) { lr = 0; ++slab; }
     }
   }
   __syncthreads();
   for (int64_t r = threadIdx.x; r < nrows; r += blockDim.x) {
     double s = 0.0;
 #pragma unroll
-    for (int c = 0; c < CONS; ++c) s += slot[r * CONS + c];
+    for (int c = 0; c < WPG; ++c) s += slot[r * WPG + c];
     const float yv = (float)(s * a.scale);
     if (F64IO) static_cast<double*>(a.y)[row_lo + r] = (double)yv;
     else static_cast<float*>(a.y)[row_lo + r] = yv;
@@ -500,10 +603,23 @@ static int dl_consumers() {
   return v && atoi(v) == 8 ? 8 : 16;
 }
 
+// consumer groups: one for short CTA row ranges (config 4: 111 rows, where the
+// per-CTA start-up dominates), two for long ones (config 5: 443 rows, 4 slabs)
+static int dl_groups_for(int64_t rows_per_cta) {
+  if (const char* v = getenv("INVOP_DL_GROUPS")) return atoi(v) == 2 ? 2 : 1;
+  return rows_per_cta >= 256 ? 2 : 1;
+}
+
+// shared memory besides the ring: slot + unit offsets of the largest CTA
 static size_t dl_side_bytes(const invop_plan* p, int cons) {
   const int64_t rpc = cdiv(p->rows, p->dl_grid);
-  return (size_t)rpc * cons * 8 + (size_t)(rpc * p->dl_nslabs + 1) * 8 + 64;
+  return (size_t)rpc * (cons / p->dl_groups) * 8 + (size_t)(rpc * p->dl_nslabs + 1) * 8 + 64 +
+         DL_NS * 24;
 }
+
+// units that must fit in the ring at once (see the producer): G == 1: the two
+// units of a consumer iteration plus a wrap gap; G groups: 2G
+static int dl_ring_units(int G) { return G == 1 ? 3 : 2 * G; }
 
 int dl_build(invop_plan* p, cudaStream_t s) {
   if (p->dl_ready) return p->dl_ready > 0 ? INVOP_OK : INVOP_E_UNSUPPORTED;
@@ -519,7 +635,10 @@ int dl_build(invop_plan* p, cudaStream_t s) {
   a.nch = (int)(p->ld / 512);
   a.nslabs = (int)cdiv(a.nch, 32);
   a.grid = (int)std::min<int64_t>(num_sms(), p->rows);
+  a.groups = dl_groups_for(cdiv(p->rows, a.grid));
+  if (dl_consumers() % a.groups) a.groups = 1;
   p->dl_grid = a.grid;
+  p->dl_groups = a.groups;
   p->dl_nslabs = a.nslabs;
   const int64_t units = p->rows * a.nslabs;
   uint8_t* width = nullptr;
@@ -544,7 +663,7 @@ int dl_build(invop_plan* p, cudaStream_t s) {
   p->dl_bytes = total;
   p->dl_maxunit = (int64_t)mx;
   int rc = INVOP_OK;
-  const size_t need = 3 * (size_t)mx + dl_side_bytes(p, dl_consumers()) + DL_NS * 24 + 128;
+  const size_t need = (size_t)dl_ring_units(a.groups) * mx + dl_side_bytes(p, dl_consumers()) + 128;
   if (total >= (int64_t)p->P * p->rows * p->ld || need > 225 * 1024) {
     rc = INVOP_E_UNSUPPORTED;          // no gain over the byte planes / does not fit
   } else {
@@ -566,6 +685,17 @@ int dl_build(invop_plan* p, cudaStream_t s) {
   return INVOP_OK;
 }
 
+template <int CONS, int G, int ROWS, bool F64IO>
+static void dl_launch(const DlArgs& a, int grid, size_t smem, cudaStream_t s) {
+  static size_t smem_set = 0;            // opt-in once per instantiation and size
+  if (smem_set < smem) {
+    cudaFuncSetAttribute(k2_dl<CONS, G, ROWS, F64IO>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    smem_set = smem;
+  }
+  k2_dl<CONS, G, ROWS, F64IO><<<grid, (CONS + 1) * 32, smem, s>>>(a);
+}
+
 int apply_dl_launch(invop_plan* p, const void* x, void* y, bool f64io, cudaStream_t s) {
   DlArgs a;
   a.data = p->dl_data;
@@ -577,19 +707,37 @@ int apply_dl_launch(invop_plan* p, const void* x, void* y, bool f64io, cudaStrea
   a.nslabs = p->dl_nslabs;
   a.scale = p->scale;
   a.x = x; a.y = y;
-  const int cons = dl_consumers();
-  const size_t side = dl_side_bytes(p, cons) + DL_NS * 24;
+  int cons = dl_consumers();
+  if (cons % p->dl_groups) cons = 16;
+  const size_t side = dl_side_bytes(p, cons);
   int64_t ring = (225 * 1024 - (int64_t)side) / 128 * 128;
   if (const char* v = getenv("INVOP_DL_RING_KB")) ring = std::min<int64_t>(ring, atoi(v) * 1024);
-  // consumers take two consecutive units at once: with a ring of >= 3 max
-  // units, any two consecutive units fit side by side after a wrap
-  if (ring < 3 * p->dl_maxunit) return fail(INVOP_E_UNSUPPORTED, "k2_dl: not enough shared memory");
+  if (ring < dl_ring_units(p->dl_groups) * p->dl_maxunit)
+    return fail(INVOP_E_UNSUPPORTED, "k2_dl: not enough shared memory");
   a.ring_bytes = (int)ring;
   const size_t smem = (size_t)ring + side;
-  auto kern = cons == 8 ? (f64io ? k2_dl<8, true> : k2_dl<8, false>)
-                        : (f64io ? k2_dl<16, true> : k2_dl<16, false>);
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<p->dl_grid, (cons + 1) * 32, smem, s>>>(a);
+  int rows = 2;
+  if (const char* v = getenv("INVOP_DL_ROWS")) rows = atoi(v) == 1 ? 1 : 2;
+  const int key = cons * 1000 + p->dl_groups * 100 + rows * 10 + (f64io ? 1 : 0);
+  switch (key) {
+    case 16120: dl_launch<16, 1, 2, false>(a, p->dl_grid, smem, s); break;
+    case 16121: dl_launch<16, 1, 2, true>(a, p->dl_grid, smem, s); break;
+    case 16110: dl_launch<16, 1, 1, false>(a, p->dl_grid, smem, s); break;
+    case 16111: dl_launch<16, 1, 1, true>(a, p->dl_grid, smem, s); break;
+    case 16210: dl_launch<16, 2, 1, false>(a, p->dl_grid, smem, s); break;
+    case 16211: dl_launch<16, 2, 1, true>(a, p->dl_grid, smem, s); break;
+    case 16220: dl_launch<16, 2, 2, false>(a, p->dl_grid, smem, s); break;
+    case 16221: dl_launch<16, 2, 2, true>(a, p->dl_grid, smem, s); break;
+    case 8120: dl_launch<8, 1, 2, false>(a, p->dl_grid, smem, s); break;
+    case 8121: dl_launch<8, 1, 2, true>(a, p->dl_grid, smem, s); break;
+    case 8110: dl_launch<8, 1, 1, false>(a, p->dl_grid, smem, s); break;
+    case 8111: dl_launch<8, 1, 1, true>(a, p->dl_grid, smem, s); break;
+    case 8210: dl_launch<8, 2, 1, false>(a, p->dl_grid, smem, s); break;
+    case 8211: dl_launch<8, 2, 1, true>(a, p->dl_grid, smem, s); break;
+    case 8220: dl_launch<8, 2, 2, false>(a, p->dl_grid, smem, s); break;
+    case 8221: dl_launch<8, 2, 2, true>(a, p->dl_grid, smem, s); break;
+    default: return fail(INVOP_E_VALUE, "k2_dl: unsupported consumer layout");
+  }
   INVOP_LAUNCHED(1);
   INVOP_CHECK_LAUNCH("k2_dl");
   return INVOP_OK;
