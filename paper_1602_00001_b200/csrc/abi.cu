@@ -241,6 +241,22 @@ __global__ void k_f32_to_f64(const float* __restrict__ a, double* __restrict__ b
     b[i] = (double)a[i];
 }
 
+// x from page-locked host memory (mapped) into device memory; the dependent
+// apply grid may launch immediately
+__global__ void k_pull_x(const double* __restrict__ xh, double* __restrict__ xd, int64_t n) {
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int64_t n2 = n / 2;
+  const double2* h2 = reinterpret_cast<const double2*>(xh);
+  double2* d2 = reinterpret_cast<double2*>(xd);
+  const bool vec = ((reinterpret_cast<uintptr_t>(xh) | reinterpret_cast<uintptr_t>(xd)) & 15) == 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (vec ? n2 : 0);
+       i += (int64_t)gridDim.x * blockDim.x)
+    d2[i] = h2[i];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x + (vec ? 2 * n2 : 0); i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    xd[i] = xh[i];
+}
+
 static bool is_pinned(const void* ptr) {
   cudaPointerAttributes at;
   if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
@@ -260,14 +276,25 @@ extern "C" int invop_apply_host(invop_plan* p, const double* x, double* y, int64
   if (mode == INVOP_MODE_FAST && nrhs == 1 && fast_route(p, 1) == ROUTE_DL && is_pinned(y) &&
       dl_build(p, s) == INVOP_OK) {
     // page-locked y: the DL kernel writes its fp64 rows straight into host
-    // memory (each row once; zero copy), after one H2D copy of x (x is read by
-    // every CTA, so it is staged in device memory)
-    void* dyp = nullptr;
+    // memory (each row once; zero copy). x is read by every CTA, so it is
+    // staged in device memory: page-locked x is pulled over PCIe by a small
+    // grid that lets the apply grid start at once (programmatic dependent
+    // launch: the producer streams the operator while x arrives; the
+    // consumers wait for it); otherwise one H2D copy.
+    void *dyp = nullptr, *dxp = nullptr;
     int rc = ensure_scratch(&p->dev_x, &p->dev_x_bytes, xb + 64);
     if (rc) return rc;
     if (cudaHostGetDevicePointer(&dyp, y, 0) == cudaSuccess) {
-      INVOP_CUDA(cudaMemcpyAsync(p->dev_x, x, xb, cudaMemcpyHostToDevice, s));
-      rc = apply_dl_launch(p, p->dev_x, dyp, true, s);
+      bool pdl = is_pinned(x) && cudaHostGetDevicePointer(&dxp, (void*)x, 0) == cudaSuccess;
+      if (pdl) {
+        k_pull_x<<<(unsigned)std::min<int64_t>(cdiv(p->n, 512), 64), 256, 0, s>>>(
+            (const double*)dxp, (double*)p->dev_x, p->n);
+        INVOP_LAUNCHED(1);
+      } else {
+        cudaGetLastError();
+        INVOP_CUDA(cudaMemcpyAsync(p->dev_x, x, xb, cudaMemcpyHostToDevice, s));
+      }
+      rc = apply_dl_launch(p, p->dev_x, dyp, true, s, pdl);
       if (rc == INVOP_OK) {
         INVOP_CUDA(cudaStreamSynchronize(s));
         return INVOP_OK;

@@ -130,7 +130,8 @@ int apply_tvw_launch(invop_plan* p, const float* x, float* y, cudaStream_t s);
 int apply_vw_launch(invop_plan* p, const float* x, float* y, cudaStream_t s);
 int hl_build(invop_plan* p, cudaStream_t s);
 int dl_build(invop_plan* p, cudaStream_t s);
-int apply_dl_launch(invop_plan* p, const void* x, void* y, bool f64io, cudaStream_t s);
+int apply_dl_launch(invop_plan* p, const void* x, void* y, bool f64io, cudaStream_t s,
+                    bool pdl = false);
 int apply_hl_launch(invop_plan* p, const float* x, float* y, cudaStream_t s);
 int apply_ordered_launch(const invop_plan* p, const double* x, int64_t ldx, double* y,
                          int64_t ldy, int64_t nrhs, cudaStream_t s);

@@ -476,6 +476,10 @@ __global__ void __launch_bounds__((CONS + 1) * 32, 1) k2_dl(DlArgs a) {
     uint32_t stepv = 0;             // bit t: chunk t of this warp lies inside the operator
     for (int slab = 0; slab < a.nslabs; ++slab) {
       stepv = 0;
+      // x may come from the preceding grid (programmatic dependent launch of
+      // the host entry: that grid pulls x over PCIe while the producer
+      // already streams the operator); a no-op for ordinary launches
+      if (slab == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
       // x piece of this warp -> 23-bit fixed point (warp-wide exponent):
       // one pass for max|x| and finiteness, one for the digits (SW > 2; the
       // values stay in registers for SW <= 2)
@@ -686,17 +690,27 @@ int dl_build(invop_plan* p, cudaStream_t s) {
 }
 
 template <int CONS, int G, int ROWS, bool F64IO>
-static void dl_launch(const DlArgs& a, int grid, size_t smem, cudaStream_t s) {
+static cudaError_t dl_launch(const DlArgs& a, int grid, size_t smem, bool pdl, cudaStream_t s) {
   static size_t smem_set = 0;            // opt-in once per instantiation and size
+  auto kern = k2_dl<CONS, G, ROWS, F64IO>;
   if (smem_set < smem) {
-    cudaFuncSetAttribute(k2_dl<CONS, G, ROWS, F64IO>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     smem_set = smem;
   }
-  k2_dl<CONS, G, ROWS, F64IO><<<grid, (CONS + 1) * 32, smem, s>>>(a);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3((CONS + 1) * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
-int apply_dl_launch(invop_plan* p, const void* x, void* y, bool f64io, cudaStream_t s) {
+int apply_dl_launch(invop_plan* p, const void* x, void* y, bool f64io, cudaStream_t s, bool pdl) {
   DlArgs a;
   a.data = p->dl_data;
   a.uoff = p->dl_uoff;
@@ -719,25 +733,27 @@ int apply_dl_launch(invop_plan* p, const void* x, void* y, bool f64io, cudaStrea
   int rows = 2;
   if (const char* v = getenv("INVOP_DL_ROWS")) rows = atoi(v) == 1 ? 1 : 2;
   const int key = cons * 1000 + p->dl_groups * 100 + rows * 10 + (f64io ? 1 : 0);
+  cudaError_t e = cudaSuccess;
   switch (key) {
-    case 16120: dl_launch<16, 1, 2, false>(a, p->dl_grid, smem, s); break;
-    case 16121: dl_launch<16, 1, 2, true>(a, p->dl_grid, smem, s); break;
-    case 16110: dl_launch<16, 1, 1, false>(a, p->dl_grid, smem, s); break;
-    case 16111: dl_launch<16, 1, 1, true>(a, p->dl_grid, smem, s); break;
-    case 16210: dl_launch<16, 2, 1, false>(a, p->dl_grid, smem, s); break;
-    case 16211: dl_launch<16, 2, 1, true>(a, p->dl_grid, smem, s); break;
-    case 16220: dl_launch<16, 2, 2, false>(a, p->dl_grid, smem, s); break;
-    case 16221: dl_launch<16, 2, 2, true>(a, p->dl_grid, smem, s); break;
-    case 8120: dl_launch<8, 1, 2, false>(a, p->dl_grid, smem, s); break;
-    case 8121: dl_launch<8, 1, 2, true>(a, p->dl_grid, smem, s); break;
-    case 8110: dl_launch<8, 1, 1, false>(a, p->dl_grid, smem, s); break;
-    case 8111: dl_launch<8, 1, 1, true>(a, p->dl_grid, smem, s); break;
-    case 8210: dl_launch<8, 2, 1, false>(a, p->dl_grid, smem, s); break;
-    case 8211: dl_launch<8, 2, 1, true>(a, p->dl_grid, smem, s); break;
-    case 8220: dl_launch<8, 2, 2, false>(a, p->dl_grid, smem, s); break;
-    case 8221: dl_launch<8, 2, 2, true>(a, p->dl_grid, smem, s); break;
+    case 16120: e = dl_launch<16, 1, 2, false>(a, p->dl_grid, smem, pdl, s); break;
+    case 16121: e = dl_launch<16, 1, 2, true>(a, p->dl_grid, smem, pdl, s); break;
+    case 16110: e = dl_launch<16, 1, 1, false>(a, p->dl_grid, smem, pdl, s); break;
+    case 16111: e = dl_launch<16, 1, 1, true>(a, p->dl_grid, smem, pdl, s); break;
+    case 16210: e = dl_launch<16, 2, 1, false>(a, p->dl_grid, smem, pdl, s); break;
+    case 16211: e = dl_launch<16, 2, 1, true>(a, p->dl_grid, smem, pdl, s); break;
+    case 16220: e = dl_launch<16, 2, 2, false>(a, p->dl_grid, smem, pdl, s); break;
+    case 16221: e = dl_launch<16, 2, 2, true>(a, p->dl_grid, smem, pdl, s); break;
+    case 8120: e = dl_launch<8, 1, 2, false>(a, p->dl_grid, smem, pdl, s); break;
+    case 8121: e = dl_launch<8, 1, 2, true>(a, p->dl_grid, smem, pdl, s); break;
+    case 8110: e = dl_launch<8, 1, 1, false>(a, p->dl_grid, smem, pdl, s); break;
+    case 8111: e = dl_launch<8, 1, 1, true>(a, p->dl_grid, smem, pdl, s); break;
+    case 8210: e = dl_launch<8, 2, 1, false>(a, p->dl_grid, smem, pdl, s); break;
+    case 8211: e = dl_launch<8, 2, 1, true>(a, p->dl_grid, smem, pdl, s); break;
+    case 8220: e = dl_launch<8, 2, 2, false>(a, p->dl_grid, smem, pdl, s); break;
+    case 8221: e = dl_launch<8, 2, 2, true>(a, p->dl_grid, smem, pdl, s); break;
     default: return fail(INVOP_E_VALUE, "k2_dl: unsupported consumer layout");
   }
+  if (e != cudaSuccess) return cuda_fail(e, "k2_dl launch");
   INVOP_LAUNCHED(1);
   INVOP_CHECK_LAUNCH("k2_dl");
   return INVOP_OK;
