@@ -85,6 +85,7 @@ extern "C" int invop_plan_destroy(invop_plan* p) {
   if (p->k3d_idx1) cudaFree(p->k3d_idx1);
   if (p->dl_data) cudaFree(p->dl_data);
   if (p->dl_uoff) cudaFree(p->dl_uoff);
+  if (p->dl_rowlo) cudaFree(p->dl_rowlo);
   if (p->host_pinned) cudaFreeHost(p->host_pinned);
   delete p;
   return INVOP_OK;
@@ -257,13 +258,16 @@ __global__ void k_pull_x(const double* __restrict__ xh, double* __restrict__ xd,
     xd[i] = xh[i];
 }
 
-static bool is_pinned(const void* ptr) {
+// device alias of page-locked (mapped) host memory; false for pageable memory
+static bool host_alias(const void* ptr, void** alias) {
   cudaPointerAttributes at;
-  if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+  if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess || at.type != cudaMemoryTypeHost ||
+      !at.devicePointer) {
     cudaGetLastError();
     return false;
   }
-  return at.type == cudaMemoryTypeHost;
+  *alias = at.devicePointer;
+  return true;
 }
 
 extern "C" int invop_apply_host(invop_plan* p, const double* x, double* y, int64_t nrhs,
@@ -273,32 +277,33 @@ extern "C" int invop_apply_host(invop_plan* p, const double* x, double* y, int64
   cudaStream_t s = (cudaStream_t)stream;
   size_t xb = (size_t)nrhs * p->n * sizeof(double);
   size_t yb = (size_t)nrhs * p->rows * sizeof(double);
-  if (mode == INVOP_MODE_FAST && nrhs == 1 && fast_route(p, 1) == ROUTE_DL && is_pinned(y) &&
-      dl_build(p, s) == INVOP_OK) {
+  void* ydev = nullptr;
+  if (mode == INVOP_MODE_FAST && nrhs == 1 && fast_route(p, 1) == ROUTE_DL &&
+      dl_build(p, s) == INVOP_OK && host_alias(y, &ydev)) {
     // page-locked y: the DL kernel writes its fp64 rows straight into host
     // memory (each row once; zero copy). x is read by every CTA, so it is
     // staged in device memory: page-locked x is pulled over PCIe by a small
     // grid that lets the apply grid start at once (programmatic dependent
     // launch: the producer streams the operator while x arrives; the
-    // consumers wait for it); otherwise one H2D copy.
-    void *dyp = nullptr, *dxp = nullptr;
+    // consumers wait for it); otherwise one H2D copy. (Polling a mapped
+    // completion word published by the grid's last CTA instead of
+    // synchronising the stream was measured slower: the system-scope fences
+    // at the grid's tail cost more than the synchronisation.)
     int rc = ensure_scratch(&p->dev_x, &p->dev_x_bytes, xb + 64);
     if (rc) return rc;
-    if (cudaHostGetDevicePointer(&dyp, y, 0) == cudaSuccess) {
-      bool pdl = is_pinned(x) && cudaHostGetDevicePointer(&dxp, (void*)x, 0) == cudaSuccess;
-      if (pdl) {
-        k_pull_x<<<(unsigned)std::min<int64_t>(cdiv(p->n, 512), 64), 256, 0, s>>>(
-            (const double*)dxp, (double*)p->dev_x, p->n);
-        INVOP_LAUNCHED(1);
-      } else {
-        cudaGetLastError();
-        INVOP_CUDA(cudaMemcpyAsync(p->dev_x, x, xb, cudaMemcpyHostToDevice, s));
-      }
-      rc = apply_dl_launch(p, p->dev_x, dyp, true, s, pdl);
-      if (rc == INVOP_OK) {
-        INVOP_CUDA(cudaStreamSynchronize(s));
-        return INVOP_OK;
-      }
+    void* xdev = nullptr;
+    const bool pdl = host_alias(x, &xdev);
+    if (pdl) {
+      k_pull_x<<<(unsigned)std::min<int64_t>(cdiv(p->n, 512), 64), 256, 0, s>>>(
+          (const double*)xdev, (double*)p->dev_x, p->n);
+      INVOP_LAUNCHED(1);
+    } else {
+      INVOP_CUDA(cudaMemcpyAsync(p->dev_x, x, xb, cudaMemcpyHostToDevice, s));
+    }
+    rc = apply_dl_launch(p, p->dev_x, ydev, true, s, pdl);
+    if (rc == INVOP_OK) {
+      INVOP_CUDA(cudaStreamSynchronize(s));
+      return INVOP_OK;
     }
     cudaGetLastError();
   }

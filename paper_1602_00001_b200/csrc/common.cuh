@@ -31,6 +31,7 @@ struct invop_plan {
   float* partial = nullptr; size_t partial_bytes = 0;
   int* counters = nullptr; size_t counters_n = 0;
   void* dev_x = nullptr; size_t dev_x_bytes = 0;
+
   void* dev_y = nullptr; size_t dev_y_bytes = 0;
   double* host_pinned = nullptr; size_t host_pinned_bytes = 0;
   // K3 (tensor-core batched apply): workspace and cached TMA descriptors
@@ -62,6 +63,8 @@ struct invop_plan {
   int64_t* dl_uoff = nullptr;       // [units+1] byte offsets, units in (CTA, slab, row) order
   int64_t dl_bytes = 0, dl_maxunit = 0;
   int dl_ready = 0, dl_grid = 0, dl_nslabs = 0, dl_groups = 1;
+  int64_t* dl_rowlo = nullptr;      // [grid + 1] CTA row ranges (byte-balanced)
+  int64_t dl_maxrows = 0;
   alignas(64) unsigned char k3_mapA[2][128];
   int k3_maps_ready = 0;
   // K3 on row residuals (batched.cu): digit-0 tiles for every (row tile, K

@@ -32,17 +32,23 @@
 #include "common.cuh"
 #include "ptx.cuh"
 #include <algorithm>
+#include <vector>
 
 namespace invop {
 
 constexpr int DL_SLAB = 16384;       // columns per unit: 32 chunks, one mask word
 constexpr int DL_HDR = 48;
 
-__host__ __device__ inline int dl_cta_of(int64_t r, int64_t rows, int grid) {
-  int b = (int)(r * grid / rows);
-  while (b + 1 < grid && (int64_t)(b + 1) * rows / grid <= r) ++b;
-  while (b > 0 && (int64_t)b * rows / grid > r) --b;
-  return b;
+// CTA of row r: row ranges [rowlo[b], rowlo[b+1]) chosen at build time so that
+// every CTA streams about the same number of bytes
+__host__ __device__ inline int dl_cta_of(int64_t r, const int64_t* rowlo, int grid) {
+  int lo = 0, hi = grid - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (rowlo[mid] <= r) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
 }
 
 // A CTA's rows [lo, lo + n) are split into G segments of consecutive rows
@@ -54,11 +60,11 @@ struct DlPos {
   int g;               // segment
   int64_t i;           // row index within the segment
 };
-__host__ __device__ inline DlPos dl_pos(int64_t r, int64_t rows, int grid, int G) {
+__host__ __device__ inline DlPos dl_pos(int64_t r, const int64_t* rowlo, int grid, int G) {
   DlPos p;
-  const int b = dl_cta_of(r, rows, grid);
-  p.lo = (int64_t)b * rows / grid;
-  p.n = (int64_t)(b + 1) * rows / grid - p.lo;
+  const int b = dl_cta_of(r, rowlo, grid);
+  p.lo = rowlo[b];
+  p.n = rowlo[b + 1] - p.lo;
   const int64_t l = r - p.lo, base = p.n / G, rem = p.n % G;
   if (l < rem * (base + 1)) {
     p.g = (int)(l / (base + 1));
@@ -111,11 +117,12 @@ struct DlBuild {
   int P, sgn;
   int64_t rows, n, ld;
   int nch, nslabs, grid, groups;
+  const int64_t* rowlo;       // [grid + 1] CTA row ranges
 };
 
 __device__ __forceinline__ void dl_residual16(const DlBuild& a, int64_t r, int c, int lane,
                                               int32_t* e) {
-  const DlPos ps = dl_pos(r, a.rows, a.grid, a.groups);
+  const DlPos ps = dl_pos(r, a.rowlo, a.grid, a.groups);
   const int order = (int)(ps.i < 2 ? ps.i : 2);
   const int64_t off = r * a.ld + (int64_t)c * 512 + lane * 16;
   dl_load16(a.planes, a.P, a.sgn, off, e);
@@ -152,9 +159,9 @@ __global__ void k_dl_width(DlBuild a, uint8_t* __restrict__ width) {
 
 // unit index of (row r, slab s) in processing order (CTA, slab, segment row,
 // segment)
-__host__ __device__ inline int64_t dl_unit(int64_t r, int s, int64_t rows, int nslabs, int grid,
-                                           int G) {
-  const DlPos p = dl_pos(r, rows, grid, G);
+__host__ __device__ inline int64_t dl_unit(int64_t r, int s, const int64_t* rowlo, int nslabs,
+                                           int grid, int G) {
+  const DlPos p = dl_pos(r, rowlo, grid, G);
   return p.lo * nslabs + (int64_t)s * p.n + p.i * G + p.g;
 }
 
@@ -172,7 +179,7 @@ __global__ void k_dl_units(DlBuild a, const uint8_t* __restrict__ width, uint4* 
     h[c >> 2] |= start << (8 * (c & 3));
     if (c < cn) start += width[r * a.nch + c0 + c];
   }
-  const int64_t u = dl_unit(r, s, a.rows, a.nslabs, a.grid, a.groups);
+  const int64_t u = dl_unit(r, s, a.rowlo, a.nslabs, a.grid, a.groups);
   for (int k = 0; k < 3; ++k) hdrs[3 * u + k] = make_uint4(h[4 * k], h[4 * k + 1], h[4 * k + 2], h[4 * k + 3]);
   const int64_t bytes = DL_HDR + 512 * (int64_t)start;
   size[u] = bytes;
@@ -220,7 +227,7 @@ __global__ void k_dl_write(DlBuild a, const uint4* __restrict__ hdrs,
   const int64_t r = gw / a.nch;
   const int c = (int)(gw - r * a.nch);
   const int s = c / 32, cl = c % 32;
-  const int64_t u = dl_unit(r, s, a.rows, a.nslabs, a.grid, a.groups);
+  const int64_t u = dl_unit(r, s, a.rowlo, a.nslabs, a.grid, a.groups);
   uint8_t* unit = data + off[u];
   const uint8_t* h = reinterpret_cast<const uint8_t*>(hdrs + 3 * u);
   if (cl == 0 && lane < 3) reinterpret_cast<uint4*>(unit)[lane] = hdrs[3 * u + lane];
@@ -235,6 +242,7 @@ struct DlArgs {
   const uint8_t* data;
   const int64_t* uoff;          // [units + 1]
   const uint8_t* planes[3];     // plain codes, for warps whose x piece is not finite
+  const int64_t* rowlo;         // [grid + 1] CTA row ranges
   int P, sgn;
   int64_t rows, n, ld;
   int nslabs;
@@ -418,8 +426,8 @@ __global__ void __launch_bounds__((CONS + 1) * 32, 1) k2_dl(DlArgs a) {
   const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
   const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(bars);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t row_lo = (int64_t)blockIdx.x * a.rows / gridDim.x;
-  const int64_t row_hi = (int64_t)(blockIdx.x + 1) * a.rows / gridDim.x;
+  const int64_t row_lo = a.rowlo[blockIdx.x];
+  const int64_t row_hi = a.rowlo[blockIdx.x + 1];
   const int64_t nrows = row_hi - row_lo;
   const int64_t units = nrows * a.nslabs;
   const int64_t ubase = row_lo * a.nslabs;
@@ -602,6 +610,12 @@ __global__ void __launch_bounds__((CONS + 1) * 32, 1) k2_dl(DlArgs a) {
   }
 }
 
+static bool layout_flag_dl(const char* env, bool dflt) {
+  const char* v = getenv(env);
+  if (!v || !*v) return dflt;
+  return *v != '0';
+}
+
 static int dl_consumers() {
   const char* v = getenv("INVOP_DL_CONS");
   return v && atoi(v) == 8 ? 8 : 16;
@@ -616,7 +630,7 @@ static int dl_groups_for(int64_t rows_per_cta) {
 
 // shared memory besides the ring: slot + unit offsets of the largest CTA
 static size_t dl_side_bytes(const invop_plan* p, int cons) {
-  const int64_t rpc = cdiv(p->rows, p->dl_grid);
+  const int64_t rpc = p->dl_maxrows;
   return (size_t)rpc * (cons / p->dl_groups) * 8 + (size_t)(rpc * p->dl_nslabs + 1) * 8 + 64 +
          DL_NS * 24;
 }
@@ -656,7 +670,43 @@ int dl_build(invop_plan* p, cudaStream_t s) {
   INVOP_CUDA(cudaMalloc(&p->dl_uoff, (size_t)(units + 1) * 8));
   INVOP_CUDA(cudaMemsetAsync(dmax, 0, 8, s));
   const int64_t warps = p->rows * a.nch;
+  // CTA row ranges: equal row counts. INVOP_DL_BALANCE=1 re-cuts them so that
+  // every CTA gets the same bytes plus per-row work (rows near the domain
+  // boundary have smaller residuals: +8 % bytes max/mean at config 4); measured
+  // neutral to slower (the consumers are bound by per-row work), so off. The
+  // widths are recomputed because residual orders restart at every range start
+  std::vector<int64_t> lo(a.grid + 1);
+  for (int b = 0; b <= a.grid; ++b) lo[b] = (int64_t)b * p->rows / a.grid;
+  if (!p->dl_rowlo) INVOP_CUDA(cudaMalloc(&p->dl_rowlo, (size_t)(a.grid + 1) * 8));
+  INVOP_CUDA(cudaMemcpyAsync(p->dl_rowlo, lo.data(), lo.size() * 8, cudaMemcpyHostToDevice, s));
+  a.rowlo = p->dl_rowlo;
   k_dl_width<<<(unsigned)cdiv(warps * 32, 256), 256, 0, s>>>(a, width);
+  if (a.grid > 1 && layout_flag_dl("INVOP_DL_BALANCE", false)) {
+    std::vector<uint8_t> w((size_t)p->rows * a.nch);
+    INVOP_CUDA(cudaMemcpyAsync(w.data(), width, w.size(), cudaMemcpyDeviceToHost, s));
+    INVOP_CUDA(cudaStreamSynchronize(s));
+    std::vector<double> pre(p->rows + 1, 0.0);
+    // per-row consumer work in byte equivalents (~100 instructions per warp
+    // and row against 13 per 512-byte plane: ~64 KB)
+    double rowcost = 65536.0;
+    if (const char* v = getenv("INVOP_DL_ROWCOST")) rowcost = atof(v);
+    for (int64_t r = 0; r < p->rows; ++r) {
+      int64_t planes = 0;
+      for (int c = 0; c < a.nch; ++c) planes += w[(size_t)r * a.nch + c];
+      pre[r + 1] = pre[r] + rowcost * a.nslabs + 512.0 * (double)planes;   // + per-row work
+    }
+    for (int b = 1; b < a.grid; ++b) {
+      const double target = pre[p->rows] * b / a.grid;
+      int64_t r = std::lower_bound(pre.begin(), pre.end(), target) - pre.begin();
+      r = std::max<int64_t>(r, lo[b - 1] + 2);
+      r = std::min<int64_t>(r, p->rows - 2 * (a.grid - b));
+      lo[b] = r;
+    }
+    INVOP_CUDA(cudaMemcpyAsync(p->dl_rowlo, lo.data(), lo.size() * 8, cudaMemcpyHostToDevice, s));
+    k_dl_width<<<(unsigned)cdiv(warps * 32, 256), 256, 0, s>>>(a, width);
+  }
+  p->dl_maxrows = 0;
+  for (int b = 0; b < a.grid; ++b) p->dl_maxrows = std::max<int64_t>(p->dl_maxrows, lo[b + 1] - lo[b]);
   k_dl_units<<<(unsigned)cdiv(units, 256), 256, 0, s>>>(a, width, hdrs, size, dmax);
   k_dl_scan<<<1, 1024, 0, s>>>(units, size, p->dl_uoff);
   int64_t total = 0;
@@ -714,6 +764,7 @@ int apply_dl_launch(invop_plan* p, const void* x, void* y, bool f64io, cudaStrea
   DlArgs a;
   a.data = p->dl_data;
   a.uoff = p->dl_uoff;
+  a.rowlo = p->dl_rowlo;
   for (int b = 0; b < 3; ++b) a.planes[b] = p->planes[b < p->P ? b : 0];
   a.P = p->P;
   a.sgn = p->is_signed;
