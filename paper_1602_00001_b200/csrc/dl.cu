@@ -671,10 +671,12 @@ int dl_build(invop_plan* p, cudaStream_t s) {
   INVOP_CUDA(cudaMemsetAsync(dmax, 0, 8, s));
   const int64_t warps = p->rows * a.nch;
   // CTA row ranges: equal row counts. INVOP_DL_BALANCE=1 re-cuts them so that
-  // every CTA gets the same bytes plus per-row work (rows near the domain
-  // boundary have smaller residuals: +8 % bytes max/mean at config 4); measured
-  // neutral to slower (the consumers are bound by per-row work), so off. The
-  // widths are recomputed because residual orders restart at every range start
+  // every CTA gets the same sum over its rows of max(streaming bytes, per-row
+  // consumer time in bytes) (rows near the domain boundary have smaller
+  // residuals: +8 % bytes max/mean at config 4). Measured at config 4: pure
+  // byte balance 10 % slower, the max() model 0.8 % faster; off by default.
+  // The widths are recomputed because residual orders restart at every range
+  // start.
   std::vector<int64_t> lo(a.grid + 1);
   for (int b = 0; b <= a.grid; ++b) lo[b] = (int64_t)b * p->rows / a.grid;
   if (!p->dl_rowlo) INVOP_CUDA(cudaMalloc(&p->dl_rowlo, (size_t)(a.grid + 1) * 8));
@@ -686,14 +688,16 @@ int dl_build(invop_plan* p, cudaStream_t s) {
     INVOP_CUDA(cudaMemcpyAsync(w.data(), width, w.size(), cudaMemcpyDeviceToHost, s));
     INVOP_CUDA(cudaStreamSynchronize(s));
     std::vector<double> pre(p->rows + 1, 0.0);
-    // per-row consumer work in byte equivalents (~100 instructions per warp
-    // and row against 13 per 512-byte plane: ~64 KB)
-    double rowcost = 65536.0;
+    // per-row consumer time in bytes streamed meanwhile (~0.63 us per row at
+    // ~44 GB/s per SM: ~27 KB per 16384-column slab)
+    double rowcost = 27648.0;
     if (const char* v = getenv("INVOP_DL_ROWCOST")) rowcost = atof(v);
     for (int64_t r = 0; r < p->rows; ++r) {
       int64_t planes = 0;
       for (int c = 0; c < a.nch; ++c) planes += w[(size_t)r * a.nch + c];
-      pre[r + 1] = pre[r] + rowcost * a.nslabs + 512.0 * (double)planes;   // + per-row work
+      // a row costs its streaming time or its consumer time, whichever is
+      // longer (the pipeline overlaps the two)
+      pre[r + 1] = pre[r] + std::max(rowcost * a.nslabs, 48.0 * a.nslabs + 512.0 * (double)planes);
     }
     for (int b = 1; b < a.grid; ++b) {
       const double target = pre[p->rows] * b / a.grid;
