@@ -299,6 +299,36 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
           const uint64_t dzero = desc_sw64(smem_u32(zero_tile));
           const uint32_t id_lo = idesc_i8(DL ? 1 : 0), id_hi = idesc_i8(DL ? 1 : a.hi_signed);
           const uint32_t mask = DL ? s_mask[st] : 0xffffffffu;
+          if constexpr (DL && P == 2 && K3_ND == 3) {
+            // straight-line issue (the generic loop below spends more issue
+            // slots on its per-MMA control flow than the tensor core needs):
+            // class w = plane + digit; classes 0-2 are started by plane 0,
+            // class 3 by plane 1 or, when the unit's first K block has no
+            // digit-1 tile, by a zero tile
+#pragma unroll
+            for (int kk = 0; kk < K3_BK / 32; ++kk) {
+              const uint32_t cont = (i > 0 || kk > 0) ? 1u : 0u;
+              const uint64_t db0 = dbase + (uint64_t)((A_BYTES + 0 * K3_B_TILE + kk * 32) >> 4);
+              const uint64_t db1 = dbase + (uint64_t)((A_BYTES + 1 * K3_B_TILE + kk * 32) >> 4);
+              const uint64_t db2 = dbase + (uint64_t)((A_BYTES + 2 * K3_B_TILE + kk * 32) >> 4);
+#pragma unroll
+              for (int ti = 0; ti < TILES; ++ti) {
+                const uint32_t t0 = tmem + (uint32_t)(ti * NACC * K3_NR);
+                const uint64_t a0 = dbase + (uint64_t)(((ti * P + 0) * K3_A_TILE + kk * 32) >> 4);
+                mma_i8_elect(t0 + 0 * K3_NR, a0, db0, id_lo, cont);
+                mma_i8_elect(t0 + 1 * K3_NR, a0, db1, id_lo, cont);
+                mma_i8_elect(t0 + 2 * K3_NR, a0, db2, id_lo, cont);
+                if ((mask >> ti) & 1u) {                     // warp-uniform
+                  const uint64_t a1 = dbase + (uint64_t)(((ti * P + 1) * K3_A_TILE + kk * 32) >> 4);
+                  mma_i8_elect(t0 + 1 * K3_NR, a1, db0, id_hi, 1u);
+                  mma_i8_elect(t0 + 2 * K3_NR, a1, db1, id_hi, 1u);
+                  mma_i8_elect(t0 + 3 * K3_NR, a1, db2, id_hi, cont);
+                } else if (!cont) {
+                  mma_i8_elect(t0 + 3 * K3_NR, dzero + (uint64_t)((kk * 32) >> 4), db2, id_hi, 0u);
+                }
+              }
+            }
+          } else
 #pragma unroll
           for (int kk = 0; kk < K3_BK / 32; ++kk) {
 #pragma unroll
