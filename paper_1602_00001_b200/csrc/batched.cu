@@ -166,8 +166,8 @@ __device__ __forceinline__ void tmem_wait_ld() {
 }
 
 // kind::i8 instruction descriptor: D=s32, A u8/s8, B s8, both K-major
-__host__ __device__ constexpr uint32_t idesc_i8(int a_signed) {
-  return (2u << 4) | ((uint32_t)a_signed << 7) | (1u << 10) | ((uint32_t)(K3_NR >> 3) << 17) |
+__host__ __device__ constexpr uint32_t idesc_i8(int a_signed, int n = K3_NR) {
+  return (2u << 4) | ((uint32_t)a_signed << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) |
          ((uint32_t)(K3_BM >> 4) << 24);
 }
 
@@ -300,31 +300,29 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
           const uint32_t id_lo = idesc_i8(DL ? 1 : 0), id_hi = idesc_i8(DL ? 1 : a.hi_signed);
           const uint32_t mask = DL ? s_mask[st] : 0xffffffffu;
           if constexpr (DL && P == 2 && K3_ND == 3) {
-            // straight-line issue (the generic loop below spends more issue
-            // slots on its per-MMA control flow than the tensor core needs):
-            // class w = plane + digit; classes 0-2 are started by plane 0,
-            // class 3 by plane 1 or, when the unit's first K block has no
-            // digit-1 tile, by a zero tile
+            // straight-line issue with N = 192: the three digit tiles of B
+            // are contiguous in shared memory and the weight classes of a
+            // tile are contiguous in TMEM (class w = plane + digit at column
+            // 64 w), so plane 0 x all digits is ONE MMA into classes 0-2 and
+            // plane 1 x all digits one MMA into classes 1-3 (a third of the
+            // MMAs of the N = 64 form; the tensor core re-reads A per MMA).
+            // Class 3 is started by a zero tile at the unit's first K block.
+            const uint32_t id0 = idesc_i8(1, K3_ND * K3_NR);
 #pragma unroll
             for (int kk = 0; kk < K3_BK / 32; ++kk) {
               const uint32_t cont = (i > 0 || kk > 0) ? 1u : 0u;
-              const uint64_t db0 = dbase + (uint64_t)((A_BYTES + 0 * K3_B_TILE + kk * 32) >> 4);
-              const uint64_t db1 = dbase + (uint64_t)((A_BYTES + 1 * K3_B_TILE + kk * 32) >> 4);
-              const uint64_t db2 = dbase + (uint64_t)((A_BYTES + 2 * K3_B_TILE + kk * 32) >> 4);
+              const uint64_t db = dbase + (uint64_t)((A_BYTES + kk * 32) >> 4);
 #pragma unroll
               for (int ti = 0; ti < TILES; ++ti) {
                 const uint32_t t0 = tmem + (uint32_t)(ti * NACC * K3_NR);
+                if (!cont)
+                  mma_i8_elect(t0 + 3 * K3_NR, dzero + (uint64_t)((kk * 32) >> 4),
+                               dbase + (uint64_t)((A_BYTES + 2 * K3_B_TILE + kk * 32) >> 4), id_hi, 0u);
                 const uint64_t a0 = dbase + (uint64_t)(((ti * P + 0) * K3_A_TILE + kk * 32) >> 4);
-                mma_i8_elect(t0 + 0 * K3_NR, a0, db0, id_lo, cont);
-                mma_i8_elect(t0 + 1 * K3_NR, a0, db1, id_lo, cont);
-                mma_i8_elect(t0 + 2 * K3_NR, a0, db2, id_lo, cont);
+                mma_i8_elect(t0, a0, db, id0, cont);
                 if ((mask >> ti) & 1u) {                     // warp-uniform
                   const uint64_t a1 = dbase + (uint64_t)(((ti * P + 1) * K3_A_TILE + kk * 32) >> 4);
-                  mma_i8_elect(t0 + 1 * K3_NR, a1, db0, id_hi, 1u);
-                  mma_i8_elect(t0 + 2 * K3_NR, a1, db1, id_hi, 1u);
-                  mma_i8_elect(t0 + 3 * K3_NR, a1, db2, id_hi, cont);
-                } else if (!cont) {
-                  mma_i8_elect(t0 + 3 * K3_NR, dzero + (uint64_t)((kk * 32) >> 4), db2, id_hi, 0u);
+                  mma_i8_elect(t0 + 1 * K3_NR, a1, db, id0, 1u);
                 }
               }
             }
