@@ -48,6 +48,11 @@ constexpr int K3_BK = 64;             // K bytes per stage (SWIZZLE_64B row)
 constexpr int K3_NR = 64;             // right-hand sides per MMA (N)
 constexpr int K3_ND = 3;              // x digits
 constexpr int K3_STAGES = 4;
+#ifndef K3_DL_STAGES_OVERRIDE
+constexpr int K3_DL_STAGES = 5;       // DL: 44 KB stages + a 4 KB zero B tile fit 5
+#else
+constexpr int K3_DL_STAGES = K3_DL_STAGES_OVERRIDE;
+#endif
 constexpr int K3_THREADS = 192;       // warp0 TMA, warp1 MMA+TMEM, warps 2-5 epilogue
 constexpr int K3_KMAX = 32768;        // max columns per work unit (int32 safety)
 
@@ -188,11 +193,13 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], tfull, tempty;
   __shared__ uint32_t tmem_slot;
   __shared__ uint32_t s_mask[STAGES];                       // DL: tiles whose digit-1 plane is loaded
-  // DL: an all-zero A tile after the stages (initialises the accumulator that
-  // only digit-1 planes feed when the unit's first K block has none)
+  // DL: an all-zero operand tile after the stages (initialises the
+  // accumulator that only digit-1 planes feed when the unit's first K block
+  // has none): a B tile (4 KB) for the straight-line issue, an A tile otherwise
+  constexpr int ZERO_BYTES = (P == 2 && K3_ND == 3) ? K3_B_TILE : K3_A_TILE;
   unsigned char* zero_tile = base + (size_t)STAGES * STAGE;
   if (DL) {
-    for (int i = threadIdx.x; i < K3_A_TILE / 16; i += blockDim.x)
+    for (int i = threadIdx.x; i < ZERO_BYTES / 16; i += blockDim.x)
       reinterpret_cast<uint4*>(zero_tile)[i] = make_uint4(0, 0, 0, 0);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -315,10 +322,9 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
 #pragma unroll
               for (int ti = 0; ti < TILES; ++ti) {
                 const uint32_t t0 = tmem + (uint32_t)(ti * NACC * K3_NR);
-                if (!cont)
-                  mma_i8_elect(t0 + 3 * K3_NR, dzero + (uint64_t)((kk * 32) >> 4),
-                               dbase + (uint64_t)((A_BYTES + 2 * K3_B_TILE + kk * 32) >> 4), id_hi, 0u);
                 const uint64_t a0 = dbase + (uint64_t)(((ti * P + 0) * K3_A_TILE + kk * 32) >> 4);
+                if (!cont)                                    // class 3 = A x 0
+                  mma_i8_elect(t0 + 3 * K3_NR, a0, dzero + (uint64_t)((kk * 32) >> 4), id_hi, 0u);
                 mma_i8_elect(t0, a0, db, id0, cont);
                 if ((mask >> ti) & 1u) {                     // warp-uniform
                   const uint64_t a1 = dbase + (uint64_t)(((ti * P + 1) * K3_A_TILE + kk * 32) >> 4);
@@ -757,7 +763,7 @@ template <int P, int TILES, int STAGES, bool DL = false>
 static int launch_k3(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b,
                      const K3Args& args, int grid, cudaStream_t s) {
   constexpr int STAGE = TILES * P * K3_A_TILE + K3_ND * K3_B_TILE;
-  size_t smem = (size_t)STAGES * STAGE + 1024 + (DL ? K3_A_TILE : 0);
+  size_t smem = (size_t)STAGES * STAGE + 1024 + (DL ? (P == 2 ? K3_B_TILE : K3_A_TILE) : 0);
   auto kern = k3_batched<P, TILES, STAGES, DL>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   kern<<<grid, K3_THREADS, smem, s>>>(a0, a1, b, args);
@@ -865,7 +871,7 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
   size_t acc_off = round_up(max_off + (size_t)nrhs * 4, 256);
   int krc = k3d_build(p, s);
   if (krc != INVOP_OK && krc != INVOP_E_UNSUPPORTED) return krc;
-  const bool dl = p->k3d_ready > 0 && tiles == 2 && stages == 4;
+  const bool dl = p->k3d_ready > 0 && tiles == 2 && stages == 4;   // default config -> DL kernel
   size_t acc_bytes = splits > 1 ? (size_t)K3_NR * p->rows * 8 : 0;
   if (dl)   // + segment carries of the row prefix sums
     acc_bytes = (size_t)K3_NR * p->rows * 8 + (size_t)K3_NR * cdiv(p->rows, K3D_SEG) * 16;
@@ -928,7 +934,7 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
     const CUtensorMap* A1 = (const CUtensorMap*)(dl ? p->k3d_mapA[1] : p->k3_mapA[1]);
     const int key = dl ? 999 : p->P * 100 + tiles * 10 + stages;
     switch (key) {
-      case 999: rc = launch_k3<2, 2, 4, true>(*A0, *A1, mapB, a, grid, s); break;
+      case 999: rc = launch_k3<2, 2, K3_DL_STAGES, true>(*A0, *A1, mapB, a, grid, s); break;
       case 124: rc = launch_k3<1, 2, 4>(*A0, *A1, mapB, a, grid, s); break;
       case 116: rc = launch_k3<1, 1, 6>(*A0, *A1, mapB, a, grid, s); break;
       case 224: rc = launch_k3<2, 2, 4>(*A0, *A1, mapB, a, grid, s); break;
