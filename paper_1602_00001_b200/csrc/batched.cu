@@ -879,17 +879,23 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
   if (rc) return rc;
   unsigned int* maxbits = (unsigned int*)((char*)p->k3_ws + max_off);
   int* flag = (int*)((char*)p->k3_ws + flag_off);
-  // max|x_t| of every right-hand side in one launch; inf/nan in x needs the
-  // reference's zero-mantissa skip (fp32 masked kernels): one small sync
+  // max|x_t| of every right-hand side in one launch. inf/nan in x needs the
+  // reference's zero-mantissa skip (fp32 masked kernels): the flag travels to
+  // page-locked host memory behind an event while the tensor-core apply is
+  // enqueued speculatively; the host reads it once the event fires (the GPU
+  // is busy with the apply meanwhile) and, if set, enqueues the masked apply,
+  // which overwrites y in stream order.
+  if (!p->k3_flag_host) {
+    INVOP_CUDA(cudaHostAlloc((void**)&p->k3_flag_host, 64, cudaHostAllocDefault));
+    INVOP_CUDA(cudaEventCreateWithFlags(&p->k3_flag_event, cudaEventDisableTiming));
+  }
   {
     INVOP_CUDA(cudaMemsetAsync((char*)p->k3_ws + flag_off, 0, max_off - flag_off + (size_t)nrhs * 4, s));
     dim3 g((unsigned)std::min<int64_t>(cdiv(p->n, 256), 64), (unsigned)nrhs);
     k3_xmax<<<g, 256, 0, s>>>(x, p->n, ldx, maxbits, flag);
     INVOP_LAUNCHED(1);
-    int h = 0;
-    INVOP_CUDA(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
-    INVOP_CUDA(cudaStreamSynchronize(s));
-    if (h) return apply_fast_launch(p, x, ldx, y, ldy, nrhs, s);
+    INVOP_CUDA(cudaMemcpyAsync(p->k3_flag_host, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    INVOP_CUDA(cudaEventRecord(p->k3_flag_event, s));
   }
   if (rc) return rc;
   int8_t* B = (int8_t*)p->k3_ws;
@@ -964,6 +970,8 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
     }
   }
   INVOP_CHECK_LAUNCH("k3 epilogue");
+  INVOP_CUDA(cudaEventSynchronize(p->k3_flag_event));
+  if (*(volatile int*)p->k3_flag_host) return apply_fast_launch(p, x, ldx, y, ldy, nrhs, s);
   return INVOP_OK;
 }
 

@@ -642,3 +642,15 @@ def test_k3_row_residuals(invop, O, rows, N, k, splits, monkeypatch):
     for t in (0, k // 2, k - 1):
         yo = O.ordered_apply(mant, 4, Xr[t])
         assert relerr(Y_dl[t], yo) <= F32_TOL
+    # non-finite x: the speculative tensor-core result is replaced by the
+    # masked fp32 apply (reference zero skip) in stream order
+    monkeypatch.setenv("INVOP_K3_DL", "1")
+    X2 = X.copy()
+    X2[1, 7] = np.inf
+    Y2 = dplan.apply_device(torch.tensor(X2, device="cuda", dtype=torch.float32), mode=0).cpu().numpy()
+    Yo2 = O.ordered_apply(mant, 4, X2[1].astype(np.float32).astype(np.float64))
+    assert np.array_equal(np.isfinite(Y2[1]), np.isfinite(Yo2))
+    fin = np.isfinite(Yo2)
+    assert relerr(Y2[1][fin], Yo2[fin]) <= F32_TOL
+    yo0 = O.ordered_apply(mant, 4, Xr[0])
+    assert relerr(Y2[0], yo0) <= F32_TOL
