@@ -276,9 +276,8 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
               if (P > 1) tma_2d(sb + (ti * P + 1) * K3_A_TILE, &mapA1, 0, trow, fb, pol_a);
             }
           }
-#pragma unroll
-          for (int l = 0; l < K3_ND; ++l)
-            tma_2d(sb + A_BYTES + l * K3_B_TILE, &mapB, kb * K3_BK, l * K3_NR, fb, pol_b);
+          // the three digit tiles are consecutive rows of B: one 192-row box
+          tma_2d(sb + A_BYTES, &mapB, kb * K3_BK, 0, fb, pol_b);
           if (++st == STAGES) { st = 0; ph ^= 1; }
         }
       }
@@ -920,7 +919,7 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
     p->k3_maps_ready = 1;
   }
   CUtensorMap mapB;
-  rc = make_map_u8(&mapB, B, ldb, (uint64_t)K3_ND * K3_NR, ldb, K3_BK, K3_NR);
+  rc = make_map_u8(&mapB, B, ldb, (uint64_t)K3_ND * K3_NR, ldb, K3_BK, K3_ND * K3_NR);
   if (rc) return rc;
   for (int64_t t0 = 0; t0 < nrhs; t0 += K3_NR) {
     const int nr = (int)std::min<int64_t>(K3_NR, nrhs - t0);
