@@ -76,6 +76,8 @@ struct K3Args {
   const int* idx1;         // DL: compact index of a tile's digit-1 plane, -1 if absent
 };
 
+__host__ __device__ inline int64_t k3d_tile0(int64_t rt, int64_t kb, int64_t kbs);
+
 // ------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -260,11 +262,21 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
             }
             s_mask[st] = mask;
             k3_expect_tx(fb, bytes);
+            if (P == 2 && TILES == 2) {
+              // stage: [digit-0 tile 0][digit-0 tile 1][digit-1 tile 0][digit-1 tile 1]
+              const int trow = (int)(k3d_tile0(row0 / K3_BM, kb, a.kb_stride) * K3_BM);
+              tma_2d(sb, &mapA0, 0, trow, fb, pol_a);         // both digit-0 tiles
 #pragma unroll
-            for (int ti = 0; ti < TILES; ++ti) {
-              const int trow = (int)(((int64_t)(row0 / K3_BM + ti) * a.kb_stride + kb) * K3_BM);
-              tma_2d(sb + (ti * P + 0) * K3_A_TILE, &mapA0, 0, trow, fb, pol_a);
-              if (i1[ti] >= 0) tma_2d(sb + (ti * P + 1) * K3_A_TILE, &mapA1, 0, i1[ti] * K3_BM, fb, pol_a);
+              for (int ti = 0; ti < TILES; ++ti)
+                if (i1[ti] >= 0)
+                  tma_2d(sb + (TILES + ti) * K3_A_TILE, &mapA1, 0, i1[ti] * K3_BM, fb, pol_a);
+            } else {
+#pragma unroll
+              for (int ti = 0; ti < TILES; ++ti) {
+                const int trow = (int)(k3d_tile0(row0 / K3_BM + ti, kb, a.kb_stride) * K3_BM);
+                tma_2d(sb + (ti * P + 0) * K3_A_TILE, &mapA0, 0, trow, fb, pol_a);
+                if (i1[ti] >= 0) tma_2d(sb + (ti * P + 1) * K3_A_TILE, &mapA1, 0, i1[ti] * K3_BM, fb, pol_a);
+              }
             }
           } else {
             k3_expect_tx(fb, STAGE);
@@ -321,12 +333,12 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
 #pragma unroll
               for (int ti = 0; ti < TILES; ++ti) {
                 const uint32_t t0 = tmem + (uint32_t)(ti * NACC * K3_NR);
-                const uint64_t a0 = dbase + (uint64_t)(((ti * P + 0) * K3_A_TILE + kk * 32) >> 4);
+                const uint64_t a0 = dbase + (uint64_t)((ti * K3_A_TILE + kk * 32) >> 4);
                 if (!cont)                                    // class 3 = A x 0
                   mma_i8_elect(t0 + 3 * K3_NR, a0, dzero + (uint64_t)((kk * 32) >> 4), id_hi, 0u);
                 mma_i8_elect(t0, a0, db, id0, cont);
                 if ((mask >> ti) & 1u) {                     // warp-uniform
-                  const uint64_t a1 = dbase + (uint64_t)(((ti * P + 1) * K3_A_TILE + kk * 32) >> 4);
+                  const uint64_t a1 = dbase + (uint64_t)(((TILES + ti) * K3_A_TILE + kk * 32) >> 4);
                   mma_i8_elect(t0 + 1 * K3_NR, a1, db, id0, 1u);
                 }
               }
@@ -523,6 +535,12 @@ struct K3DBuild {
   int64_t kbs, rtiles;
 };
 
+// digit-0 tiles: the two row tiles of a pair at the same K block are adjacent,
+// so one 256-row TMA box loads both
+__host__ __device__ inline int64_t k3d_tile0(int64_t rt, int64_t kb, int64_t kbs) {
+  return ((rt >> 1) * kbs + kb) * 2 + (rt & 1);
+}
+
 __device__ __forceinline__ int32_t k3d_resid(const K3DBuild& a, int64_t r, int64_t j) {
   if (r < 2 || r >= a.rows) return 0;
   const int64_t off = r * a.ld + j;
@@ -580,7 +598,7 @@ __global__ void k3d_write(K3DBuild a, const int* __restrict__ idx1, uint8_t* __r
   const int64_t r = t / a.kbs, kb = t - r * a.kbs;
   const int64_t tile = (r / K3_BM) * a.kbs + kb;
   const int i1 = idx1[tile];
-  uint8_t* d0 = t0 + tile * K3_A_TILE + (r % K3_BM) * K3_BK;
+  uint8_t* d0 = t0 + k3d_tile0(r / K3_BM, kb, a.kbs) * K3_A_TILE + (r % K3_BM) * K3_BK;
   uint8_t* d1 = i1 >= 0 ? t1 + (int64_t)i1 * K3_A_TILE + (r % K3_BM) * K3_BK : nullptr;
   for (int q0 = 0; q0 < K3_BK; q0 += 16) {
     uint32_t w0[4] = {0, 0, 0, 0}, w1[4] = {0, 0, 0, 0};
@@ -810,7 +828,7 @@ static int k3d_build(invop_plan* p, cudaStream_t s) {
       k3d_write<<<(unsigned)cdiv(thr, 256), 256, 0, s>>>(a, p->k3d_idx1, p->k3d_tiles[0],
                                                          p->k3d_tiles[1]);
       rc = make_map_u8((CUtensorMap*)p->k3d_mapA[0], p->k3d_tiles[0], K3_BK,
-                       (uint64_t)tiles * K3_BM, K3_BK, K3_BK, K3_BM);
+                       (uint64_t)tiles * K3_BM, K3_BK, K3_BK, p->P == 2 ? 2 * K3_BM : K3_BM);
       if (!rc)
         rc = make_map_u8((CUtensorMap*)p->k3d_mapA[1], p->k3d_tiles[1], K3_BK,
                          (uint64_t)std::max<int64_t>(p->k3d_n1, 1) * K3_BM, K3_BK, K3_BK, K3_BM);
