@@ -250,6 +250,7 @@ struct DlArgs {
   const void* x;                // fp32, or fp64 when F64IO (rounded to fp32 on load)
   void* y;                      // fp32, or fp64 when F64IO (the fp32 result widened)
   int ring_bytes;               // variable-size unit ring (FIFO) in shared memory
+  int x_dep;                    // x is written by the preceding grid (host entry)
 };
 
 #ifndef DL_NS_OVERRIDE
@@ -425,6 +426,11 @@ __global__ void __launch_bounds__((CONS + 1) * 32, 1) k2_dl(DlArgs a) {
   double* slot = reinterpret_cast<double*>(s_pos + 2 * S);
   const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
   const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(bars);
+  // the next apply in the stream (launched as a programmatic dependent) may
+  // take SMs as soon as this grid's CTAs retire: its producers start
+  // streaming while this grid's slowest CTAs finish; it waits for this grid
+  // before writing y (griddepcontrol.wait below)
+  if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row_lo = a.rowlo[blockIdx.x];
   const int64_t row_hi = a.rowlo[blockIdx.x + 1];
@@ -487,7 +493,7 @@ __global__ void __launch_bounds__((CONS + 1) * 32, 1) k2_dl(DlArgs a) {
       // x may come from the preceding grid (programmatic dependent launch of
       // the host entry: that grid pulls x over PCIe while the producer
       // already streams the operator); a no-op for ordinary launches
-      if (slab == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
+      if (slab == 0 && a.x_dep) asm volatile("griddepcontrol.wait;" ::: "memory");
       // x piece of this warp -> 23-bit fixed point (warp-wide exponent):
       // one pass for max|x| and finiteness, one for the digits (SW > 2; the
       // values stay in registers for SW <= 2)
@@ -600,6 +606,7 @@ __global__ void __launch_bounds__((CONS + 1) * 32, 1) k2_dl(DlArgs a) {
     }
   }
   __syncthreads();
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // the preceding grid's y is done
   for (int64_t r = threadIdx.x; r < nrows; r += blockDim.x) {
     double s = 0.0;
 #pragma unroll
@@ -614,6 +621,13 @@ static bool layout_flag_dl(const char* env, bool dflt) {
   const char* v = getenv(env);
   if (!v || !*v) return dflt;
   return *v != '0';
+}
+
+// every apply is launched as a programmatic dependent of the preceding grid
+// (overlaps the previous apply's tail); INVOP_DL_PDL=0 disables
+static bool dl_pdl_env() {
+  const char* v = getenv("INVOP_DL_PDL");
+  return !(v && *v == '0');
 }
 
 static int dl_consumers() {
@@ -776,6 +790,7 @@ int apply_dl_launch(invop_plan* p, const void* x, void* y, bool f64io, cudaStrea
   a.nslabs = p->dl_nslabs;
   a.scale = p->scale;
   a.x = x; a.y = y;
+  a.x_dep = pdl ? 1 : 0;
   int cons = dl_consumers();
   if (cons % p->dl_groups) cons = 16;
   const size_t side = dl_side_bytes(p, cons);
@@ -790,22 +805,22 @@ int apply_dl_launch(invop_plan* p, const void* x, void* y, bool f64io, cudaStrea
   const int key = cons * 1000 + p->dl_groups * 100 + rows * 10 + (f64io ? 1 : 0);
   cudaError_t e = cudaSuccess;
   switch (key) {
-    case 16120: e = dl_launch<16, 1, 2, false>(a, p->dl_grid, smem, pdl, s); break;
-    case 16121: e = dl_launch<16, 1, 2, true>(a, p->dl_grid, smem, pdl, s); break;
-    case 16110: e = dl_launch<16, 1, 1, false>(a, p->dl_grid, smem, pdl, s); break;
-    case 16111: e = dl_launch<16, 1, 1, true>(a, p->dl_grid, smem, pdl, s); break;
-    case 16210: e = dl_launch<16, 2, 1, false>(a, p->dl_grid, smem, pdl, s); break;
-    case 16211: e = dl_launch<16, 2, 1, true>(a, p->dl_grid, smem, pdl, s); break;
-    case 16220: e = dl_launch<16, 2, 2, false>(a, p->dl_grid, smem, pdl, s); break;
-    case 16221: e = dl_launch<16, 2, 2, true>(a, p->dl_grid, smem, pdl, s); break;
-    case 8120: e = dl_launch<8, 1, 2, false>(a, p->dl_grid, smem, pdl, s); break;
-    case 8121: e = dl_launch<8, 1, 2, true>(a, p->dl_grid, smem, pdl, s); break;
-    case 8110: e = dl_launch<8, 1, 1, false>(a, p->dl_grid, smem, pdl, s); break;
-    case 8111: e = dl_launch<8, 1, 1, true>(a, p->dl_grid, smem, pdl, s); break;
-    case 8210: e = dl_launch<8, 2, 1, false>(a, p->dl_grid, smem, pdl, s); break;
-    case 8211: e = dl_launch<8, 2, 1, true>(a, p->dl_grid, smem, pdl, s); break;
-    case 8220: e = dl_launch<8, 2, 2, false>(a, p->dl_grid, smem, pdl, s); break;
-    case 8221: e = dl_launch<8, 2, 2, true>(a, p->dl_grid, smem, pdl, s); break;
+    case 16120: e = dl_launch<16, 1, 2, false>(a, p->dl_grid, smem, dl_pdl_env(), s); break;
+    case 16121: e = dl_launch<16, 1, 2, true>(a, p->dl_grid, smem, dl_pdl_env(), s); break;
+    case 16110: e = dl_launch<16, 1, 1, false>(a, p->dl_grid, smem, dl_pdl_env(), s); break;
+    case 16111: e = dl_launch<16, 1, 1, true>(a, p->dl_grid, smem, dl_pdl_env(), s); break;
+    case 16210: e = dl_launch<16, 2, 1, false>(a, p->dl_grid, smem, dl_pdl_env(), s); break;
+    case 16211: e = dl_launch<16, 2, 1, true>(a, p->dl_grid, smem, dl_pdl_env(), s); break;
+    case 16220: e = dl_launch<16, 2, 2, false>(a, p->dl_grid, smem, dl_pdl_env(), s); break;
+    case 16221: e = dl_launch<16, 2, 2, true>(a, p->dl_grid, smem, dl_pdl_env(), s); break;
+    case 8120: e = dl_launch<8, 1, 2, false>(a, p->dl_grid, smem, dl_pdl_env(), s); break;
+    case 8121: e = dl_launch<8, 1, 2, true>(a, p->dl_grid, smem, dl_pdl_env(), s); break;
+    case 8110: e = dl_launch<8, 1, 1, false>(a, p->dl_grid, smem, dl_pdl_env(), s); break;
+    case 8111: e = dl_launch<8, 1, 1, true>(a, p->dl_grid, smem, dl_pdl_env(), s); break;
+    case 8210: e = dl_launch<8, 2, 1, false>(a, p->dl_grid, smem, dl_pdl_env(), s); break;
+    case 8211: e = dl_launch<8, 2, 1, true>(a, p->dl_grid, smem, dl_pdl_env(), s); break;
+    case 8220: e = dl_launch<8, 2, 2, false>(a, p->dl_grid, smem, dl_pdl_env(), s); break;
+    case 8221: e = dl_launch<8, 2, 2, true>(a, p->dl_grid, smem, dl_pdl_env(), s); break;
     default: return fail(INVOP_E_VALUE, "k2_dl: unsupported consumer layout");
   }
   if (e != cudaSuccess) return cuda_fail(e, "k2_dl launch");
