@@ -250,7 +250,6 @@ struct DlArgs {
   const void* x;                // fp32, or fp64 when F64IO (rounded to fp32 on load)
   void* y;                      // fp32, or fp64 when F64IO (the fp32 result widened)
   int ring_bytes;               // variable-size unit ring (FIFO) in shared memory
-  int x_dep;                    // x is written by the preceding grid (host entry)
 };
 
 #ifndef DL_NS_OVERRIDE
@@ -428,8 +427,9 @@ __global__ void __launch_bounds__((CONS + 1) * 32, 1) k2_dl(DlArgs a) {
   const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(bars);
   // the next apply in the stream (launched as a programmatic dependent) may
   // take SMs as soon as this grid's CTAs retire: its producers start
-  // streaming while this grid's slowest CTAs finish; it waits for this grid
-  // before writing y (griddepcontrol.wait below)
+  // streaming the operator while this grid's slowest CTAs finish; its
+  // consumers wait for this grid before reading x (which may be this grid's
+  // y) and before writing y
   if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row_lo = a.rowlo[blockIdx.x];
@@ -493,7 +493,9 @@ __global__ void __launch_bounds__((CONS + 1) * 32, 1) k2_dl(DlArgs a) {
       // x may come from the preceding grid (programmatic dependent launch of
       // the host entry: that grid pulls x over PCIe while the producer
       // already streams the operator); a no-op for ordinary launches
-      if (slab == 0 && a.x_dep) asm volatile("griddepcontrol.wait;" ::: "memory");
+      // x may be the preceding grid's output (chained applies): wait for
+      // that grid before reading it (the producer has been streaming)
+      if (slab == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
       // x piece of this warp -> 23-bit fixed point (warp-wide exponent):
       // one pass for max|x| and finiteness, one for the digits (SW > 2; the
       // values stay in registers for SW <= 2)
@@ -790,7 +792,6 @@ int apply_dl_launch(invop_plan* p, const void* x, void* y, bool f64io, cudaStrea
   a.nslabs = p->dl_nslabs;
   a.scale = p->scale;
   a.x = x; a.y = y;
-  a.x_dep = pdl ? 1 : 0;
   int cons = dl_consumers();
   if (cons % p->dl_groups) cons = 16;
   const size_t side = dl_side_bytes(p, cons);

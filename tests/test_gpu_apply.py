@@ -654,3 +654,29 @@ def test_k3_row_residuals(invop, O, rows, N, k, splits, monkeypatch):
     assert relerr(Y2[1][fin], Yo2[fin]) <= F32_TOL
     yo0 = O.ordered_apply(mant, 4, Xr[0])
     assert relerr(Y2[0], yo0) <= F32_TOL
+
+
+def test_dl_chained_applies_are_stream_ordered(invop):
+    """Consecutive applies overlap (programmatic dependent launch); an apply
+    whose x is the previous apply's y must still see the finished y: a chain
+    of applies without synchronisation equals the synchronised chain."""
+    import torch
+
+    rows = N = 9000
+    rng = np.random.default_rng(11)
+    mant = np.abs(_smooth_rows(rng, rows, N, 3_000_000, False))
+    dplan = invop._plan.DevicePlan.from_mantissas(mant, 6, row0=0, n=N)
+    assert dplan.code_bytes == 3
+    x0 = torch.tensor(rng.standard_normal(N), device="cuda", dtype=torch.float32)
+    y = x0
+    for _ in range(4):                        # y_{i+1} = L^-1 y_i, kernel after kernel
+        y = dplan.apply_device(y, mode=0)
+    free_run = y.cpu().numpy()
+    assert dplan.apply_kernel(1) == "k2_dl"
+    assert np.isfinite(free_run).all()
+    z = x0
+    for _ in range(4):
+        torch.cuda.synchronize()
+        z = dplan.apply_device(z, mode=0)
+        torch.cuda.synchronize()
+    assert free_run.tobytes() == z.cpu().numpy().tobytes()
