@@ -398,7 +398,9 @@ def run_ours(args, world, rank, local):
     int8_ops = 2.0 * rows * N * k * (code_bytes * 3) if k > 1 else None
     traffic = None
     prof = ROOT / "profiles" / ("ncu_cfg%d_%s.json" % (cfg.key, kname))
-    if prof.exists():
+    # the committed capture is of the whole operator on one GPU: it describes
+    # a launch only when this rank holds all rows
+    if prof.exists() and world == 1 and (not args.nrhs or args.nrhs == cfg.nrhs):
         try:
             traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
         except Exception:  # noqa: BLE001
