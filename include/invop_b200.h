@@ -158,6 +158,19 @@ int invop_plan_apply_bytes(invop_plan* plan, int64_t nrhs, int mode, int64_t* by
    benchmark labels; static string, "" for a NULL plan. */
 const char* invop_apply_kernel(const invop_plan* plan, int64_t nrhs, int mode);
 
+/* Row-sharded multi-GPU apply (new — the reference is one
+   process). Each rank holds the plan of its rows [row_offsets[rank],
+   row_offsets[rank+1]) of the operator; x: device [nrhs x n] (ldx), the full
+   right-hand sides on every rank; y: device [nrhs x n] (ldy >= n) receives
+   this rank's rows and, through one NCCL group of in-place broadcasts over
+   `nccl_comm` (an ncclComm_t of the ranks, in rank order), every other
+   rank's rows. row_offsets: host int64 [nranks + 1]. Stream-ordered on
+   `stream`; NCCL is resolved from the process at run time
+   (INVOP_E_UNSUPPORTED when it is not loaded). */
+int invop_apply_sharded(const invop_plan* shard, void* nccl_comm, const int64_t* row_offsets,
+                        const void* x, int64_t ldx, void* y, int64_t ldy, int64_t nrhs,
+                        int dtype, int mode, void* stream);
+
 /* A8 — naive quantized apply of the reference (applyplan.py:194-209):
    identical arithmetic to ORDERED mode; provided under its own name. */
 int invop_apply_naive(const invop_plan* plan, const double* x, double* y, int64_t nrhs,

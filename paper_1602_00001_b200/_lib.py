@@ -59,6 +59,7 @@ SIGNATURES = {
     "invop_plan_csc": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _pi64, _pi64, _vp],
     "invop_apply": [_vp, _vp, _i64, _vp, _i64, _i64, _int, _int, _vp],
     "invop_apply_host": [_vp, _vp, _vp, _i64, _int, _vp],
+    "invop_apply_sharded": [_vp, _vp, _vp, _vp, _i64, _vp, _i64, _i64, _int, _int, _vp],
     "invop_apply_naive": [_vp, _vp, _vp, _i64, _vp],
     "invop_plan_apply_bytes": [_vp, _i64, _int, _pi64, _vp],
     "invop_apply_kernel": [_vp, _i64, _int],

@@ -10,6 +10,11 @@ rows), so nothing of the operator crosses NVLink. An apply is
 rho is either replicated by construction (same seed on every rank) or
 broadcast once from rank 0. Uneven N is handled by padding the gathered
 buffer to G * ceil(N/G) rows.
+
+The same exchange is available below the Python layer for a C/C++ caller
+that owns an ncclComm_t: `invop_apply_sharded` (include/invop_b200.h)
+applies the local rows in place into the full y and exchanges the slices
+with one NCCL group of in-place broadcasts (uneven shards, no padding).
 """
 
 from __future__ import annotations

@@ -680,3 +680,42 @@ def test_dl_chained_applies_are_stream_ordered(invop):
         z = dplan.apply_device(z, mode=0)
         torch.cuda.synchronize()
     assert free_run.tobytes() == z.cpu().numpy().tobytes()
+
+
+def test_apply_sharded_c_abi_one_rank(invop):
+    """invop_apply_sharded through a one-rank NCCL communicator (the box has
+    one GPU): the local rows land in place and the (self-)broadcast leaves
+    them intact, so y equals the single-plan apply bit for bit. Wrong offsets
+    are rejected."""
+    import ctypes as C
+    import torch
+    from paper_1602_00001_b200 import _lib as L
+    from paper_1602_00001_b200 import _device as dev
+
+    try:
+        nccl = C.CDLL("libnccl.so.2")
+    except OSError:
+        pytest.skip("libnccl.so.2 not loadable")
+    rng = np.random.default_rng(5)
+    rows = n = 3000
+    mant = np.abs(_smooth_rows(rng, rows, n, 20000, False))
+    dplan = invop._plan.DevicePlan.from_mantissas(mant, 4, row0=0, n=n)
+    comm = C.c_void_p()
+    devs = (C.c_int * 1)(torch.cuda.current_device())
+    assert nccl.ncclCommInitAll(C.byref(comm), 1, devs) == 0
+    try:
+        for k in (1, 3):
+            X = torch.tensor(rng.standard_normal((k, n)), device="cuda", dtype=torch.float32)
+            ref = dplan.apply_device(X, mode=0).clone()
+            Y = torch.full((k, n), float("nan"), device="cuda")
+            offs = (C.c_int64 * 2)(0, n)
+            L.check(L.lib.invop_apply_sharded(dplan.handle, comm, offs, X.data_ptr(), n,
+                                              Y.data_ptr(), n, k, L.F32, L.MODE_FAST,
+                                              C.c_void_p(dev.stream_ptr())), "apply_sharded")
+            torch.cuda.synchronize()
+            assert Y.cpu().numpy().tobytes() == ref.reshape(k, n).cpu().numpy().tobytes()
+        bad = (C.c_int64 * 2)(0, n - 1)
+        assert L.lib.invop_apply_sharded(dplan.handle, comm, bad, X.data_ptr(), n, Y.data_ptr(), n, 1,
+                                         L.F32, L.MODE_FAST, C.c_void_p(dev.stream_ptr())) != 0
+    finally:
+        nccl.ncclCommDestroy(comm)
