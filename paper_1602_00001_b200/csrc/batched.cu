@@ -708,18 +708,20 @@ __global__ void __launch_bounds__(K3D_SEG) k3d_seg_sums(const long long* __restr
   }
 }
 
-// one thread per RHS: segment carries in place, (sum D, sum z) -> (Z_in, Y_in)
-__global__ void k3d_seg_carry(long long* __restrict__ seg, int nseg, int nrhs) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nrhs) return;
-  long long Z = 0, Y = 0;
-  for (int k = 0; k < nseg; ++k) {
-    long long* p = seg + ((int64_t)t * nseg + k) * 2;
-    const long long sd = p[0], sz = p[1];
-    p[0] = Z;
-    p[1] = Y;
-    Y += (long long)K3D_SEG * Z + sz;   // y at segment end
-    Z += sd;
+// segment carries in place, (sum D, sum z) -> (Z_in, Y_in): one block per RHS,
+// one thread per segment (nseg <= K3D_SEG), two block scans:
+//   Z_in(k) = sum_{j<k} sumD_j,  Y_in(k) = sum_{j<k} (K3D_SEG Z_in(j) + sumz_j)
+__global__ void __launch_bounds__(K3D_SEG) k3d_seg_carry(long long* __restrict__ seg, int nseg) {
+  __shared__ long long sh[32];
+  const int t = blockIdx.x, k = threadIdx.x;
+  long long* p = seg + ((int64_t)t * nseg + k) * 2;
+  const long long sd = k < nseg ? p[0] : 0, sz = k < nseg ? p[1] : 0;
+  const long long zin = k3d_block_incl(sd, sh) - sd;
+  const long long term = (long long)K3D_SEG * zin + sz;
+  const long long yin = k3d_block_incl(term, sh) - term;
+  if (k < nseg) {
+    p[0] = zin;
+    p[1] = yin;
   }
 }
 
@@ -976,7 +978,8 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
       long long* seg = yacc + (size_t)K3_NR * p->rows;
       dim3 gs((unsigned)nseg, (unsigned)nr);
       k3d_seg_sums<<<gs, K3D_SEG, 0, s>>>(yacc, p->rows, seg);
-      k3d_seg_carry<<<1, 64, 0, s>>>(seg, nseg, nr);
+      if (nseg > K3D_SEG) return fail(INVOP_E_UNSUPPORTED, "k3 DL: more than 1024 row segments");
+      k3d_seg_carry<<<nr, (unsigned)round_up(nseg, 32), 0, s>>>(seg, nseg);
       k3d_seg_apply<<<gs, K3D_SEG, 0, s>>>(yacc, p->rows, seg, e, p->scale, y + t0 * ldy, ldy);
       INVOP_LAUNCHED(4);
     } else if (splits > 1) {
