@@ -693,18 +693,42 @@ __device__ __forceinline__ long long k3d_block_incl(long long v, long long* sh) 
   return r;
 }
 
-// grid = (segments, RHS), 1024 threads: one row per thread
-__global__ void __launch_bounds__(K3D_SEG) k3d_seg_sums(const long long* __restrict__ yacc,
+// grid = (segments, RHS), K3D_TPB threads x K3D_RPT consecutive rows each:
+// thread-local prefixes, then one block scan per prefix level
+constexpr int K3D_RPT = 4;
+constexpr int K3D_TPB = K3D_SEG / K3D_RPT;
+
+// d[] -> z[] (inclusive prefix over the segment) and yl[] (prefix of z)
+__device__ __forceinline__ void k3d_seg_prefix(const long long* d, long long* z, long long* yl,
+                                               long long* sh) {
+  long long c[K3D_RPT];
+  c[0] = d[0];
+#pragma unroll
+  for (int i = 1; i < K3D_RPT; ++i) c[i] = c[i - 1] + d[i];
+  const long long ze = k3d_block_incl(c[K3D_RPT - 1], sh) - c[K3D_RPT - 1];
+#pragma unroll
+  for (int i = 0; i < K3D_RPT; ++i) z[i] = ze + c[i];
+  long long w[K3D_RPT];
+  w[0] = z[0];
+#pragma unroll
+  for (int i = 1; i < K3D_RPT; ++i) w[i] = w[i - 1] + z[i];
+  const long long we = k3d_block_incl(w[K3D_RPT - 1], sh) - w[K3D_RPT - 1];
+#pragma unroll
+  for (int i = 0; i < K3D_RPT; ++i) yl[i] = we + w[i];
+}
+
+__global__ void __launch_bounds__(K3D_TPB) k3d_seg_sums(const long long* __restrict__ yacc,
                                                         int64_t rows, long long* __restrict__ seg) {
   __shared__ long long sh[32];
   const int t = blockIdx.y;
-  const int64_t r = (int64_t)blockIdx.x * K3D_SEG + threadIdx.x;
-  const long long d = r < rows ? yacc[(int64_t)t * rows + r] : 0;
-  const long long z = k3d_block_incl(d, sh);          // local first prefix
-  const long long zs = k3d_block_incl(z, sh);         // its prefix: local y
-  if (threadIdx.x == K3D_SEG - 1) {
-    seg[((int64_t)t * gridDim.x + blockIdx.x) * 2 + 0] = z;    // sum of D
-    seg[((int64_t)t * gridDim.x + blockIdx.x) * 2 + 1] = zs;   // sum of z_local
+  const int64_t r0 = (int64_t)blockIdx.x * K3D_SEG + threadIdx.x * K3D_RPT;
+  long long d[K3D_RPT], z[K3D_RPT], yl[K3D_RPT];
+#pragma unroll
+  for (int i = 0; i < K3D_RPT; ++i) d[i] = r0 + i < rows ? yacc[(int64_t)t * rows + r0 + i] : 0;
+  k3d_seg_prefix(d, z, yl, sh);
+  if (threadIdx.x == K3D_TPB - 1) {
+    seg[((int64_t)t * gridDim.x + blockIdx.x) * 2 + 0] = z[K3D_RPT - 1];    // sum of D
+    seg[((int64_t)t * gridDim.x + blockIdx.x) * 2 + 1] = yl[K3D_RPT - 1];   // sum of z_local
   }
 }
 
@@ -725,19 +749,25 @@ __global__ void __launch_bounds__(K3D_SEG) k3d_seg_carry(long long* __restrict__
   }
 }
 
-__global__ void __launch_bounds__(K3D_SEG) k3d_seg_apply(const long long* __restrict__ yacc,
+__global__ void __launch_bounds__(K3D_TPB) k3d_seg_apply(const long long* __restrict__ yacc,
                                                          int64_t rows, const long long* __restrict__ seg,
                                                          const int* __restrict__ e, double scale,
                                                          float* __restrict__ y, int64_t ldy) {
   __shared__ long long sh[32];
   const int t = blockIdx.y;
-  const int64_t r = (int64_t)blockIdx.x * K3D_SEG + threadIdx.x;
-  const long long d = r < rows ? yacc[(int64_t)t * rows + r] : 0;
-  const long long z = k3d_block_incl(d, sh);
-  const long long yl = k3d_block_incl(z, sh);
+  const int64_t r0 = (int64_t)blockIdx.x * K3D_SEG + threadIdx.x * K3D_RPT;
+  long long d[K3D_RPT], z[K3D_RPT], yl[K3D_RPT];
+#pragma unroll
+  for (int i = 0; i < K3D_RPT; ++i) d[i] = r0 + i < rows ? yacc[(int64_t)t * rows + r0 + i] : 0;
+  k3d_seg_prefix(d, z, yl, sh);
   const long long* c = seg + ((int64_t)t * gridDim.x + blockIdx.x) * 2;
-  const long long Y = yl + (long long)(threadIdx.x + 1) * c[0] + c[1];
-  if (r < rows) y[(int64_t)t * ldy + r] = (float)((double)Y * ldexp(scale, -e[t]));
+  const long long zin = c[0], yin = c[1];
+  const double sc = ldexp(scale, -e[t]);
+#pragma unroll
+  for (int i = 0; i < K3D_RPT; ++i) {
+    const long long Y = yl[i] + (long long)(threadIdx.x * K3D_RPT + i + 1) * zin + yin;
+    if (r0 + i < rows) y[(int64_t)t * ldy + r0 + i] = (float)((double)Y * sc);
+  }
 }
 
 // ------------------------------------------------------------ host side
@@ -977,10 +1007,10 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
       const int nseg = (int)cdiv(p->rows, K3D_SEG);
       long long* seg = yacc + (size_t)K3_NR * p->rows;
       dim3 gs((unsigned)nseg, (unsigned)nr);
-      k3d_seg_sums<<<gs, K3D_SEG, 0, s>>>(yacc, p->rows, seg);
+      k3d_seg_sums<<<gs, K3D_TPB, 0, s>>>(yacc, p->rows, seg);
       if (nseg > K3D_SEG) return fail(INVOP_E_UNSUPPORTED, "k3 DL: more than 1024 row segments");
       k3d_seg_carry<<<nr, (unsigned)round_up(nseg, 32), 0, s>>>(seg, nseg);
-      k3d_seg_apply<<<gs, K3D_SEG, 0, s>>>(yacc, p->rows, seg, e, p->scale, y + t0 * ldy, ldy);
+      k3d_seg_apply<<<gs, K3D_TPB, 0, s>>>(yacc, p->rows, seg, e, p->scale, y + t0 * ldy, ldy);
       INVOP_LAUNCHED(4);
     } else if (splits > 1) {
       int64_t tot = (int64_t)nr * p->rows;
