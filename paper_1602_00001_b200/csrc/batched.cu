@@ -480,26 +480,43 @@ __device__ __forceinline__ int k3_exponent(unsigned int bits) {
   return (m > 0.0f && isfinite(m)) ? 22 - ex : 0;   // max|x_t| * 2^e_t < 2^22
 }
 
-// balanced base-256 digits of X = rint(x * 2^e), into B[l][t][j] (int8)
+// balanced base-256 digits of X = rint(x * 2^e), into B[l][t][j] (int8);
+// one thread per 16 consecutive columns of one right-hand side (ldb is a
+// multiple of 64): three 16-byte stores
 __global__ void k3_digits(const float* __restrict__ x, int64_t n, int64_t ldx, int nrhs,
                           const unsigned int* __restrict__ maxbits, int* __restrict__ e,
                           int8_t* __restrict__ B, int64_t ldb) {
-  const int64_t total = (int64_t)K3_NR * ldb;
+  const int64_t per = ldb / 16;
+  const int64_t total = (int64_t)K3_NR * per;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
        k += (int64_t)gridDim.x * blockDim.x) {
-    const int t = (int)(k / ldb);
-    const int64_t j = k - (int64_t)t * ldb;
-    int X = 0;
+    const int t = (int)(k / per);
+    const int64_t j0 = (k - (int64_t)t * per) * 16;
     const int et = t < nrhs ? k3_exponent(maxbits[t]) : 0;
-    if (j == 0) e[t] = et;
-    if (t < nrhs && j < n) X = __float2int_rn(ldexpf(x[t * ldx + j], et));
-    const int d0 = ((X + 128) & 255) - 128;
-    const int X1 = (X - d0) >> 8;
-    const int d1 = ((X1 + 128) & 255) - 128;
-    const int d2 = (X1 - d1) >> 8;
-    B[(0 * K3_NR + t) * ldb + j] = (int8_t)d0;
-    B[(1 * K3_NR + t) * ldb + j] = (int8_t)d1;
-    B[(2 * K3_NR + t) * ldb + j] = (int8_t)d2;
+    if (j0 == 0) e[t] = et;
+    uint32_t w[3][4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint32_t b0 = 0, b1 = 0, b2 = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int64_t j = j0 + 4 * q + i;
+        int X = 0;
+        if (t < nrhs && j < n) X = __float2int_rn(ldexpf(x[t * ldx + j], et));
+        const int d0 = ((X + 128) & 255) - 128;
+        const int X1 = (X - d0) >> 8;
+        const int d1 = ((X1 + 128) & 255) - 128;
+        const int d2 = (X1 - d1) >> 8;
+        b0 |= ((uint32_t)d0 & 255u) << (8 * i);
+        b1 |= ((uint32_t)d1 & 255u) << (8 * i);
+        b2 |= ((uint32_t)d2 & 255u) << (8 * i);
+      }
+      w[0][q] = b0; w[1][q] = b1; w[2][q] = b2;
+    }
+#pragma unroll
+    for (int l = 0; l < 3; ++l)
+      *reinterpret_cast<uint4*>(B + (int64_t)(l * K3_NR + t) * ldb + j0) =
+          make_uint4(w[l][0], w[l][1], w[l][2], w[l][3]);
   }
 }
 
@@ -973,7 +990,7 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
   if (rc) return rc;
   for (int64_t t0 = 0; t0 < nrhs; t0 += K3_NR) {
     const int nr = (int)std::min<int64_t>(K3_NR, nrhs - t0);
-    k3_digits<<<(unsigned)std::min<int64_t>(cdiv((int64_t)K3_NR * ldb, 256), sms * 16), 256, 0, s>>>(
+    k3_digits<<<(unsigned)std::min<int64_t>(cdiv((int64_t)K3_NR * ldb / 16, 256), sms * 16), 256, 0, s>>>(
         x + t0 * ldx, p->n, ldx, nr, maxbits + t0, e, B, ldb);
     INVOP_LAUNCHED(2);   // k3_digits + k3_batched
     if (splits > 1) INVOP_CUDA(cudaMemsetAsync(yacc, 0, acc_bytes, s));
