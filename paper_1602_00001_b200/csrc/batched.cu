@@ -470,7 +470,15 @@ __global__ void k3_xmax(const float* __restrict__ x, int64_t n, int64_t ldx,
   }
   for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1);
-  if ((threadIdx.x & 31) == 0) atomicMax(&maxbits[t], __float_as_uint(m));
+  // one atomic per block (per-warp atomics on one address serialise in L2)
+  __shared__ float wm[32];
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? wm[threadIdx.x] : 0.0f;
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (threadIdx.x == 0) atomicMax(&maxbits[t], __float_as_uint(v));
+  }
 }
 
 __device__ __forceinline__ int k3_exponent(unsigned int bits) {
