@@ -138,7 +138,7 @@ extern "C" const char* invop_apply_kernel(const invop_plan* p, int64_t nrhs, int
   if (!p) return "";
   if (mode == INVOP_MODE_ORDERED) return "k2_ordered";
   switch (fast_route(p, nrhs)) {
-    case ROUTE_K3: return p->k3d_ready > 0 ? "k3_batched_dl" : "k3_batched";
+    case ROUTE_K3: return k3d_bytes(p) > 0 ? "k3_batched_dl" : "k3_batched";
     case ROUTE_DL: return "k2_dl";
     case ROUTE_HL: return "k2_hl";
     case ROUTE_TVW: return "k2_tvw";

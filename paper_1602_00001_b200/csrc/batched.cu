@@ -909,7 +909,7 @@ static int k3d_build(invop_plan* p, cudaStream_t s) {
 }
 
 int64_t k3d_bytes(const invop_plan* p) {
-  if (p->k3d_ready <= 0) return -1;
+  if (p->k3d_ready <= 0 || cdiv(p->rows, K3D_SEG) > K3D_SEG) return -1;   // DL kernel not used
   const int64_t tiles = round_up(cdiv(p->rows, K3_BM), 2) * (p->ld / K3_BK);
   return (tiles + p->k3d_n1) * K3_A_TILE + tiles * 4;
 }
@@ -945,7 +945,9 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
   size_t acc_off = round_up(max_off + (size_t)nrhs * 4, 256);
   int krc = k3d_build(p, s);
   if (krc != INVOP_OK && krc != INVOP_E_UNSUPPORTED) return krc;
-  const bool dl = p->k3d_ready > 0 && tiles == 2 && stages == 4;   // default config -> DL kernel
+  // default config -> DL kernel (its row prefix sum handles <= 1024 segments)
+  const bool dl = p->k3d_ready > 0 && tiles == 2 && stages == 4 &&
+                  cdiv(p->rows, K3D_SEG) <= K3D_SEG;
   size_t acc_bytes = splits > 1 ? (size_t)K3_NR * p->rows * 8 : 0;
   if (dl)   // + segment carries of the row prefix sums
     acc_bytes = (size_t)K3_NR * p->rows * 8 + (size_t)K3_NR * cdiv(p->rows, K3D_SEG) * 16;
@@ -1033,7 +1035,6 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
       long long* seg = yacc + (size_t)K3_NR * p->rows;
       dim3 gs((unsigned)nseg, (unsigned)nr);
       k3d_seg_sums<<<gs, K3D_TPB, 0, s>>>(yacc, p->rows, seg);
-      if (nseg > K3D_SEG) return fail(INVOP_E_UNSUPPORTED, "k3 DL: more than 1024 row segments");
       k3d_seg_carry<<<nr, (unsigned)round_up(nseg, 32), 0, s>>>(seg, nseg);
       k3d_seg_apply<<<gs, K3D_TPB, 0, s>>>(yacc, p->rows, seg, e, p->scale, y + t0 * ldy, ldy);
       INVOP_LAUNCHED(4);
