@@ -5,16 +5,23 @@ BASELINE.json metric: "inverse-operator applies/sec and achieved HBM GB/s
 128x128 grid, N=16384, 5 decimal digits, single fp32 right-hand side).
 
 A step is one apply y = L_eps^-1 rho of the quantized operator resident in
-HBM (one K2 launch; plus the NCCL all-gather of the row shards for N>1).
-Inputs are larger than L2 (the 3-byte codes of config 4 are 805 MB), so no
-L2 flush is needed between steps.
+HBM (one K2 launch; for N>1 plus the NCCL all-gather of the row shards and
+the unshard kernel). The operator streamed per apply (424 MB at config 4) is
+larger than 2x L2, so no L2 flush is needed between steps; shards that would
+fit are flushed (config["l2"]).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4]
     python bench.py --impl reference ...   # the reference's CPU kernel
 
 Under torchrun each rank owns a contiguous row block of L^-1 (built on its
 own GPU by the block-LU constructor), applies it to rho, and the row blocks
-are all-gathered. Rank 0 prints one JSON line.
+are all-gathered: the operator is fixed, so the scaling is strong and the
+line reports whole-job applies/s. Rank 0 prints one JSON line.
+
+--impl reference times the reference's own compiled plan_apply (oracle/_ref,
+built from /root/reference's _native.pyx) on the host, over the whole
+quantized operator when it fits the run (config 4 at the driver's step
+counts), else on a column sample scaled by N/cols.
 """
 
 from __future__ import annotations
@@ -125,22 +132,75 @@ def dist_init(args):
     return world, rank, local
 
 
-# ------------------------------------------------------------------ cpu baseline
-def reference_sample(cfg, max_seconds: float, target_step_s: float = 0.25, seed_cols: int = 7):
-    """Bounded sample of the workload for the reference CPU kernel: a set of
-    C columns of the quantized L^-1 (from a host sparse LU, quantized with the
-    reference's rounding), its plan tables (reference build_plan restated),
-    and the reference's own compiled plan_apply (oracle/_ref) — or the
-    oracle's C port of it when oracle/_ref was not built."""
+# ------------------------------------------------------------------ workload
+def workload_config(cfg, world: int, k: int) -> dict:
+    """The `config` object of the JSON line: a function of the workload and
+    N only, so both arms (ours, --impl reference) print the same one."""
+    from paper_1602_00001_b200.sharded import shard_rows
+
+    N = cfg.N
+    rows = shard_rows(N, world, 0)[1]          # the largest shard
+    # every device layout stores >= 1 byte per entry: a shard below 2x L2
+    # could be served from L2 in a back-to-back loop, so those runs flush
+    flush = rows * N < 2 * L2_BYTES
+    return {
+        "workload": cfg.name, "N": N, "digits": cfg.digits, "nrhs": k,
+        "rows_per_gpu": rows,
+        "parallelism": "row-shard x%d + one all-gather" % world if world > 1 else "single GPU",
+        "l2": ("operator shard < 2x L2: 256 MB written between timed steps (per-step events)"
+               if flush else "operator shard larger than 2x L2 (126 MB); no flush"),
+    }
+
+
+def _rhs(cfg, nrhs: int) -> np.ndarray:
+    X = cfg.rhs()
+    if nrhs:
+        reps = -(-nrhs // X.shape[0])
+        X = np.ascontiguousarray(np.tile(X, (reps, 1))[:nrhs])
+    return X
+
+
+def _mem_available() -> int:
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
+
+
+# ------------------------------------------------------------------ reference (CPU)
+def reference_full(cfg):
+    """The whole quantized operator of `cfg` as the reference builds it —
+    dense L^-1 by LU + solve on the identity (dense.py:36-62), quantize
+    (quant.py:48-65), build_plan's CSC tables (applyplan.py:116-172, restated
+    in C with threads: the numpy lexsort takes minutes at N=16384) — and the
+    reference's own compiled plan_apply (oracle/_ref)."""
+    from oracle import invop_oracle as O
+
+    st = cfg.operator()
+    t0 = time.perf_counter()
+    inv = O.invert_dense(st.to_sparse().toarray())
+    t1 = time.perf_counter()
+    mant = O.quantize(inv, cfg.digits)
+    del inv
+    t2 = time.perf_counter()
+    plan = O.build_plan_large(mant, cfg.digits)
+    del mant
+    t3 = time.perf_counter()
+    return plan, {"invert": t1 - t0, "quantize": t2 - t1, "build_plan": t3 - t2}
+
+
+def reference_sample(cfg, target_step_s: float = 0.25, seed_cols: int = 7):
+    """Bounded sample of the workload for the reference CPU kernel: C columns
+    of the quantized L^-1 (host sparse LU, reference rounding, reference
+    grouping restated), all rows; a step's time is scaled by N/C."""
     from oracle import invop_oracle as O
     import scipy.sparse.linalg as spla
 
     st = cfg.operator()
     N = st.n
-    ref = O.reference_native()
-    kind = "reference" if ref is not None else "port"
-    # pick the column count so that one sampled apply takes ~target_step_s
-    cols = 256
     rng = np.random.default_rng(seed_cols)
     lu = spla.splu(st.to_sparse().tocsc())
 
@@ -148,11 +208,10 @@ def reference_sample(cfg, max_seconds: float, target_step_s: float = 0.25, seed_
         J = np.sort(rng.choice(N, size=cols, replace=False))
         E = np.zeros((N, cols))
         E[J, np.arange(cols)] = 1.0
-        Z = lu.solve(E)                        # columns J of L^-1
-        mant = O.quantize(Z, cfg.digits)       # N x cols
-        plan = O.build_plan_rect(mant, cfg.digits)
-        return J, plan
+        mant = O.quantize(lu.solve(E), cfg.digits)       # columns J of L^-1
+        return J, O.build_plan_rect(mant, cfg.digits)
 
+    ref = O.reference_native()
     x_full = cfg.rhs()[0]
 
     def run(J, plan):
@@ -165,84 +224,149 @@ def reference_sample(cfg, max_seconds: float, target_step_s: float = 0.25, seed_
             O.plan_apply(plan, x_full[J])
         return time.perf_counter() - t0
 
+    cols = 256
     J, plan = make(cols)
-    t = run(J, plan)
-    scale = max(0.05, min(16.0, target_step_s / max(t, 1e-6)))
+    scale = max(0.05, min(16.0, target_step_s / max(run(J, plan), 1e-6)))
     cols = int(min(N, max(16, cols * scale)))
     J, plan = make(cols)
-    return dict(J=J, plan=plan, run=run, cols=cols, N=N, kind=kind)
+    return dict(J=J, plan=plan, run=run, cols=cols, N=N,
+                kind="reference" if ref is not None else "port")
 
 
 def cpu_baseline(cfg, budget_s: float = 15.0):
-    s = reference_sample(cfg, budget_s)
+    """`cpu_baseline` of our line: ~budget_s of reference plan_apply on a
+    column sample of the workload (single-threaded: the reference holds the GIL)."""
+    s = reference_sample(cfg)
     times = []
     t_end = time.perf_counter() + budget_s
     while time.perf_counter() < t_end or len(times) < 3:
         times.append(s["run"](s["J"], s["plan"]))
         if len(times) >= 50:
             break
-    best = min(times)
-    per_apply = best * s["N"] / s["cols"]
+    per_apply = min(times) * s["N"] / s["cols"]
     return {
         "value": 1.0 / per_apply,
         "unit": UNIT,
         "cores": 1,
         "kind": s["kind"],
         "sample": "%d of %d columns of the quantized L^-1 (all %d rows), reference plan_apply "
-                  "best of %d runs, scaled by N/cols; single-threaded (the reference holds the GIL)"
-                  % (s["cols"], s["N"], s["N"], len(times)),
+                  "best of %d runs, scaled by N/cols (extrapolated); single-threaded (the "
+                  "reference holds the GIL)" % (s["cols"], s["N"], s["N"], len(times)),
         "host_cpus": os.cpu_count(),
         "affinity_cpus": len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else None,
     }
 
 
-# ------------------------------------------------------------------ reference arm
 def run_reference(args, world, rank):
+    """--impl reference: the reference's own compiled plan_apply
+    (_native.pyx:15-49, built from its source into oracle/_ref) on the host
+    cores, through its own table format, on our arm's workload. Never loads
+    libinvop_b200.so (the package's library is dlopen'ed lazily)."""
     from paper_1602_00001_b200 import configs
+    from oracle import invop_oracle as O
 
     if rank != 0:
         return
     cfg = configs.get(args.config)
-    # size each step so the whole --steps/--warmup run stays around a minute
-    target = max(0.005, min(0.2, 60.0 / max(1, args.steps + args.warmup)))
-    s = reference_sample(cfg, 0.0, target_step_s=target)
-    for _ in range(args.warmup):
-        s["run"](s["J"], s["plan"])
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        s["run"](s["J"], s["plan"])
-    el = time.perf_counter() - t0
-    per_apply = el / args.steps * s["N"] / s["cols"]
-    value = 1.0 / per_apply
+    X = _rhs(cfg, args.nrhs)
+    k, N = X.shape
+    ref = O.reference_native()
+    kind = "reference" if ref is not None else "port"
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_apply * 1e3,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "impl": "reference", "metric": METRIC, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded; BASELINE.json config %d)" % cfg.key,
-        "config": {"workload": cfg.name, "N": cfg.N, "digits": cfg.digits, "nrhs": 1},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": s["kind"],
-                         "sample": "%d of %d columns per step, scaled by N/cols" % (s["cols"], s["N"])},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "config": workload_config(cfg, world, k),
     }
+    # whole-operator timing when it fits the host and the run stays short:
+    # one step = k full applies (~2.5 ns per entry on one core)
+    est_step = k * N * N * 2.5e-9
+    need = 48 * N * N                          # dense fp64 inverse + LU + tables
+    full = (ref is not None and N * N <= 2 ** 29 and _mem_available() > need
+            and (args.steps + args.warmup) * est_step <= 240.0)
+    if full:
+        plan, setup = reference_full(cfg)
+        args_t = (plan["col_ptr"], plan["group_coeff"], plan["group_ptr"], plan["entry_rows"],
+                  plan["entry_signs"])
+
+        def step():
+            for t in range(k):
+                ref.plan_apply(*args_t, X[t], np.zeros(N))
+
+        for _ in range(args.warmup):
+            step()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            step()
+        el = time.perf_counter() - t0
+        value = k * args.steps / el
+        sample = ("whole operator: the reference's plan_apply over all %d x %d entries (%d groups, "
+                  "%d entries) per RHS, every step" % (N, N, plan["group_ptr"].size - 1,
+                                                       plan["entry_rows"].size))
+        line["setup_s"] = setup
+    else:
+        target = max(0.005, min(0.2, 60.0 / max(1, args.steps + args.warmup)))
+        s = reference_sample(cfg, target_step_s=target)
+        for _ in range(args.warmup):
+            s["run"](s["J"], s["plan"])
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            s["run"](s["J"], s["plan"])
+        el = time.perf_counter() - t0
+        value = 1.0 / (el / args.steps * s["N"] / s["cols"])
+        sample = ("%d of %d columns per step, scaled by N/cols (extrapolated: the whole operator "
+                  "does not fit this run's time or memory budget)" % (s["cols"], s["N"]))
+    line.update({
+        "value": value, "ms_per_step": k * 1e3 / value,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": kind, "sample": sample,
+                         "host_cpus": os.cpu_count()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    })
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------------ our arm
+def _int8_peak():
+    p = ROOT / "profiles" / "int8_tc_peak.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["tops"]), "measured (%s)" % p.relative_to(ROOT)
+    return None, "unmeasured"
+
+
+def quantization_error(cfg, X32: np.ndarray, Y: np.ndarray) -> float:
+    """the apply against a direct sparse solve of the
+    unquantized operator, y_exact = splu(A).solve(x) on the same fp32-rounded
+    x; Eq. 6 normalisation (reference bench.py:73-85), worst RHS."""
+    import scipy.sparse.linalg as spla
+
+    A = cfg.operator().to_sparse().tocsc()
+    lu = spla.splu(A)
+    Xd = X32.astype(np.float64)
+    exact = lu.solve(np.ascontiguousarray(Xd.T)).T          # [k, N]
+    num = np.abs(Y - exact).max(axis=1)
+    den = np.abs(exact).max(axis=1)
+    return float((num / den).max())
+
+
 def run_ours(args, world, rank, local):
+    import ctypes as C
+
     import torch
 
     import paper_1602_00001_b200 as invop
     from paper_1602_00001_b200 import configs, _lib as L
+    from paper_1602_00001_b200.sharded import row_offsets, shard_rows
 
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     cfg = configs.get(args.config)
     st = cfg.operator()
     N = st.n
-    rows = N // world
-    row0 = rank * rows
-    if rank == world - 1:
-        rows = N - row0
+    row0, rows = shard_rows(N, world, rank)
+    pad = shard_rows(N, world, 0)[1]
+    offs = row_offsets(N, world)
     # ---- setup (timed separately): block-LU factor + construct + encode
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -252,40 +376,41 @@ def run_ours(args, world, rank, local):
     plan = dop.quantized_rows(cfg.digits, row0, rows)
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t0
+    del dop
 
-    X = cfg.rhs()
-    if args.nrhs:
-        reps = -(-args.nrhs // X.shape[0])
-        X = np.ascontiguousarray(np.tile(X, (reps, 1))[:args.nrhs])
+    X = _rhs(cfg, args.nrhs)
     k = X.shape[0]
-    x64 = torch.tensor(X, dtype=torch.float64, device=dev)      # [k, N]
-    x32 = x64.float().contiguous()
-    y32 = torch.empty((k, rows), dtype=torch.float32, device=dev)
-    full = torch.empty((world, k, rows), dtype=torch.float32, device=dev) if world > 1 else None
+    x32 = torch.tensor(X, dtype=torch.float32, device=dev)      # [k, N], resident
+    x64 = x32.double()
+    stage = torch.empty((world, k, pad), dtype=torch.float32, device=dev)
+    mine = stage[rank]
+    Y = torch.empty((k, N), dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
-    sptr = stream.cuda_stream
+    sptr = C.c_void_p(stream.cuda_stream)
     h = plan.handle
-    import ctypes as C
 
     def launch_fast():
-        L.lib.invop_apply(h, x32.data_ptr(), N, y32.data_ptr(), rows, k, L.F32, L.MODE_FAST,
-                          C.c_void_p(sptr))
+        L.lib.invop_apply(h, x32.data_ptr(), N, mine.data_ptr(), pad, k, L.F32, L.MODE_FAST, sptr)
 
     def step():
         launch_fast()
         if world > 1:
-            torch.distributed.all_gather_into_tensor(full.view(-1), y32.view(-1))
+            torch.distributed.all_gather_into_tensor(stage.view(-1), mine.reshape(-1))
+            L.lib.invop_unshard(stage.data_ptr(), world, offs.ctypes.data, k, pad, Y.data_ptr(), N,
+                                L.F32, sptr)
 
-    L.check(L.lib.invop_apply(h, x32.data_ptr(), N, y32.data_ptr(), rows, k, L.F32, L.MODE_FAST,
-                              C.c_void_p(sptr)), "apply")
-    # operator bytes one apply streams (the layout the first apply built)
+    L.check(L.lib.invop_apply(h, x32.data_ptr(), N, mine.data_ptr(), pad, k, L.F32, L.MODE_FAST,
+                              sptr), "apply")
     op_bytes = C.c_int64()
-    L.check(L.lib.invop_plan_apply_bytes(h, k, L.MODE_FAST, C.byref(op_bytes), C.c_void_p(sptr)))
+    L.check(L.lib.invop_plan_apply_bytes(h, k, L.MODE_FAST, C.byref(op_bytes), sptr))
     op_bytes = op_bytes.value
-    # an operator shard that fits twice into L2 would be served from L2 in a
-    # back-to-back loop: then every timed step gets its own event pair and a
-    # write of 2x L2 between steps (outside the events)
-    flush_l2 = op_bytes < 2 * L2_BYTES
+    ord_bytes = C.c_int64()
+    L.check(L.lib.invop_plan_apply_bytes(h, k, L.MODE_ORDERED, C.byref(ord_bytes), sptr))
+    ord_bytes = ord_bytes.value
+    tc_ops = C.c_int64()
+    L.check(L.lib.invop_plan_tensor_ops(h, k, L.MODE_FAST, C.byref(tc_ops), sptr))
+    tc_ops = tc_ops.value
+    flush_l2 = rows * N < 2 * L2_BYTES
     flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device=dev) if flush_l2 else None
     for _ in range(max(args.warmup, 3)):
         step()
@@ -293,9 +418,11 @@ def run_ours(args, world, rank, local):
     if world > 1:
         torch.distributed.barrier()
 
-    def timed(fn, reps):
-        """Device milliseconds of `reps` calls of fn (CUDA events on the launching stream)."""
-        if not flush_l2:
+    def timed(fn, reps, sync_each=False):
+        """Device ms of `reps` calls of fn (CUDA events on the launching stream);
+        per-call event pairs (+ L2 flush between calls when needed, or a host
+        synchronisation after each call for the isolated-launch figure)."""
+        if not flush_l2 and not sync_each:
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
@@ -307,10 +434,13 @@ def run_ours(args, world, rank, local):
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(reps)]
         for i in range(reps):
-            flush.fill_(i)
+            if flush_l2:
+                flush.fill_(i)
             evs[i][0].record(stream)
             fn()
             evs[i][1].record(stream)
+            if sync_each:
+                torch.cuda.synchronize()
         torch.cuda.synchronize()
         return sum(a.elapsed_time(b) for a, b in evs)
 
@@ -323,83 +453,83 @@ def run_ours(args, world, rank, local):
         launches = L.lib.invop_launch_count() - lc0
     if world > 1:
         torch.distributed.barrier()
-    if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
     ms_per_step = ms / args.steps
 
-    # ---- kernel-only timing of the apply launch(es) (dominant kernel) for the roofline
+    # ---- the apply alone (dominant kernel(s)): back to back, and isolated
     kreps = max(20, min(args.steps, 2000 if k == 1 else 50))
     k_ms = timed(launch_fast, kreps) / kreps
+    ireps = max(10, min(args.steps, 200 if k == 1 else 20))
+    iso_ms = timed(launch_fast, ireps, sync_each=True) / ireps
 
-    # ---- ordered (bitwise fp64) kernel for reference
+    # ---- ordered (bitwise fp64) kernel
     y64 = torch.empty((k, rows), dtype=torch.float64, device=dev)
-    for _ in range(2):
-        L.lib.invop_apply(h, x64.data_ptr(), N, y64.data_ptr(), rows, k, L.F64, L.MODE_ORDERED,
-                          C.c_void_p(sptr))
-    o0 = torch.cuda.Event(enable_timing=True)
-    o1 = torch.cuda.Event(enable_timing=True)
-    oreps = max(5, min(args.steps, 500 if k == 1 else 5))
-    o0.record(stream)
-    for _ in range(oreps):
-        L.lib.invop_apply(h, x64.data_ptr(), N, y64.data_ptr(), rows, k, L.F64, L.MODE_ORDERED,
-                          C.c_void_p(sptr))
-    o1.record(stream)
-    torch.cuda.synchronize()
-    ord_ms = o0.elapsed_time(o1) / oreps
 
-    # ---- end to end through the C ABI with host buffers (H2D + apply + D2H)
-    xh = torch.from_numpy(np.ascontiguousarray(X)).pin_memory()
-    yh = torch.empty((k, rows), dtype=torch.float64).pin_memory()
+    def launch_ordered():
+        L.lib.invop_apply(h, x64.data_ptr(), N, y64.data_ptr(), rows, k, L.F64, L.MODE_ORDERED, sptr)
+
     for _ in range(2):
-        L.check(L.lib.invop_apply_host(h, xh.data_ptr(), yh.data_ptr(), k, L.MODE_FAST,
-                                       C.c_void_p(sptr)))
+        launch_ordered()
+    oreps = max(5, min(args.steps, 500 if k == 1 else 5))
+    ord_ms = timed(launch_ordered, oreps) / oreps
+
+    # ---- end to end with host buffers
+    if world == 1:
+        xh = torch.from_numpy(np.ascontiguousarray(X)).pin_memory()        # fp64 host
+        yh = torch.empty((k, rows), dtype=torch.float64).pin_memory()
+
+        def e2e_step():
+            L.lib.invop_apply_host(h, xh.data_ptr(), yh.data_ptr(), k, L.MODE_FAST, sptr)
+
+        e2e_h2d, e2e_d2h = k * N * 8, k * rows * 8
+        e2e_path = "invop_apply_host (C ABI, pinned host fp64 x in, fp64 y out)"
+    else:
+        xh = torch.from_numpy(np.ascontiguousarray(X.astype(np.float32))).pin_memory()
+        yh = torch.empty((k, N), dtype=torch.float32).pin_memory()
+
+        def e2e_step():
+            x32.copy_(xh, non_blocking=True)
+            step()
+            yh.copy_(Y, non_blocking=True)
+            stream.synchronize()
+
+        e2e_h2d, e2e_d2h = k * N * 4, k * N * 4
+        e2e_path = "pinned fp32 x -> device, sharded apply + all-gather + unshard, full Y -> pinned host"
+    for _ in range(2):
+        e2e_step()
     e2e_steps = max(10, min(args.steps, 1000 if k == 1 else 30))
     if world > 1:
         torch.distributed.barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        L.lib.invop_apply_host(h, xh.data_ptr(), yh.data_ptr(), k, L.MODE_FAST, C.c_void_p(sptr))
+        e2e_step()
+    torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
     if world > 1:
         t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_s = float(t.item())
 
-    # ---- correctness spot check of this run (fp32 path vs fp64 ordered, same codes)
-    err = float(((y32.double() - y64).abs().max() / y64.abs().max()).item())
-    # ---- quantization error: against the unquantized fp64 rows
-    # of L^-1 (device block LU) applied to the same fp32-rounded x; Eq. 6 norm
-    qerr = 0.0
-    xr = x32.double()
-    for b0 in range(0, rows, 4096):
-        nb = min(4096, rows - b0)
-        exact = dop.inverse_rows(row0 + b0, nb) @ xr.t()          # [nb, k]
-        num = (y32[:, b0:b0 + nb].double().t() - exact).abs().amax(dim=0)
-        if b0 == 0:
-            qnum, qden = num, exact.abs().amax(dim=0)
-        else:
-            qnum = torch.maximum(qnum, num)
-            qden = torch.maximum(qden, exact.abs().amax(dim=0))
-        del exact
+    # ---- result of this run: full Y (gathered), fp32 vs the ordered fp64 path
+    step()
+    torch.cuda.synchronize()
+    y32 = (Y if world > 1 else mine[:, :rows]).double()
+    y32_local = mine[:, :rows].double()
+    err = float(((y32_local - y64).abs().amax(dim=1) / y64.abs().amax(dim=1)).max().item())
+    Yh = y32.cpu().numpy()
     if world > 1:
-        torch.distributed.all_reduce(qnum, op=torch.distributed.ReduceOp.MAX)
-        torch.distributed.all_reduce(qden, op=torch.distributed.ReduceOp.MAX)
-    qerr = float((qnum / qden).max().item())
-    del dop
+        t = torch.tensor([err], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        err = float(t.item())
 
-    # ---- roofline of the dominant kernel (K2 fast, one launch per step)
     peak, peak_src = _peaks()
-    code_bytes = plan.code_bytes
     kname = L.lib.invop_apply_kernel(h, k, L.MODE_FAST).decode()
     alg_bytes = op_bytes + k * N * 4 + k * rows * 4
     achieved = alg_bytes / (k_ms * 1e-3) / 1e9
-    int8_ops = 2.0 * rows * N * k * (code_bytes * 3) if k > 1 else None
     traffic = None
     prof = ROOT / "profiles" / ("ncu_cfg%d_%s.json" % (cfg.key, kname))
-    # the committed capture is of the whole operator on one GPU: it describes
-    # a launch only when this rank holds all rows
     if prof.exists() and world == 1 and (not args.nrhs or args.nrhs == cfg.nrhs):
         try:
             traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
@@ -411,60 +541,54 @@ def run_ours(args, world, rank, local):
         mults, adds = plan.counts() if (world == 1 and N <= 16384) else (None, plan.counts()[1])
         value = k * args.steps / (ms * 1e-3)
         result = {
-            "metric": METRIC,
-            "value": value,
-            "unit": UNIT,
-            "n_gpus": world,
-            "steps": args.steps,
-            "warmup": args.warmup,
-            "ms_per_step": ms_per_step,
-            "higher_is_better": True,
-            "scaling": "strong",
-            "vs_baseline": None,
-            "dtype": "f32",
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded; BASELINE.json config %d; operator pinned in DESIGN.md)" % cfg.key,
-            "config": {
-                "workload": cfg.name, "N": N, "digits": cfg.digits, "nrhs": k,
-                "rows_per_gpu": rows, "code_bytes_per_entry": code_bytes,
+            "config": workload_config(cfg, world, k),
+            "layout": {
+                "kernel": kname, "code_bytes_per_entry": plan.code_bytes,
                 "operator_bytes_per_gpu": op_bytes,
                 "operator_bytes_per_entry": op_bytes / (rows * N),
-                "parallelism": "row-shard x%d + all-gather" % world if world > 1 else "single GPU",
-                "l2": ("operator shard %.0f MB < 2x L2: %d MB written between timed steps "
-                       "(per-step CUDA events)" % (op_bytes / 1e6, 2 * L2_BYTES // 2**20))
-                      if flush_l2 else
-                      "inputs larger than L2 (operator %.0f MB streamed per apply vs 126 MB L2); no flush"
-                      % (op_bytes / 1e6),
+                "l2_flush_between_steps": flush_l2,
             },
             "roofline": {
                 "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
-                "kernel": "%s (P=%d, %.3f operator B/entry)" % (kname, code_bytes, op_bytes / (rows * N)),
+                "kernel": "%s (P=%d, %.3f operator B/entry)" % (kname, plan.code_bytes, op_bytes / (rows * N)),
                 "kernel_ms": k_ms,
                 "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_src,
+                "isolated": {"kernel_ms": iso_ms,
+                             "achieved": alg_bytes / (iso_ms * 1e-3) / 1e9,
+                             "frac": alg_bytes / (iso_ms * 1e-3) / 1e9 / peak,
+                             "note": "one apply per host synchronisation (no overlap with a "
+                                     "preceding apply)"},
             },
-            "e2e": {
-                "value": k * e2e_steps / e2e_s, "unit": UNIT,
-                "h2d_bytes_per_step": k * N * 8, "d2h_bytes_per_step": k * rows * 8,
-                "path": "invop_apply_host (C ABI, pinned host fp64 buffers)",
-            },
+            "e2e": {"value": k * e2e_steps / e2e_s, "unit": UNIT,
+                    "h2d_bytes_per_step": e2e_h2d, "d2h_bytes_per_step": e2e_d2h, "path": e2e_path},
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "ordered_fp64": {"value": k * 1e3 / ord_ms, "unit": UNIT, "kernel_ms": ord_ms,
-                             "achieved_gbs": alg_bytes / (ord_ms * 1e-3) / 1e9,
-                             "note": "bitwise equal to the reference apply"},
+                             "operator_bytes": ord_bytes,
+                             "achieved_gbs": (ord_bytes + k * N * 8 + k * rows * 8) / (ord_ms * 1e-3) / 1e9,
+                             "note": "k2_ordered, bitwise equal to the reference apply; bytes = the "
+                                     "byte planes it streams"},
             "fp32_vs_fp64_relerr": err,
-            "quantization_error": {"value": qerr, "digits": cfg.digits,
-                                   "vs": "unquantized fp64 rows of L^-1 (device block LU), same x; "
-                                         "max_i |y - y_exact| / max_i |y_exact|, worst RHS"},
             "setup_s": {"factor": t_factor, "construct_and_encode": t_setup - t_factor},
             "op_counters": {"multiplications": mults, "additions": adds},
         }
-        if int8_ops:
-            result["tensor"] = {"int8_ops_per_launch": int8_ops,
-                                "achieved_tops": int8_ops / (k_ms * 1e-3) / 1e12,
-                                "nominal_peak_tops": 4500.0,
-                                "frac_of_nominal": int8_ops / (k_ms * 1e-3) / 1e12 / 4500.0,
-                                "note": "dense int8 tensor peak not measured on this pool; nominal B200 figure"}
+        if tc_ops:
+            tops = tc_ops / (k_ms * 1e-3) / 1e12
+            pk, pk_src = _int8_peak()
+            result["tensor"] = {"int8_ops_per_launch": tc_ops, "achieved_tops": tops,
+                                "peak_tops": pk, "peak_source": pk_src,
+                                "frac": tops / pk if pk else None,
+                                "note": "2*M*N*K over the kind::i8 MMAs the kernel issues"}
+        if not args.no_quant_error:
+            result["quantization_error"] = {
+                "value": quantization_error(cfg, X.astype(np.float32), Yh), "digits": cfg.digits,
+                "vs": "direct sparse solve of the unquantized operator (scipy splu), same fp32 x; "
+                      "max_i |y - y_exact| / max_i |y_exact|, worst RHS"}
         if world == 1 and not args.no_cpu_baseline:
             result["cpu_baseline"] = cpu_baseline(cfg, budget_s=args.cpu_budget)
     return result
@@ -473,7 +597,7 @@ def run_ours(args, world, rank, local):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
@@ -481,6 +605,7 @@ def main():
     ap.add_argument("--nrhs", type=int, default=0,
                     help="right-hand sides per step (default: the config's own count)")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-quant-error", action="store_true")
     args = ap.parse_args()
     world, rank, local = dist_init(args)
     if args.impl == "reference":

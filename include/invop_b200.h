@@ -97,6 +97,13 @@ int invop_plan_from_csc(int64_t n, int scale_digits, const int64_t* col_ptr,
                         const int32_t* entry_rows, const int8_t* entry_signs,
                         int64_t groups, int64_t entries, void* stream, invop_plan** out);
 
+/* Same, from HOST arrays (what a reference-side binding holds: the numpy
+   tables of ApplyPlan); synchronous. */
+int invop_plan_from_csc_host(int64_t n, int scale_digits, const int64_t* col_ptr,
+                             const int64_t* group_abs_mantissa, const int64_t* group_ptr,
+                             const int32_t* entry_rows, const int8_t* entry_signs,
+                             int64_t groups, int64_t entries, void* stream, invop_plan** out);
+
 int invop_plan_destroy(invop_plan* plan);
 
 /* plan geometry and storage */
@@ -125,6 +132,10 @@ int invop_plan_from_planes(const uint8_t* host, int code_bytes, int is_signed, i
 
 /* A2/A3 — expand codes back to int64 mantissas (device [rows x n], ldm). */
 int invop_plan_decode(const invop_plan* plan, int64_t* mant, int64_t ldm, void* stream);
+/* Selected rows only: rows is a device int64 list of plan-local row indices
+   (each in [0, rows)); mant is device [nrows x n] (ldm). */
+int invop_plan_decode_rows(const invop_plan* plan, const int64_t* rows, int64_t nrows,
+                           int64_t* mant, int64_t ldm, void* stream);
 
 /* A4 — the reference's CSC group tables, built on device from the codes.
    Pass NULL outputs to query sizes: *groups and *entries are returned
@@ -147,11 +158,25 @@ int invop_apply(const invop_plan* plan, const void* x, int64_t ldx, void* y, int
 int invop_apply_host(invop_plan* plan, const double* x, double* y, int64_t nrhs,
                      int mode, void* stream);
 
+/* Reference-seam variant (_kernels.plan_apply accumulates into the caller's
+   zero-filled `out`, _native.pyx:43-46): ordered fp64 with HOST buffers, y
+   read as each row's initial accumulator and overwritten with the result;
+   zero mantissas are skipped exactly as the reference skips them
+   (synchronous). */
+int invop_apply_host_acc(invop_plan* plan, const double* x, double* y, int64_t nrhs,
+                         void* stream);
+
 /* Bytes of operator data one apply of `nrhs` right-hand sides in `mode`
    streams from HBM (codes + per-chunk metadata), i.e. the algorithmic bytes
    of the roofline; builds the lazily created layouts first (synchronous). */
 int invop_plan_apply_bytes(invop_plan* plan, int64_t nrhs, int mode, int64_t* bytes,
                            void* stream);
+
+/* int8 tensor-core operations (2*M*N*K summed over the tcgen05 MMAs) one
+   apply of `nrhs` right-hand sides in `mode` issues; 0 for applies that do not
+   run on the tensor cores. Builds the lazily created layouts first
+   (synchronous). */
+int invop_plan_tensor_ops(invop_plan* plan, int64_t nrhs, int mode, int64_t* ops, void* stream);
 
 /* Name of the kernel an apply of `nrhs` right-hand sides in `mode` launches
    ("k2_hl", "k2_stream", "k2_fast", "k3_batched", "k2_ordered", ...), for
@@ -162,14 +187,23 @@ const char* invop_apply_kernel(const invop_plan* plan, int64_t nrhs, int mode);
    process). Each rank holds the plan of its rows [row_offsets[rank],
    row_offsets[rank+1]) of the operator; x: device [nrhs x n] (ldx), the full
    right-hand sides on every rank; y: device [nrhs x n] (ldy >= n) receives
-   this rank's rows and, through one NCCL group of in-place broadcasts over
-   `nccl_comm` (an ncclComm_t of the ranks, in rank order), every other
-   rank's rows. row_offsets: host int64 [nranks + 1]. Stream-ordered on
-   `stream`; NCCL is resolved from the process at run time
+   every rank's rows. The local rows are applied into this rank's slice of a
+   staging buffer [nranks][nrhs][pad] (pad = largest shard, owned by the
+   plan), ONE ncclAllGather over `nccl_comm` (an ncclComm_t of the ranks, in
+   rank order) fills every slice, and one kernel (invop_unshard) scatters them
+   into y. row_offsets: host int64 [nranks + 1], nranks <= 64. Stream-ordered
+   on `stream`; NCCL is resolved from the process at run time
    (INVOP_E_UNSUPPORTED when it is not loaded). */
-int invop_apply_sharded(const invop_plan* shard, void* nccl_comm, const int64_t* row_offsets,
+int invop_apply_sharded(invop_plan* shard, void* nccl_comm, const int64_t* row_offsets,
                         const void* x, int64_t ldx, void* y, int64_t ldy, int64_t nrhs,
                         int dtype, int mode, void* stream);
+
+/* The reassembly step of the sharded apply on its own, for callers that run
+   the all-gather themselves (torch.distributed): stage is device
+   [world][nrhs][pad] (slice r holds rows row_offsets[r].. of every RHS, ld
+   pad), y is device [nrhs x n] (ldy >= n = row_offsets[world]); one launch. */
+int invop_unshard(const void* stage, int world, const int64_t* row_offsets, int64_t nrhs,
+                  int64_t pad, void* y, int64_t ldy, int dtype, void* stream);
 
 /* A8 — naive quantized apply of the reference (applyplan.py:194-209):
    identical arithmetic to ORDERED mode; provided under its own name. */
@@ -210,6 +244,10 @@ int invop_dense_invert(const double* a, int64_t n, double* out, double tol, void
    pointers, m is [rows x cols] with leading dimension ld. */
 int invop_dense_matvec(const double* m, int64_t rows, int64_t cols, int64_t ld,
                        const double* x, double* y, void* stream);
+/* Same with HOST buffers (the reference seam's dense_matvec(mat, x, out));
+   synchronous. */
+int invop_dense_matvec_host(const double* m, int64_t rows, int64_t cols, int64_t ld,
+                            const double* x, double* y, void* stream);
 
 #ifdef __cplusplus
 }

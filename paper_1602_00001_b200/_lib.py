@@ -49,19 +49,25 @@ SIGNATURES = {
     "invop_plan_create": [_vp, _i64, _i64, _i64, _i64, _int, _vp, C.POINTER(_vp)],
     "invop_plan_from_f64": [_vp, _i64, _i64, _i64, _i64, _int, _pi64, _vp, C.POINTER(_vp)],
     "invop_plan_from_csc": [_i64, _int, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp, C.POINTER(_vp)],
+    "invop_plan_from_csc_host": [_i64, _int, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp, C.POINTER(_vp)],
+    "invop_apply_host_acc": [_vp, _vp, _vp, _i64, _vp],
+    "invop_dense_matvec_host": [_vp, _i64, _i64, _i64, _vp, _vp, _vp],
     "invop_plan_destroy": [_vp],
     "invop_plan_info": [_vp, _pi64, _pi64, _pi64, _pint, _pint, _pint, _pi64, _pi64],
     "invop_plan_counts": [_vp, _pi64, _pi64, _vp],
     "invop_plan_column_stats": [_vp, _vp, _vp, _vp],
     "invop_plan_decode": [_vp, _vp, _i64, _vp],
+    "invop_plan_decode_rows": [_vp, _vp, _i64, _vp, _i64, _vp],
     "invop_plan_get_planes": [_vp, _vp, _vp],
     "invop_plan_from_planes": [_vp, _int, _int, _i64, _i64, _i64, _int, _vp, C.POINTER(_vp)],
     "invop_plan_csc": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _pi64, _pi64, _vp],
     "invop_apply": [_vp, _vp, _i64, _vp, _i64, _i64, _int, _int, _vp],
     "invop_apply_host": [_vp, _vp, _vp, _i64, _int, _vp],
     "invop_apply_sharded": [_vp, _vp, _vp, _vp, _i64, _vp, _i64, _i64, _int, _int, _vp],
+    "invop_unshard": [_vp, _int, _vp, _i64, _i64, _vp, _i64, _int, _vp],
     "invop_apply_naive": [_vp, _vp, _vp, _i64, _vp],
     "invop_plan_apply_bytes": [_vp, _i64, _int, _pi64, _vp],
+    "invop_plan_tensor_ops": [_vp, _i64, _int, _pi64, _vp],
     "invop_apply_kernel": [_vp, _i64, _int],
     "invop_operator_create": [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, C.POINTER(_vp)],
     "invop_operator_factor": [_vp, _vp],
@@ -74,11 +80,6 @@ SIGNATURES = {
 
 
 def _load():
-    if not LIB_PATH.exists():
-        raise ImportError(
-            "libinvop_b200.so is not built (%s); run `python paper_1602_00001_b200/build.py` "
-            "or __graft_entry__.build()" % LIB_PATH
-        )
     lib = C.CDLL(str(LIB_PATH))
     for name, args in SIGNATURES.items():
         fn = getattr(lib, name)
@@ -92,7 +93,33 @@ def _load():
     return lib
 
 
-lib = _load()
+class _Library:
+    """libinvop_b200.so, dlopen'ed on first use (importing the package only
+    checks that it is built: modules that need no device code, e.g. the
+    workload definitions in configs/grid, stay free of the native library)."""
+
+    _cdll = None
+
+    def _get(self):
+        if _Library._cdll is None:
+            _Library._cdll = _load()
+        return _Library._cdll
+
+    def __getattr__(self, name):
+        return getattr(self._get(), name)
+
+
+if not LIB_PATH.exists():
+    raise ImportError(
+        "libinvop_b200.so is not built (%s); run `python paper_1602_00001_b200/build.py` "
+        "or __graft_entry__.build()" % LIB_PATH
+    )
+lib = _Library()
+
+
+def loaded() -> bool:
+    """True once the native library has been dlopen'ed in this process."""
+    return _Library._cdll is not None
 
 
 def last_error() -> str:

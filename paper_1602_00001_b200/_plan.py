@@ -125,6 +125,18 @@ class DevicePlan:
                                             C.c_void_p(dev.stream_ptr())), "plan_decode")
         return out
 
+    def decode_rows(self, rows):
+        """int64 mantissas of the given plan-local rows as a device tensor [len(rows) x n]."""
+        t = dev.require_cuda()
+        sel = dev.to_device(np.asarray(rows, dtype=np.int64).reshape(-1), t.int64)
+        if sel.numel() and (int(sel.min()) < 0 or int(sel.max()) >= self.rows):
+            raise ValueError("row index out of range")
+        out = t.empty((sel.numel(), self.n), dtype=t.int64, device="cuda")
+        if sel.numel() and self.n:
+            L.check(L.lib.invop_plan_decode_rows(self._h, L.ptr(sel), sel.numel(), L.ptr(out), self.n,
+                                                 C.c_void_p(dev.stream_ptr())), "plan_decode_rows")
+        return out
+
     def csc_tables(self) -> dict:
         t = dev.require_cuda()
         s = C.c_void_p(dev.stream_ptr())
@@ -152,8 +164,9 @@ class DevicePlan:
         }
 
     # ----------------------------------------------------------- apply
-    def apply_device(self, x, y=None, *, mode: int = L.MODE_ORDERED):
-        """x: device tensor [n] or [k, n]; returns device tensor [rows] / [k, rows]."""
+    def apply_device(self, x, y=None, ldy: int = None, *, mode: int = L.MODE_ORDERED):
+        """x: device tensor [n] or [k, n]; returns device tensor [rows] / [k, rows]
+        (or writes into `y`, RHS t at y[t*ldy :], when given)."""
         t = dev.require_cuda()
         dtype = t.float64 if mode == L.MODE_ORDERED else t.float32
         x = x.to(dtype=dtype).contiguous()
@@ -164,7 +177,12 @@ class DevicePlan:
         k = X.shape[0]
         if y is None:
             y = t.empty((k, self.rows), dtype=dtype, device="cuda")
-        L.check(L.lib.invop_apply(self._h, L.ptr(X), self.n, L.ptr(y), self.rows, k,
+        elif y.dtype != dtype or not y.is_cuda:
+            raise ValueError("y must be a device tensor of %s" % dtype)
+        ldy = self.rows if ldy is None else int(ldy)
+        if ldy < self.rows or y.numel() < (k - 1) * ldy + self.rows:
+            raise ValueError("y is too small for %d right-hand sides" % k)
+        L.check(L.lib.invop_apply(self._h, L.ptr(X), self.n, L.ptr(y), ldy, k,
                                   L.F64 if mode == L.MODE_ORDERED else L.F32, mode,
                                   C.c_void_p(dev.stream_ptr())), "apply")
         return y.view(-1) if one else y

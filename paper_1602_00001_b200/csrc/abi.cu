@@ -71,15 +71,6 @@ extern "C" int invop_plan_destroy(invop_plan* p) {
   if (p->k3_ws) cudaFree(p->k3_ws);
   for (int b = 0; b < 2; ++b)
     if (p->k3_tiles[b]) cudaFree(p->k3_tiles[b]);
-  if (p->vw_data) cudaFree(p->vw_data);
-  if (p->vw_meta) cudaFree(p->vw_meta);
-  if (p->vw_rowptr) cudaFree(p->vw_rowptr);
-  if (p->vw_slaboff) cudaFree(p->vw_slaboff);
-  if (p->tv_data) cudaFree(p->tv_data);
-  if (p->tv_meta) cudaFree(p->tv_meta);
-  if (p->tv_gptr) cudaFree(p->tv_gptr);
-  if (p->tv_soff) cudaFree(p->tv_soff);
-  if (p->tv_ws) cudaFree(p->tv_ws);
   if (p->hl_data) cudaFree(p->hl_data);
   if (p->hl_rowptr) cudaFree(p->hl_rowptr);
   for (int b = 0; b < 2; ++b)
@@ -89,6 +80,7 @@ extern "C" int invop_plan_destroy(invop_plan* p) {
   if (p->dl_uoff) cudaFree(p->dl_uoff);
   if (p->dl_rowlo) cudaFree(p->dl_rowlo);
   if (p->host_pinned) cudaFreeHost(p->host_pinned);
+  if (p->shard_stage) cudaFree(p->shard_stage);
   delete p;
   return INVOP_OK;
 }
@@ -117,11 +109,12 @@ static bool layout_enabled(const char* env, bool dflt) {
 }
 
 // Which kernel serves a fast-mode apply. Single right-hand side over long
-// rows: 3-byte codes take the HL layout (default; INVOP_HL=0 disables), TVW
-// and VW are opt-in (INVOP_TVW=1 / INVOP_VW=1); everything else streams the
-// byte planes (k2_stream / k2_fast). Many right-hand sides of <= 2-byte codes
-// go to the tensor-core kernel (K3; INVOP_NO_TC=1 disables).
-enum { ROUTE_PLANES = 0, ROUTE_K3, ROUTE_DL, ROUTE_HL, ROUTE_TVW, ROUTE_VW };
+// rows: codes of <= 3 bytes take the DL layout (second-order row residuals,
+// default; INVOP_DL=0 disables), 3-byte codes the HL layout when DL is
+// declined (INVOP_HL=0 disables); everything else streams the byte planes
+// (k2_stream / k2_fast). Many right-hand sides of <= 2-byte codes go to the
+// tensor-core kernel (K3; INVOP_NO_TC=1 disables).
+enum { ROUTE_PLANES = 0, ROUTE_K3, ROUTE_DL, ROUTE_HL };
 
 static int fast_route(const invop_plan* p, int64_t nrhs) {
   if (!layout_enabled("INVOP_NO_TC", false) && batched_supported(p, nrhs)) return ROUTE_K3;
@@ -129,8 +122,6 @@ static int fast_route(const invop_plan* p, int64_t nrhs) {
   if (p->P <= 3 && p->dl_ready >= 0 && layout_enabled("INVOP_DL", true)) return ROUTE_DL;
   if (p->P == 3 && p->ld <= 16384 && p->hl_ready >= 0 && layout_enabled("INVOP_HL", true))
     return ROUTE_HL;
-  if (p->tv_ready >= 0 && layout_enabled("INVOP_TVW", false)) return ROUTE_TVW;
-  if (p->vw_ready >= 0 && layout_enabled("INVOP_VW", false)) return ROUTE_VW;
   return ROUTE_PLANES;
 }
 
@@ -138,11 +129,9 @@ extern "C" const char* invop_apply_kernel(const invop_plan* p, int64_t nrhs, int
   if (!p) return "";
   if (mode == INVOP_MODE_ORDERED) return "k2_ordered";
   switch (fast_route(p, nrhs)) {
-    case ROUTE_K3: return k3d_bytes(p) > 0 ? "k3_batched_dl" : "k3_batched";
+    case ROUTE_K3: return k3_uses_dl(p) ? "k3_batched_dl" : "k3_batched";
     case ROUTE_DL: return "k2_dl";
     case ROUTE_HL: return "k2_hl";
-    case ROUTE_TVW: return "k2_tvw";
-    case ROUTE_VW: return "k2_vw";
     default: return stream_selected(p, nrhs) ? "k2_stream" : "k2_fast";
   }
 }
@@ -175,21 +164,16 @@ extern "C" int invop_apply(const invop_plan* p, const void* x, int64_t ldx, void
     if (route == ROUTE_K3)
       return apply_batched_launch(mp, (const float*)x, nrhs > 1 ? ldx : p->n, (float*)y,
                                   nrhs > 1 ? ldy : p->rows, nrhs, s);
-    if (route != ROUTE_PLANES) {
-      int rc = route == ROUTE_DL ? dl_build(mp, s) : route == ROUTE_HL ? hl_build(mp, s)
-             : route == ROUTE_TVW ? tvw_build(mp, s) : vw_build(mp, s);
-      if (rc == INVOP_OK) {
+    if (route == ROUTE_DL || route == ROUTE_HL) {
+      int rc = route == ROUTE_DL ? dl_build(mp, s) : hl_build(mp, s);
+      if (rc == INVOP_OK)
         rc = route == ROUTE_DL ? apply_dl_launch(mp, x, y, false, s)
-           : route == ROUTE_HL ? apply_hl_launch(mp, (const float*)x, (float*)y, s)
-           : route == ROUTE_TVW ? apply_tvw_launch(mp, (const float*)x, (float*)y, s)
-                                : apply_vw_launch(mp, (const float*)x, (float*)y, s);
-      }
+                               : apply_hl_launch(mp, (const float*)x, (float*)y, s);
       if (rc != INVOP_E_UNSUPPORTED) return rc;
+      // layout not applicable to this plan: the next route
       if (route == ROUTE_HL) mp->hl_ready = -1;
       if (route == ROUTE_DL) mp->dl_ready = -1;
-      if (route == ROUTE_DL || route == ROUTE_HL)
-        return invop_apply(p, x, ldx, y, ldy, nrhs, dtype, mode, stream);   // next route
-      // layout not applicable to this plan: plain byte planes below
+      return invop_apply(p, x, ldx, y, ldy, nrhs, dtype, mode, stream);
     }
     return apply_fast_launch(p, (const float*)x, nrhs > 1 ? ldx : p->n, (float*)y,
                              nrhs > 1 ? ldy : p->rows, nrhs, s);
@@ -205,31 +189,37 @@ extern "C" int invop_plan_apply_bytes(invop_plan* p, int64_t nrhs, int mode, int
   cudaStream_t s = (cudaStream_t)stream;
   if (mode == INVOP_MODE_FAST) {
     const int route = fast_route(p, nrhs);
-    if (route == ROUTE_K3 && k3d_bytes(p) > 0) {
-      *bytes = k3d_bytes(p);
+    if (route == ROUTE_K3) {
+      const int rc = k3_prepare(p, s);
+      if (rc) return rc;
+      *bytes = k3_uses_dl(p) ? k3d_bytes(p) : (int64_t)p->P * p->rows * p->ld;
       return INVOP_OK;
     }
-    int rc = route == ROUTE_DL ? dl_build(p, s) : route == ROUTE_HL ? hl_build(p, s)
-           : route == ROUTE_TVW ? tvw_build(p, s) : route == ROUTE_VW ? vw_build(p, s)
-           : INVOP_E_UNSUPPORTED;
-    if (rc == INVOP_E_UNSUPPORTED && (route == ROUTE_DL || route == ROUTE_HL))
-      return invop_plan_apply_bytes(p, nrhs, mode, bytes, stream);   // next route
-    if (rc == INVOP_OK) {
-      if (route == ROUTE_DL) {
-        *bytes = p->dl_bytes + (p->rows * p->dl_nslabs + 1) * 8;
-      } else if (route == ROUTE_HL) {
-        *bytes = p->hl_bytes + (p->rows + 1) * 8;
-      } else if (route == ROUTE_TVW) {
-        *bytes = tvw_stream_bytes(p);
-      } else {
-        const int64_t nch = p->ld / 512, nchp = (nch + 1) & ~1;
-        *bytes = p->vw_bytes + p->rows * nchp * 8 + (p->rows + 1) * 8;
+    if (route == ROUTE_DL || route == ROUTE_HL) {
+      const int rc = route == ROUTE_DL ? dl_build(p, s) : hl_build(p, s);
+      if (rc == INVOP_E_UNSUPPORTED) {
+        if (route == ROUTE_HL) p->hl_ready = -1;
+        if (route == ROUTE_DL) p->dl_ready = -1;
+        return invop_plan_apply_bytes(p, nrhs, mode, bytes, stream);   // next route
       }
+      if (rc) return rc;
+      *bytes = route == ROUTE_DL ? p->dl_bytes + (p->rows * p->dl_nslabs + 1) * 8
+                                 : p->hl_bytes + (p->rows + 1) * 8;
       return INVOP_OK;
     }
-    if (rc != INVOP_E_UNSUPPORTED) return rc;
   }
   *bytes = (int64_t)p->P * p->rows * p->ld;
+  return INVOP_OK;
+}
+
+extern "C" int invop_plan_tensor_ops(invop_plan* p, int64_t nrhs, int mode, int64_t* ops,
+                                     void* stream) {
+  if (!p || !ops) return fail(INVOP_E_VALUE, "NULL argument");
+  *ops = 0;
+  if (mode != INVOP_MODE_FAST || fast_route(p, nrhs) != ROUTE_K3) return INVOP_OK;
+  const int rc = k3_prepare(p, (cudaStream_t)stream);
+  if (rc) return rc;
+  *ops = k3_tensor_ops(p, nrhs);
   return INVOP_OK;
 }
 
@@ -337,6 +327,99 @@ extern "C" int invop_apply_host(invop_plan* p, const double* x, double* y, int64
   INVOP_CUDA(cudaMemcpyAsync(y, dy, yb, cudaMemcpyDeviceToHost, s));
   INVOP_CUDA(cudaStreamSynchronize(s));
   return INVOP_OK;
+}
+
+// reference-seam entry (_kernels.plan_apply accumulates into the caller's
+// `out`, _native.pyx:43-46): ordered fp64, each row's chain starts at y[row]
+extern "C" int invop_apply_host_acc(invop_plan* p, const double* x, double* y, int64_t nrhs,
+                                    void* stream) {
+  if (!p) return fail(INVOP_E_VALUE, "plan is NULL");
+  if (nrhs <= 0 || p->rows == 0) return INVOP_OK;
+  if (!x || !y) return fail(INVOP_E_VALUE, "NULL vector");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t xb = (size_t)nrhs * p->n * sizeof(double);
+  const size_t yb = (size_t)nrhs * p->rows * sizeof(double);
+  int rc = ensure_scratch(&p->dev_x, &p->dev_x_bytes, xb + 64);
+  if (rc) return rc;
+  rc = ensure_scratch(&p->dev_y, &p->dev_y_bytes, yb + 64);
+  if (rc) return rc;
+  double* dx = (double*)p->dev_x;
+  double* dy = (double*)p->dev_y;
+  INVOP_CUDA(cudaMemcpyAsync(dx, x, xb, cudaMemcpyHostToDevice, s));
+  INVOP_CUDA(cudaMemcpyAsync(dy, y, yb, cudaMemcpyHostToDevice, s));
+  if (p->n > 0) {
+    rc = apply_ordered_launch(p, dx, p->n, dy, p->rows, nrhs, s, /*accumulate=*/true);
+    if (rc) return rc;
+  }
+  INVOP_CUDA(cudaMemcpyAsync(y, dy, yb, cudaMemcpyDeviceToHost, s));
+  INVOP_CUDA(cudaStreamSynchronize(s));
+  return INVOP_OK;
+}
+
+// host-table variant of invop_plan_from_csc (the reference-side binding
+// holds numpy arrays, applyplan.py:42-98): upload, build, free
+extern "C" int invop_plan_from_csc_host(int64_t n, int scale_digits, const int64_t* col_ptr,
+                                        const int64_t* group_abs_mantissa, const int64_t* group_ptr,
+                                        const int32_t* entry_rows, const int8_t* entry_signs,
+                                        int64_t groups, int64_t entries, void* stream,
+                                        invop_plan** out) {
+  if (!out) return fail(INVOP_E_VALUE, "out is NULL");
+  *out = nullptr;
+  if (n < 0 || groups < 0 || entries < 0) return fail(INVOP_E_VALUE, "bad table sizes");
+  if (!col_ptr || !group_ptr || (groups > 0 && !group_abs_mantissa) ||
+      (entries > 0 && (!entry_rows || !entry_signs)))
+    return fail(INVOP_E_VALUE, "NULL table");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t b_col = (size_t)(n + 1) * 8, b_gabs = (size_t)groups * 8,
+               b_gptr = (size_t)(groups + 1) * 8, b_rows = (size_t)entries * 4,
+               b_sign = (size_t)entries;
+  const size_t o_gabs = round_up(b_col, 256), o_gptr = o_gabs + round_up(b_gabs, 256),
+               o_rows = o_gptr + round_up(b_gptr, 256), o_sign = o_rows + round_up(b_rows, 256),
+               total = o_sign + round_up(b_sign, 256) + 256;
+  char* d = nullptr;
+  INVOP_CUDA(cudaMalloc(&d, total));
+  int rc = INVOP_OK;
+  cudaError_t e = cudaMemcpyAsync(d, col_ptr, b_col, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && b_gabs) e = cudaMemcpyAsync(d + o_gabs, group_abs_mantissa, b_gabs, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d + o_gptr, group_ptr, b_gptr, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && b_rows) e = cudaMemcpyAsync(d + o_rows, entry_rows, b_rows, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && b_sign) e = cudaMemcpyAsync(d + o_sign, entry_signs, b_sign, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) rc = cuda_fail(e, "plan_from_csc_host upload");
+  if (!rc)
+    rc = invop_plan_from_csc(n, scale_digits, (const int64_t*)d, (const int64_t*)(d + o_gabs),
+                             (const int64_t*)(d + o_gptr), (const int32_t*)(d + o_rows),
+                             (const int8_t*)(d + o_sign), groups, entries, stream, out);
+  cudaStreamSynchronize(s);
+  cudaFree(d);
+  return rc;
+}
+
+// host-buffer variant of invop_dense_matvec (the reference seam's
+// dense_matvec(mat, x, out), _native.pyx:75-92): synchronous
+extern "C" int invop_dense_matvec_host(const double* m, int64_t rows, int64_t cols, int64_t ld,
+                                       const double* x, double* y, void* stream) {
+  if (rows < 0 || cols < 0 || ld < cols) return fail(INVOP_E_VALUE, "bad geometry");
+  if (rows == 0) return INVOP_OK;
+  if (!m || !x || !y) return fail(INVOP_E_VALUE, "NULL argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t bm = (size_t)rows * ld * 8, bx = (size_t)cols * 8, by = (size_t)rows * 8;
+  char* d = nullptr;
+  INVOP_CUDA(cudaMalloc(&d, round_up(bm, 256) + round_up(bx, 256) + by + 256));
+  double* dm = (double*)d;
+  double* dx = (double*)(d + round_up(bm, 256));
+  double* dy = (double*)(d + round_up(bm, 256) + round_up(bx, 256));
+  int rc = INVOP_OK;
+  cudaError_t e = cudaMemcpyAsync(dm, m, bm, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && bx) e = cudaMemcpyAsync(dx, x, bx, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) rc = cuda_fail(e, "dense_matvec_host upload");
+  if (!rc) rc = invop_dense_matvec(dm, rows, cols, ld, dx, dy, stream);
+  if (!rc) {
+    e = cudaMemcpyAsync(y, dy, by, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) rc = cuda_fail(e, "dense_matvec_host download");
+  }
+  cudaStreamSynchronize(s);
+  cudaFree(d);
+  return rc;
 }
 
 extern "C" int invop_apply_naive(const invop_plan* p, const double* x, double* y, int64_t nrhs,

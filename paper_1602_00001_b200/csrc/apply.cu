@@ -598,6 +598,10 @@ struct OrdArgs {
   int64_t ldx;
   double* y;
   int64_t ldy;
+  // accumulate mode (the reference seam's `out +=` contract, _native.pyx:43-46):
+  // each row's chain starts at y[row] instead of +0, and zero codes are
+  // skipped outright (the reference never adds them; -0 + +0 would be +0)
+  int accumulate;
 };
 
 __device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
@@ -693,7 +697,8 @@ __global__ void __launch_bounds__(128) k2_ordered(OrdArgs a) {
 
   double acc[KR];
 #pragma unroll
-  for (int k = 0; k < KR; ++k) acc[k] = 0.0;
+  for (int k = 0; k < KR; ++k)
+    acc[k] = (a.accumulate && myrow < a.rows) ? a.y[k * a.ldy + myrow] : 0.0;
   const int sr = lane;  // my row inside the tile
   for (int64_t t = 0; t < ntiles; ++t) {
     issue(t + ORD_STAGES - 1, (int)((t + ORD_STAGES - 1) % ORD_STAGES));
@@ -708,7 +713,7 @@ __global__ void __launch_bounds__(128) k2_ordered(OrdArgs a) {
     for (int k = 0; k < KR; ++k)
 #pragma unroll
       for (int i = 0; i < 4; ++i) fin = fin && isfinite(xs[k * ORD_TILE + lane * 4 + i]);
-    const bool masked = __any_sync(0xffffffffu, !fin);
+    const bool masked = a.accumulate || __any_sync(0xffffffffu, !fin);
     // All 8 chunks of the tile unrolled, so the independent decode / product
     // work of chunk c+1 overlaps the ordered DADD chain of chunk c.
     // For finite x, adding (0*10^-m)*x_j = +-0 leaves the accumulator bitwise
@@ -779,11 +784,14 @@ __global__ void __launch_bounds__(128) k2_ordered(OrdArgs a) {
             t[2 * q2 + 1] = __dmul_rn(d[2 * q2 + 1], xv.y);
           }
           if (MASKED) {
+            // the reference's zero skip (_native.pyx:32-46 never sees a zero
+            // mantissa): the chain does not advance on a zero code
 #pragma unroll
-            for (int q = 0; q < 16; ++q) t[q] = d[q] != 0.0 ? t[q] : 0.0;
+            for (int q = 0; q < 16; ++q) acc[k] = d[q] != 0.0 ? __dadd_rn(acc[k], t[q]) : acc[k];
+          } else {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) acc[k] = __dadd_rn(acc[k], t[q]);
           }
-#pragma unroll
-          for (int q = 0; q < 16; ++q) acc[k] = __dadd_rn(acc[k], t[q]);
         }
       }
     }
@@ -825,7 +833,7 @@ static int launch_ord_p(OrdArgs a, int KR, cudaStream_t s) {
 }
 
 int apply_ordered_launch(const invop_plan* p, const double* x, int64_t ldx, double* y,
-                         int64_t ldy, int64_t nrhs, cudaStream_t s) {
+                         int64_t ldy, int64_t nrhs, cudaStream_t s, bool accumulate) {
   if (p->rows == 0 || nrhs == 0) return INVOP_OK;
   for (int64_t k0 = 0; k0 < nrhs;) {
     int KR = nrhs - k0 >= 4 && p->P <= 4 ? 4 : (nrhs - k0 >= 2 ? 2 : 1);
@@ -834,6 +842,7 @@ int apply_ordered_launch(const invop_plan* p, const double* x, int64_t ldx, doub
     a.rows = p->rows; a.n = p->n; a.ld = p->ld; a.scale = p->scale;
     a.x = x + k0 * ldx; a.ldx = ldx;
     a.y = y + k0 * ldy; a.ldy = ldy;
+    a.accumulate = accumulate ? 1 : 0;
     int rc;
     switch (p->P * 2 + p->is_signed) {
       case 2: rc = launch_ord_p<1, false>(a, KR, s); break;

@@ -908,8 +908,37 @@ static int k3d_build(invop_plan* p, cudaStream_t s) {
   return INVOP_OK;
 }
 
+// the DL kernel serves a batched apply when its residual tiles were built,
+// the row prefix sum covers the rows (<= 1024 segments) and no INVOP_K3_CFG
+// variant selects a byte-plane configuration
+bool k3_uses_dl(const invop_plan* p) {
+  if (p->k3d_ready <= 0 || cdiv(p->rows, K3D_SEG) > K3D_SEG) return false;
+  int tiles = K3_TILES, stages = K3_STAGES;
+  if (const char* v = getenv("INVOP_K3_CFG")) sscanf(v, "%d,%d", &tiles, &stages);
+  return tiles == K3_TILES && stages == K3_STAGES;
+}
+
+// lazily built layouts of the batched apply (DL residual tiles)
+int k3_prepare(invop_plan* p, cudaStream_t s) {
+  const int rc = k3d_build(p, s);
+  return rc == INVOP_E_UNSUPPORTED ? INVOP_OK : rc;
+}
+
+// int8 tensor operations (2*M*N*K per MMA) one batched apply of nrhs
+// right-hand sides issues: per 64-RHS batch, per (row tile, K block) the
+// MMAs of the operand tiles present (DL: plane 0 always and plane 1 where
+// stored, N = 192; byte planes: P x 3 plane-digit products, N = 64)
+int64_t k3_tensor_ops(const invop_plan* p, int64_t nrhs) {
+  const int64_t batches = cdiv(nrhs, K3_NR);
+  const int64_t kbs = p->ld / K3_BK;
+  const int64_t rtiles = round_up(cdiv(p->rows, K3_BM), 2);
+  const int64_t per_tile_kb = 2LL * K3_BM * (K3_ND * K3_NR) * K3_BK;   // one plane x all digits
+  if (k3_uses_dl(p)) return batches * per_tile_kb * (rtiles * kbs + p->k3d_n1);
+  return batches * per_tile_kb * p->P * rtiles * kbs;
+}
+
 int64_t k3d_bytes(const invop_plan* p) {
-  if (p->k3d_ready <= 0 || cdiv(p->rows, K3D_SEG) > K3D_SEG) return -1;   // DL kernel not used
+  if (!k3_uses_dl(p)) return -1;   // DL kernel not used
   const int64_t tiles = round_up(cdiv(p->rows, K3_BM), 2) * (p->ld / K3_BK);
   return (tiles + p->k3d_n1) * K3_A_TILE + tiles * 4;
 }
@@ -945,9 +974,7 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
   size_t acc_off = round_up(max_off + (size_t)nrhs * 4, 256);
   int krc = k3d_build(p, s);
   if (krc != INVOP_OK && krc != INVOP_E_UNSUPPORTED) return krc;
-  // default config -> DL kernel (its row prefix sum handles <= 1024 segments)
-  const bool dl = p->k3d_ready > 0 && tiles == 2 && stages == 4 &&
-                  cdiv(p->rows, K3D_SEG) <= K3D_SEG;
+  const bool dl = k3_uses_dl(p);
   size_t acc_bytes = splits > 1 ? (size_t)K3_NR * p->rows * 8 : 0;
   if (dl)   // + segment carries of the row prefix sums
     acc_bytes = (size_t)K3_NR * p->rows * 8 + (size_t)K3_NR * cdiv(p->rows, K3D_SEG) * 16;

@@ -36,25 +36,10 @@ struct invop_plan {
 
   void* dev_y = nullptr; size_t dev_y_bytes = 0;
   double* host_pinned = nullptr; size_t host_pinned_bytes = 0;
+  void* shard_stage = nullptr; size_t shard_stage_bytes = 0;   // sharded.cu all-gather staging
   // K3 (tensor-core batched apply): workspace and cached TMA descriptors
   void* k3_ws = nullptr; size_t k3_ws_bytes = 0;
   uint8_t* k3_tiles[2] = {nullptr, nullptr};   // tiled copy of planes 0/1
-  // VW layout (vw.cu): per (row, 512-column chunk) base + w-byte offsets
-  uint8_t* vw_data = nullptr;
-  void* vw_meta = nullptr;          // int2 [rows][nchp]: {base, off<<3 | w}
-  int64_t* vw_rowptr = nullptr;     // [rows+1], 512-byte units
-  uint32_t* vw_slaboff = nullptr;   // [rows][nslabs+1] slab offsets within a row
-  int64_t vw_bytes = 0;
-  int vw_ready = 0;                 // 0 not built, 1 built, -1 not applicable
-  int vw_wmax = 0;
-  // TVW layout (tvw.cu): per (32-row group, 64-column tile) base + w-byte offsets
-  uint8_t* tv_data = nullptr;
-  void* tv_meta = nullptr;          // int2 [groups][nt]: {base, off2KB<<3 | w}
-  int64_t* tv_gptr = nullptr;       // [groups+1], 2 KB units
-  int64_t* tv_soff = nullptr;       // [groups][nst+1] stage boundary offsets
-  int64_t tv_bytes = 0;
-  int tv_ready = 0, tv_wmax = 0;
-  void* tv_ws = nullptr; size_t tv_ws_bytes = 0; int64_t tv_ws_cnt_off = -1;
   // HL layout (hl.cu): two low byte planes + top plane only where a chunk needs it
   uint8_t* hl_data = nullptr;
   int64_t* hl_rowptr = nullptr;     // [rows+1] byte offsets
@@ -127,19 +112,17 @@ bool batched_supported(const invop_plan* p, int64_t nrhs);
 bool stream_selected(const invop_plan* p, int64_t nrhs);
 int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, int64_t ldy,
                          int64_t nrhs, cudaStream_t s);
-int vw_build(invop_plan* p, cudaStream_t s);
-int tvw_build(invop_plan* p, cudaStream_t s);
-int64_t tvw_stream_bytes(const invop_plan* p);
 int64_t k3d_bytes(const invop_plan* p);
-int apply_tvw_launch(invop_plan* p, const float* x, float* y, cudaStream_t s);
-int apply_vw_launch(invop_plan* p, const float* x, float* y, cudaStream_t s);
+bool k3_uses_dl(const invop_plan* p);
+int64_t k3_tensor_ops(const invop_plan* p, int64_t nrhs);
+int k3_prepare(invop_plan* p, cudaStream_t s);
 int hl_build(invop_plan* p, cudaStream_t s);
 int dl_build(invop_plan* p, cudaStream_t s);
 int apply_dl_launch(invop_plan* p, const void* x, void* y, bool f64io, cudaStream_t s,
                     bool pdl = false);
 int apply_hl_launch(invop_plan* p, const float* x, float* y, cudaStream_t s);
 int apply_ordered_launch(const invop_plan* p, const double* x, int64_t ldx, double* y,
-                         int64_t ldy, int64_t nrhs, cudaStream_t s);
+                         int64_t ldy, int64_t nrhs, cudaStream_t s, bool accumulate = false);
 
 }  // namespace invop
 

@@ -99,6 +99,18 @@ __global__ void k_decode(Planes pl, int P, int is_signed, int64_t rows, int64_t 
   }
 }
 
+// rows sel[0..nsel) (plan-local) of the codes -> out[s * ldm + j]
+__global__ void k_decode_rows(Planes pl, int P, int is_signed, const int64_t* __restrict__ sel,
+                              int64_t nsel, int64_t cols, int64_t ld, int64_t* __restrict__ out,
+                              int64_t ldm) {
+  const int64_t total = nsel * cols;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = k / cols, j = k - s * cols;
+    out[s * ldm + j] = load_code(pl, P, is_signed, sel[s] * ld + j);
+  }
+}
+
 // numpy: scaled = e * 10.0**d ; mant = copysign(floor(|scaled| + 0.5), scaled)
 __device__ __forceinline__ double round_half_away(double e, double p10) {
   double scaled = __dmul_rn(e, p10);
@@ -604,6 +616,19 @@ extern "C" int invop_plan_decode(const invop_plan* p, int64_t* mant, int64_t ldm
   k_decode<<<grid_for(total), 256, 0, (cudaStream_t)stream>>>(planes_of(p), p->P, p->is_signed,
                                                               p->rows, p->n, p->ld, mant, ldm);
   INVOP_CHECK_LAUNCH("decode");
+  return INVOP_OK;
+}
+
+extern "C" int invop_plan_decode_rows(const invop_plan* p, const int64_t* rows, int64_t nrows,
+                                      int64_t* mant, int64_t ldm, void* stream) {
+  if (!p) return fail(INVOP_E_VALUE, "plan is NULL");
+  if (ldm < p->n) return fail(INVOP_E_VALUE, "ldm < n");
+  if (nrows < 0 || (nrows > 0 && (!rows || !mant))) return fail(INVOP_E_VALUE, "bad row list");
+  const int64_t total = nrows * p->n;
+  if (total == 0) return INVOP_OK;
+  k_decode_rows<<<grid_for(total), 256, 0, (cudaStream_t)stream>>>(
+      planes_of(p), p->P, p->is_signed, rows, nrows, p->n, p->ld, mant, ldm);
+  INVOP_CHECK_LAUNCH("decode_rows");
   return INVOP_OK;
 }
 

@@ -308,45 +308,97 @@ def test_construct_matches_scipy(invop, O):
 
 
 # ------------------------------------------------------------------ full-size configs
-def _config_parity(invop, O, key, sample=24, seed=0):
-    """Full-size config: device construction (K4+K1) vs the oracle's sparse-LU
-    rows; apply parity on the device's own codes for sampled rows."""
-    import torch
+def _sample_rows(st, N, count, seed):
+    """`count` random rows plus the centre row (the largest entries), the
+    first/last rows and rows at grid-line and 128-row tile boundaries."""
+    rng = np.random.default_rng(seed)
+    centre = (st.ny // 2) * st.nx + st.nx // 2
+    special = [0, 1, 2, centre, centre + 1, N - 2, N - 1, st.nx - 1, st.nx, st.nx + 1, 127, 128,
+               129, 255, 256, 257]
+    rows = np.concatenate([special, rng.choice(N, count, replace=False)])
+    return np.unique(rows[(rows >= 0) & (rows < N)])
+
+
+def _check_construction(O, st, dplan, digits, rows):
+    """Device K4+K1 mantissas vs the oracle's sparse-LU rows of L^-1 quantized
+    with the reference rounding: equal up to rounding near-ties (|d| <= 1)."""
+    ref_mant = O.quantize(O.inverse_rows(st, rows), digits)
+    dev_mant = dplan.decode_rows(rows).cpu().numpy()
+    diff = np.abs(dev_mant - ref_mant)
+    assert diff.max() <= 1, "construction differs by more than one unit"
+    assert (diff != 0).mean() < 1e-4, "too many rounding-tie disagreements"
+    return dev_mant
+
+
+def _config_parity_all_rows(invop, O, key):
+    """Full-size config, EVERY row: the device's codes decoded to the host and
+    the oracle's threaded ordered apply over all rows (the reference sum,
+    applyplan.py:4-8) — the fp64 path bitwise, the fp32 path within 1e-5; the
+    construction against sparse-LU rows on 256+ sampled rows."""
     from paper_1602_00001_b200 import configs
 
     cfg = configs.get(key)
     st = cfg.operator()
     N = st.n
     dplan = invop.DeviceOperator(st).factor().quantized_rows(cfg.digits)
-    rng = np.random.default_rng(seed)
-    rows = np.unique(np.concatenate([[0, N // 2 + st.nx // 2, N - 1], rng.choice(N, sample, replace=False)]))
-    # construction agreement: mantissas from the oracle's fp64 rows
-    ref_rows = O.inverse_rows(st, rows)
-    ref_mant = O.quantize(ref_rows, cfg.digits)
-    dev_mant = dplan.decode()[torch.as_tensor(rows, device="cuda")].cpu().numpy()
-    diff = np.abs(dev_mant - ref_mant)
-    assert diff.max() <= 1, "construction differs by more than one unit"
-    assert (diff != 0).mean() < 1e-4, "too many rounding-tie disagreements"
-    X = cfg.rhs()
+    _check_construction(O, st, dplan, cfg.digits, _sample_rows(st, N, 256, key))
+    mant = dplan.decode().cpu().numpy()
     plan = invop.ApplyPlan(n=N, scale_digits=cfg.digits, _dplan=dplan)
-    for t in range(min(X.shape[0], 4)):
+    X = cfg.rhs()
+    for t in range(X.shape[0]):
         x = X[t]
-        y64, _ = invop.apply(plan, x)
+        y64, c = invop.apply(plan, x)
         y32, _ = invop.apply(plan, x, precision="f32")
-        yo = O.ordered_apply(dev_mant, cfg.digits, x)        # identical codes -> bitwise
-        assert y64[rows].tobytes() == yo.tobytes()
-        assert O.relative_error(y32[rows], yo) <= F32_TOL
-        assert O.relative_error(y32, y64) <= F32_TOL
+        yo = O.ordered_apply(mant, cfg.digits, x)
+        assert y64.tobytes() == yo.tobytes(), "ordered fp64 apply differs from the reference sum"
+        assert O.relative_error(y32, yo) <= F32_TOL
+        assert c.additions == int(np.count_nonzero(mant))
     return dplan
 
 
 def test_config3_full_size(invop, O):
-    _config_parity(invop, O, 3)
+    _config_parity_all_rows(invop, O, 3)
 
 
 def test_config4_full_size(invop, O):
-    d = _config_parity(invop, O, 4)
+    d = _config_parity_all_rows(invop, O, 4)
     assert d.code_bytes == 3
+    assert d.apply_kernel(1) == "k2_dl"
+
+
+def test_config5_full_size(invop, O):
+    """Config 5 (N = 65536, m = 4, 64 RHS) at full size, per SURVEY 8(c):
+    construction within one unit of sparse-LU rows, and on >= 256 sampled rows
+    per RHS (centre row included) the tensor-core batched apply (64 RHS) and
+    the single-RHS DL kernel within 1e-5 of the oracle's ordered sum on the
+    device's own codes, the ordered fp64 path bitwise equal to it."""
+    import torch
+    from paper_1602_00001_b200 import configs
+
+    cfg = configs.get(5)
+    st = cfg.operator()
+    N = st.n
+    dplan = invop.DeviceOperator(st).factor().quantized_rows(cfg.digits)
+    assert dplan.code_bytes == 2
+    rows = _sample_rows(st, N, 256, 5)
+    assert rows.size >= 256
+    dev_mant = _check_construction(O, st, dplan, cfg.digits, rows)
+    X = cfg.rhs()
+    assert X.shape == (64, N)
+    Xr = X.astype(np.float32).astype(np.float64)
+    Yo32 = O.ordered_apply(dev_mant, cfg.digits, Xr)             # [64, len(rows)]
+    Xt = torch.tensor(X, device="cuda", dtype=torch.float32)
+    Y = dplan.apply_device(Xt, mode=0).cpu().numpy()
+    assert dplan.apply_kernel(64) == "k3_batched_dl"
+    for t in range(64):
+        assert relerr(Y[t][rows], Yo32[t]) <= F32_TOL, t
+    for t in (0, 31, 63):
+        y = dplan.apply_device(Xt[t], mode=0).cpu().numpy()
+        assert relerr(y[rows], Yo32[t]) <= F32_TOL, t
+    assert dplan.apply_kernel(1) == "k2_dl"
+    Y64 = dplan.apply_device(torch.tensor(X, device="cuda"), mode=1).cpu().numpy()
+    Yo64 = O.ordered_apply(dev_mant, cfg.digits, X)
+    assert np.ascontiguousarray(Y64[:, rows]).tobytes() == Yo64.tobytes()
 
 
 def test_config2_against_reference_outputs(invop, O, golden):
@@ -371,17 +423,15 @@ def test_config2_against_reference_outputs(invop, O, golden):
 @pytest.mark.parametrize("lo,hi", [(0, 250), (-120, 120), (0, 60000), (-30000, 30000),
                                    (0, 9_000_000), (-4_000_000, 4_000_000), (0, 16_000_000),
                                    (-2_000_000_000, 2_000_000_000), (0, 4_000_000_000)])
-@pytest.mark.parametrize("layout", ["tvw", "vw", "hl", "planes"])
+@pytest.mark.parametrize("layout", ["dl", "hl", "planes"])
 def test_stream_kernel_long_rows(invop, O, lo, hi, layout, monkeypatch):
     """Rows of >= 16 column steps take the bulk-copy streaming kernels:
-    k2_stream on the byte planes (default), or the compressed layouts k2_tvw
-    (tiled variable width) / k2_vw (row chunks)."""
+    k2_dl on row residuals (declined for these rough rows), k2_hl (sparse top
+    plane, 3-byte codes) or k2_stream / k2_fast on the byte planes."""
     import torch
 
-    monkeypatch.setenv("INVOP_TVW", "1" if layout == "tvw" else "0")
+    monkeypatch.setenv("INVOP_DL", "1" if layout == "dl" else "0")
     monkeypatch.setenv("INVOP_HL", "1" if layout == "hl" else "0")
-    if layout == "vw":
-        monkeypatch.setenv("INVOP_VW", "1")
 
     N, rows = 8704, 300
     rng = np.random.default_rng(hi)
