@@ -34,14 +34,23 @@ The library needs a CUDA device: every call raises if none is visible.
 from __future__ import annotations
 
 import ctypes as C
+import hashlib
 import os
 import weakref
 from pathlib import Path
 
 import numpy as np
 
-_DEFAULT = Path(__file__).resolve().parents[3] / "paper_1602_00001_b200" / "libinvop_b200.so"
-_lib = C.CDLL(os.environ.get("INVOP_B200_LIB") or str(_DEFAULT))
+def _default_lib() -> str:
+    # the in-tree build of the repository this copy was staged from
+    for d in Path(__file__).resolve().parents:
+        cand = d / "paper_1602_00001_b200" / "libinvop_b200.so"
+        if cand.exists():
+            return str(cand)
+    return "libinvop_b200.so"
+
+
+_lib = C.CDLL(os.environ.get("INVOP_B200_LIB") or _default_lib())
 _vp, _i64, _int = C.c_void_p, C.c_int64, C.c_int
 _lib.invop_last_error.restype = C.c_char_p
 _lib.invop_plan_from_csc_host.argtypes = [_i64, _int] + [_vp] * 5 + [_i64, _i64, _vp, C.POINTER(_vp)]
@@ -87,10 +96,18 @@ _plans: dict = {}
 
 
 def _device_plan(col_ptr, coeff, group_ptr, entry_rows, entry_signs) -> _Plan:
-    # tables are immutable (read-only arrays of a frozen ApplyPlan): key by
-    # their buffers; the entry keeps the arrays alive so addresses stay unique
-    key = tuple((a.__array_interface__["data"][0], a.size) for a in
-                (col_ptr, coeff, group_ptr, entry_rows, entry_signs))
+    # an ApplyPlan's tables are read-only (applyplan.py:36-39): key those by
+    # their buffers (the entry keeps the arrays alive so addresses stay
+    # unique); tables a caller may still mutate are keyed by their contents
+    tabs = (col_ptr, coeff, group_ptr, entry_rows, entry_signs)
+    if any(a.flags.writeable for a in tabs):
+        dig = hashlib.blake2b(digest_size=16)
+        for a in tabs:
+            dig.update(np.int64(a.size).tobytes())
+            dig.update(a.tobytes())
+        key = ("content", dig.digest())
+    else:
+        key = tuple((a.__array_interface__["data"][0], a.size) for a in tabs)
     hit = _plans.get(key)
     if hit is not None:
         return hit[0]
