@@ -2,7 +2,8 @@
 
 Each csrc/*.cu file is compiled in parallel to an object in build/ and the
 objects are linked into paper_1602_00001_b200/libinvop_b200.so. A rebuild
-only happens when a source or header is newer than the library.
+only happens when a source or header is newer than the library, and then only
+the objects older than their source (or any header) are recompiled.
 """
 
 from __future__ import annotations
@@ -52,8 +53,21 @@ def _stale() -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def _compile(src: Path, verbose: bool) -> Path:
+def _headers() -> list:
+    return list(CSRC.glob("*.cuh")) + list((ROOT / "include").glob("*.h"))
+
+
+def _obj_fresh(src: Path, obj: Path) -> bool:
+    if not obj.exists():
+        return False
+    t = obj.stat().st_mtime
+    return all(d.stat().st_mtime <= t for d in [src, *_headers()])
+
+
+def _compile(src: Path, verbose: bool, force: bool = False) -> Path:
     obj = BUILD / (src.stem + ".o")
+    if not force and not verbose and _obj_fresh(src, obj):
+        return obj
     cmd = [nvcc(), *ARCH, *FLAGS, "-c", str(src), "-o", str(obj)]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
@@ -70,7 +84,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         return LIB
     BUILD.mkdir(parents=True, exist_ok=True)
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 2)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose), sources()))
+        objs = list(ex.map(lambda s: _compile(s, verbose, force), sources()))
     tmp = LIB.with_suffix(".so.tmp%d" % os.getpid())
     cmd = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcudart", "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)

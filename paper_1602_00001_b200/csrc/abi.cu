@@ -65,8 +65,6 @@ extern "C" int invop_plan_destroy(invop_plan* p) {
   if (p->partial) cudaFree(p->partial);
   if (p->counters) cudaFree(p->counters);
   if (p->dev_x) cudaFree(p->dev_x);
-  if (p->k3_flag_host) cudaFreeHost(p->k3_flag_host);
-  if (p->k3_flag_event) cudaEventDestroy(p->k3_flag_event);
   if (p->dev_y) cudaFree(p->dev_y);
   if (p->k3_ws) cudaFree(p->k3_ws);
   for (int b = 0; b < 2; ++b)

@@ -29,12 +29,15 @@
 // every B tile in shared memory, halving the L2 re-reads of the digits.
 #include "common.cuh"
 #include <cuda.h>
+#include <cooperative_groups.h>
 #include <algorithm>
 #include <cstring>
 #include <cstdio>
 #include <cstdlib>
 
 namespace invop {
+
+namespace cg = cooperative_groups;
 
 static bool layout_flag(const char* env, bool dflt) {
   const char* v = getenv(env);
@@ -68,11 +71,7 @@ struct K3Args {
   int splits;
   int64_t pairs;           // ceil(rows / (K3_TILES*K3_BM))
   int nrhs;
-  const int* e;            // [64] fixed-point exponents
-  double scale;
-  float* y;
-  int64_t ldy;
-  long long* yacc;         // [64][rows] when splits > 1 (DL: always; holds D)
+  long long* yacc;         // [64][rows] exact int64 row sums (DL: of the residuals)
   const int* idx1;         // DL: compact index of a tile's digit-1 plane, -1 if absent
 };
 
@@ -406,10 +405,8 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
               long long v = 0;
 #pragma unroll
               for (int w = 0; w < NACC; ++w) v += (long long)r[w][j] * (1LL << (8 * w));
-              if (DL && a.splits == 1) {
+              if (a.splits == 1) {
                 a.yacc[(int64_t)t * a.rows + row] = v;
-              } else if (a.splits == 1) {
-                a.y[(int64_t)t * a.ldy + row] = (float)((double)v * ldexp(a.scale, -a.e[t]));
               } else {
                 atomicAdd((unsigned long long*)&a.yacc[(int64_t)t * a.rows + row],
                           (unsigned long long)v);
@@ -455,64 +452,141 @@ __global__ void k3_tile_planes(const uint8_t* __restrict__ in, int64_t rows, int
 }
 
 // ------------------------------------------------------------ x preparation
-// max |x_t| for every right-hand side (as the bits of a non-negative float,
-// combined with atomicMax) plus an inf/nan flag; grid = (column chunks, RHS)
-__global__ void k3_xmax(const float* __restrict__ x, int64_t n, int64_t ldx,
-                        unsigned int* __restrict__ maxbits, int* __restrict__ nonfinite) {
-  const int t = blockIdx.y;
-  float m = 0.0f;
-  bool bad = false;
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    const float v = x[t * ldx + j];
-    bad |= !isfinite(v);
-    m = fmaxf(m, fabsf(v));
-  }
-  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1);
-  // one atomic per block (per-warp atomics on one address serialise in L2)
-  __shared__ float wm[32];
-  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    float v = threadIdx.x < (blockDim.x >> 5) ? wm[threadIdx.x] : 0.0f;
-    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-    if (threadIdx.x == 0) atomicMax(&maxbits[t], __float_as_uint(v));
-  }
-}
+// k3_prep: one cluster of K3P_CL CTAs per right-hand side t (grid (K3P_CL, 64)),
+// each CTA a contiguous share of the columns, 16 consecutive columns per
+// thread (four 16-byte loads of x; the same registers feed both passes when
+// the share fits one sweep of the CTA, i.e. n <= K3P_CL * K3P_TPB * 16).
+//  1. max |x_tj| over the finite entries: block reduction, then across the
+//     cluster through distributed shared memory (one launch, no atomics);
+//     columns whose x is inf/nan are listed instead (nf_cols[t][.]): the
+//     reference skips zero mantissas (_native.pyx:32-46), so those columns
+//     are applied exactly by k3_post and enter the digits as 0;
+//  2. the exponent e_t (max|x_t| 2^e_t < 2^22) and the balanced base-256
+//     digits of X = rint(x 2^e_t) into B[l][t][j] (int8), three 16-byte
+//     stores per thread. Right-hand sides t >= nrhs get zeros;
+//  3. DL: plan rows 0 and 1 are stored as zero residuals; their exact sums
+//     Y_0, Y_1 come from the byte-plane codes and the same X (16-byte plane
+//     loads beside the digits), reduced across the cluster, and k3_post adds
+//     the corrections D_0 += Y_0, D_1 += Y_1 - 2 Y_0 (y01[t]).
+constexpr int K3P_CL = 16;            // non-portable cluster size (opt-in at launch)
+constexpr int K3P_TPB = 256;
+constexpr int K3P_SWEEP = K3P_TPB * 16;
 
-__device__ __forceinline__ int k3_exponent(unsigned int bits) {
-  const float m = __uint_as_float(bits);
+struct K3Prep {
+  const float* x;
+  int64_t n, ldx;
+  int nrhs;
+  int8_t* B;
+  int64_t ldb;
+  int* e;
+  int* nf_count;
+  int* nf_cols;
+  const uint8_t* planes[2];   // rows 0/1 codes (DL)
+  int64_t ld, rows;
+  int P, sgn, rows01;
+  long long* y01;             // [64][2] corrections of D_0, D_1 (DL)
+};
+
+__device__ __forceinline__ int k3_exponent(float m) {
   int ex = 0;
   if (m > 0.0f && isfinite(m)) frexpf(m, &ex);
   return (m > 0.0f && isfinite(m)) ? 22 - ex : 0;   // max|x_t| * 2^e_t < 2^22
 }
 
-// balanced base-256 digits of X = rint(x * 2^e), into B[l][t][j] (int8);
-// one thread per 16 consecutive columns of one right-hand side (ldb is a
-// multiple of 64): three 16-byte stores
-__global__ void k3_digits(const float* __restrict__ x, int64_t n, int64_t ldx, int nrhs,
-                          const unsigned int* __restrict__ maxbits, int* __restrict__ e,
-                          int8_t* __restrict__ B, int64_t ldb) {
-  const int64_t per = ldb / 16;
-  const int64_t total = (int64_t)K3_NR * per;
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    const int t = (int)(k / per);
-    const int64_t j0 = (k - (int64_t)t * per) * 16;
-    const int et = t < nrhs ? k3_exponent(maxbits[t]) : 0;
-    if (j0 == 0) e[t] = et;
+__device__ __forceinline__ int32_t k3_code16(uint32_t lo, uint32_t hi, int bb, int P, int sgn) {
+  uint32_t u = (lo >> bb) & 255u;
+  if (P > 1) u |= ((hi >> bb) & 255u) << 8;
+  const int sh = 32 - 8 * P;
+  return sgn ? ((int32_t)(u << sh) >> sh) : (int32_t)u;
+}
+
+// cluster barrier halves: arrive without a release fence (only register or
+// shared-memory state the peers already consumed is involved) / wait
+__device__ __forceinline__ void k3_cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void k3_cluster_wait() {
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void k3p_load16(const float* xt, int64_t jb, int64_t n, bool live,
+                                           float* xv) {
+  if (live && jb + 16 <= n && (((uintptr_t)(xt + jb)) & 15) == 0) {
+#pragma unroll
+    for (int i = 0; i < 16; i += 4) {
+      const float4 f = *reinterpret_cast<const float4*>(xt + jb + i);
+      xv[i] = f.x; xv[i + 1] = f.y; xv[i + 2] = f.z; xv[i + 3] = f.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) xv[i] = (live && jb + i < n) ? xt[jb + i] : 0.0f;
+  }
+}
+
+__global__ void __launch_bounds__(K3P_TPB, 4) k3_prep(K3Prep a) {
+  cg::cluster_group cl = cg::this_cluster();
+  __shared__ float s_warp[K3P_TPB / 32];
+  __shared__ long long s_w01[K3P_TPB / 32][2];
+  __shared__ float s_max, s_gmax;
+  __shared__ long long s_01[2];
+  const int t = blockIdx.y;
+  const int c = (int)cl.block_rank();
+  const bool live = t < a.nrhs;
+  const float* xt = a.x + (int64_t)t * a.ldx;
+  const int64_t per = round_up(cdiv(a.ldb, K3P_CL), 16);
+  const int64_t j0 = (int64_t)c * per, j1 = min(a.ldb, j0 + per);
+  const bool one = per <= K3P_SWEEP;           // x stays in registers
+  float m = 0.0f;                              // nf_count[t] is 0 on entry (k3_post resets it)
+  float xv[16];
+  for (int64_t jb = j0 + (int64_t)threadIdx.x * 16; jb < j1; jb += K3P_SWEEP) {
+    k3p_load16(xt, jb, a.n, live, xv);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      if (isfinite(xv[i])) {
+        m = fmaxf(m, fabsf(xv[i]));
+      } else {
+        const int k = atomicAdd(&a.nf_count[t], 1);
+        a.nf_cols[(int64_t)t * a.n + k] = (int)(jb + i);
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) s_warp[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float v = 0.0f;
+#pragma unroll
+    for (int w = 0; w < K3P_TPB / 32; ++w) v = fmaxf(v, s_warp[w]);
+    s_max = v;
+  }
+  cl.sync();
+  // lane r of warp 0 reads peer r (parallel DSMEM loads), then a warp max
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < K3P_CL ? *cl.map_shared_rank(&s_max, (int)threadIdx.x) : 0.0f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (threadIdx.x == 0) s_gmax = v;
+  }
+  __syncthreads();
+  const float gm = s_gmax;
+  const int et = live ? k3_exponent(gm) : 0;
+  if (c == 0 && threadIdx.x == 0) a.e[t] = et;
+  long long s0 = 0, s1 = 0;
+  for (int64_t jb = j0 + (int64_t)threadIdx.x * 16; jb < j1; jb += K3P_SWEEP) {
+    if (!one) k3p_load16(xt, jb, a.n, live, xv);
+    int X[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) X[i] = isfinite(xv[i]) ? __float2int_rn(ldexpf(xv[i], et)) : 0;
     uint32_t w[3][4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       uint32_t b0 = 0, b1 = 0, b2 = 0;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const int64_t j = j0 + 4 * q + i;
-        int X = 0;
-        if (t < nrhs && j < n) X = __float2int_rn(ldexpf(x[t * ldx + j], et));
-        const int d0 = ((X + 128) & 255) - 128;
-        const int X1 = (X - d0) >> 8;
+        const int Xv = X[4 * q + i];
+        const int d0 = ((Xv + 128) & 255) - 128;
+        const int X1 = (Xv - d0) >> 8;
         const int d1 = ((X1 + 128) & 255) - 128;
         const int d2 = (X1 - d1) >> 8;
         b0 |= ((uint32_t)d0 & 255u) << (8 * i);
@@ -523,21 +597,62 @@ __global__ void k3_digits(const float* __restrict__ x, int64_t n, int64_t ldx, i
     }
 #pragma unroll
     for (int l = 0; l < 3; ++l)
-      *reinterpret_cast<uint4*>(B + (int64_t)(l * K3_NR + t) * ldb + j0) =
+      *reinterpret_cast<uint4*>(a.B + (int64_t)(l * K3_NR + t) * a.ldb + jb) =
           make_uint4(w[l][0], w[l][1], w[l][2], w[l][3]);
+    if (a.rows01 && live) {
+      // plane rows are ld >= ldb bytes with zero padding: 16-byte loads
+      const uint4 p00 = *reinterpret_cast<const uint4*>(a.planes[0] + jb);
+      const uint4 p01 = *reinterpret_cast<const uint4*>(a.planes[1] + jb);
+      const bool two = a.rows > 1;
+      const uint4 p10 = two ? *reinterpret_cast<const uint4*>(a.planes[0] + a.ld + jb) : make_uint4(0, 0, 0, 0);
+      const uint4 p11 = two ? *reinterpret_cast<const uint4*>(a.planes[1] + a.ld + jb) : make_uint4(0, 0, 0, 0);
+      const uint32_t A0[4] = {p00.x, p00.y, p00.z, p00.w}, A1[4] = {p01.x, p01.y, p01.z, p01.w};
+      const uint32_t B0[4] = {p10.x, p10.y, p10.z, p10.w}, B1[4] = {p11.x, p11.y, p11.z, p11.w};
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int q = i >> 2, bb = 8 * (i & 3);
+        s0 += (long long)k3_code16(A0[q], A1[q], bb, a.P, a.sgn) * X[i];
+        s1 += (long long)k3_code16(B0[q], B1[q], bb, a.P, a.sgn) * X[i];
+      }
+    }
   }
-}
-
-__global__ void k3_finalize(const long long* __restrict__ yacc, int64_t rows, int nrhs,
-                            const int* __restrict__ e, double scale, float* __restrict__ y,
-                            int64_t ldy) {
-  const int64_t total = (int64_t)nrhs * rows;
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    const int t = (int)(k / rows);
-    const int64_t i = k - (int64_t)t * rows;
-    y[t * ldy + i] = (float)((double)yacc[t * rows + i] * ldexp(scale, -e[t]));
+  if (a.rows01) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    }
+    if ((threadIdx.x & 31) == 0) { s_w01[threadIdx.x >> 5][0] = s0; s_w01[threadIdx.x >> 5][1] = s1; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      long long v0 = 0, v1 = 0;
+#pragma unroll
+      for (int w = 0; w < K3P_TPB / 32; ++w) { v0 += s_w01[w][0]; v1 += s_w01[w][1]; }
+      s_01[0] = v0;
+      s_01[1] = v1;
+    }
+    cl.sync();
+    if (c == 0 && threadIdx.x < 32) {
+      long long y0 = 0, y1 = 0;
+      if (threadIdx.x < K3P_CL) {
+        const long long* p = cl.map_shared_rank(s_01, (int)threadIdx.x);
+        y0 = p[0];
+        y1 = p[1];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        y0 += __shfl_xor_sync(0xffffffffu, y0, o);
+        y1 += __shfl_xor_sync(0xffffffffu, y1, o);
+      }
+      if (threadIdx.x == 0) {
+        a.y01[2 * t] = y0;
+        a.y01[2 * t + 1] = y1 - 2 * y0;
+      }
+    }
   }
+  // peers read s_max / s_01 through DSMEM until here (values already consumed)
+  k3_cluster_arrive_relaxed();
+  k3_cluster_wait();
 }
 
 // ------------------------------------------------------------ K3 on row residuals
@@ -639,61 +754,50 @@ __global__ void k3d_write(K3DBuild a, const int* __restrict__ idx1, uint8_t* __r
   }
 }
 
-// exact Y_0, Y_1 from the plain codes and the same x digits, added as
-// D_0 += Y_0, D_1 += Y_1 - 2 Y_0 (linear, so column pieces add atomically;
-// the tensor-core pass left 0 in both rows). grid = (column pieces, RHS),
-// 16 columns per thread
-__global__ void k3d_rows01(const uint8_t* p0, const uint8_t* p1, int P, int sgn, int64_t n,
-                           int64_t ld, int64_t rows, const int8_t* __restrict__ B, int64_t ldb,
-                           long long* __restrict__ yacc) {
-  const int t = blockIdx.y;
-  const int64_t j0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 16;
-  long long s0 = 0, s1 = 0;
-  if (j0 < n) {
-    const uint4 g0 = *reinterpret_cast<const uint4*>(B + (0 * K3_NR + t) * ldb + j0);
-    const uint4 g1 = *reinterpret_cast<const uint4*>(B + (1 * K3_NR + t) * ldb + j0);
-    const uint4 g2 = *reinterpret_cast<const uint4*>(B + (2 * K3_NR + t) * ldb + j0);
-    const uint4 a0 = *reinterpret_cast<const uint4*>(p0 + j0);
-    const uint4 a1 = P > 1 ? *reinterpret_cast<const uint4*>(p1 + j0) : make_uint4(0, 0, 0, 0);
-    const uint4 b0 = rows > 1 ? *reinterpret_cast<const uint4*>(p0 + ld + j0) : make_uint4(0, 0, 0, 0);
-    const uint4 b1 = (rows > 1 && P > 1) ? *reinterpret_cast<const uint4*>(p1 + ld + j0)
-                                         : make_uint4(0, 0, 0, 0);
-    const uint32_t G0[4] = {g0.x, g0.y, g0.z, g0.w}, G1[4] = {g1.x, g1.y, g1.z, g1.w},
-                   G2[4] = {g2.x, g2.y, g2.z, g2.w}, A0[4] = {a0.x, a0.y, a0.z, a0.w},
-                   A1[4] = {a1.x, a1.y, a1.z, a1.w}, B0[4] = {b0.x, b0.y, b0.z, b0.w},
-                   B1[4] = {b1.x, b1.y, b1.z, b1.w};
-    const int sh = 32 - 8 * P;
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const int w = q >> 2, bb = 8 * (q & 3);
-      const long long X = (long long)(int8_t)(G0[w] >> bb) + 256LL * (int8_t)(G1[w] >> bb) +
-                          65536LL * (int8_t)(G2[w] >> bb);
-      uint32_t u0 = ((A0[w] >> bb) & 255u) | (((A1[w] >> bb) & 255u) << 8);
-      uint32_t u1 = ((B0[w] >> bb) & 255u) | (((B1[w] >> bb) & 255u) << 8);
-      const int32_t v0 = sgn ? ((int32_t)(u0 << sh) >> sh) : (int32_t)u0;
-      const int32_t v1 = sgn ? ((int32_t)(u1 << sh) >> sh) : (int32_t)u1;
-      s0 += (long long)v0 * X;
-      s1 += (long long)v1 * X;
-    }
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    atomicAdd((unsigned long long*)&yacc[(int64_t)t * rows], (unsigned long long)s0);
-    if (rows > 1)
-      atomicAdd((unsigned long long*)&yacc[(int64_t)t * rows + 1], (unsigned long long)(s1 - 2 * s0));
-  }
-}
+// ------------------------------------------------------------ k3_post
+// From the exact int64 row sums the tensor-core pass accumulated in yacc to
+// fp32 y; one cluster of K3Q_CL CTAs per right-hand side (grid (K3Q_CL, nrhs)),
+// each CTA a contiguous block of rows in tiles of K3Q_TILE. Global memory is
+// touched only by coalesced row-strided accesses; a padded shared-memory
+// transpose gives every thread K3Q_RPT consecutive rows for the scans.
+//  * DL: yacc holds D = E X for the second-order row residuals (+ k3_prep's
+//    rows 0/1 corrections). Y is the double prefix sum of D along rows: per
+//    tile two block scans (thread sums of d, then of the thread-local second
+//    prefix), each CTA publishes (sum D, sum z, length) in shared memory and
+//    folds its predecessors' triples (DSMEM) into its carry-in
+//    (composition of consecutive blocks A, B: sumZ = sumZ_A + sumZ_B +
+//    len_B sumD_A);
+//  * byte planes: yacc holds Y itself;
+//  * y = fl32(Y 10^-m 2^-e_t); columns whose x is inf/nan (k3_prep's list)
+//    are applied as the reference loop would (zero mantissas skipped): nan if
+//    any non-zero v_ij meets a nan or both infinite signs occur, else +-inf;
+//  * yacc is reset to zero behind the read, ready for the next apply's
+//    atomic K-split partials (no memset launch).
+constexpr int K3Q_CL = 16;             // non-portable cluster size (opt-in at launch)
+constexpr int K3Q_TPB = 256;
+constexpr int K3Q_RPT = 16;
+constexpr int K3Q_TILE = K3Q_TPB * K3Q_RPT;
+constexpr int K3Q_SMEM = K3Q_TILE + K3Q_TILE / 16;   // 8-byte words, one pad per 16
 
-// Y = double prefix sum of D along rows, exact in int64, in segments of
-// K3D_SEG rows: pass 1 gives per segment (sum D, sum z_local) with z_local the
-// segment-local first prefix; the carries (Z_in, Y_in) follow sequentially per
-// RHS; pass 2 rebuilds y_r = y_local + (r - r0 + 1) Z_in + Y_in and scales.
-constexpr int K3D_SEG = 1024;
+__device__ __forceinline__ int k3q_pad(int k) { return k + (k >> 4); }
 
-__device__ __forceinline__ long long k3d_block_incl(long long v, long long* sh) {
+struct K3Post {
+  long long* yacc;
+  int64_t rows, n, ld;
+  const uint8_t* planes[2];
+  int P, sgn;
+  const int* e;
+  double scale;
+  int* nf_count;
+  const int* nf_cols;
+  const long long* y01;
+  const float* x;
+  int64_t ldx;
+  float* y;
+  int64_t ldy;
+};
+
+__device__ __forceinline__ long long k3q_block_excl(long long v, long long* sh) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   long long inc = v;
 #pragma unroll
@@ -704,7 +808,7 @@ __device__ __forceinline__ long long k3d_block_incl(long long v, long long* sh) 
   if (lane == 31) sh[w] = inc;
   __syncthreads();
   if (w == 0) {
-    long long s = sh[lane];
+    long long s = lane < K3Q_TPB / 32 ? sh[lane] : 0;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const long long u = __shfl_up_sync(0xffffffffu, s, o);
@@ -713,86 +817,198 @@ __device__ __forceinline__ long long k3d_block_incl(long long v, long long* sh) 
     sh[lane] = s;
   }
   __syncthreads();
-  const long long r = inc + (w > 0 ? sh[w - 1] : 0);
+  const long long r = inc - v + (w > 0 ? sh[w - 1] : 0);
   __syncthreads();
   return r;
 }
 
-// grid = (segments, RHS), K3D_TPB threads x K3D_RPT consecutive rows each:
-// thread-local prefixes, then one block scan per prefix level
-constexpr int K3D_RPT = 4;
-constexpr int K3D_TPB = K3D_SEG / K3D_RPT;
-
-// d[] -> z[] (inclusive prefix over the segment) and yl[] (prefix of z)
-__device__ __forceinline__ void k3d_seg_prefix(const long long* d, long long* z, long long* yl,
-                                               long long* sh) {
-  long long c[K3D_RPT];
-  c[0] = d[0];
+// tile s (L valid rows) -> d[]: coalesced row-strided loads into padded
+// shared memory, then this thread's K3Q_RPT consecutive rows
+__device__ __forceinline__ void k3q_load(const K3Post& a, int t, int64_t s, int64_t L,
+                                         long long add0, long long add1, long long* d,
+                                         long long* sd) {
+  const long long* src = a.yacc + (int64_t)t * a.rows + s;
 #pragma unroll
-  for (int i = 1; i < K3D_RPT; ++i) c[i] = c[i - 1] + d[i];
-  const long long ze = k3d_block_incl(c[K3D_RPT - 1], sh) - c[K3D_RPT - 1];
+  for (int i = 0; i < K3Q_RPT; ++i) {
+    const int k = i * K3Q_TPB + threadIdx.x;
+    long long v = k < L ? src[k] : 0;
+    if (s + k == 0) v += add0;          // plan rows 0 and 1 (DL corrections; 0 otherwise)
+    if (s + k == 1) v += add1;
+    sd[k3q_pad(k)] = v;
+  }
+  __syncthreads();
 #pragma unroll
-  for (int i = 0; i < K3D_RPT; ++i) z[i] = ze + c[i];
-  long long w[K3D_RPT];
-  w[0] = z[0];
-#pragma unroll
-  for (int i = 1; i < K3D_RPT; ++i) w[i] = w[i - 1] + z[i];
-  const long long we = k3d_block_incl(w[K3D_RPT - 1], sh) - w[K3D_RPT - 1];
-#pragma unroll
-  for (int i = 0; i < K3D_RPT; ++i) yl[i] = we + w[i];
+  for (int i = 0; i < K3Q_RPT; ++i) d[i] = sd[k3q_pad(threadIdx.x * K3Q_RPT + i)];
+  __syncthreads();
 }
 
-__global__ void __launch_bounds__(K3D_TPB) k3d_seg_sums(const long long* __restrict__ yacc,
-                                                        int64_t rows, long long* __restrict__ seg) {
+// d[] -> the thread's exclusive block prefixes: ze (first prefix) and we
+// (second prefix, relative to the tile start); tile sums via the thread
+// holding the tile's last valid row
+__device__ __forceinline__ void k3q_scan(const long long* d, int64_t L, long long* sh,
+                                         long long* s_tile, long long& ze, long long& we,
+                                         long long& sD, long long& sZ) {
+  long long S = 0, C = 0;
+#pragma unroll
+  for (int i = 0; i < K3Q_RPT; ++i) { S += d[i]; C += S; }
+  ze = k3q_block_excl(S, sh);
+  const long long W = (long long)K3Q_RPT * ze + C;   // sum of the thread's second prefix
+  we = k3q_block_excl(W, sh);
+  const int64_t last = L - 1;
+  if ((int64_t)threadIdx.x == last / K3Q_RPT) {
+    const int il = (int)(last % K3Q_RPT);
+    long long cs = 0, cc = 0;
+#pragma unroll
+    for (int i = 0; i < K3Q_RPT; ++i) {
+      cs += d[i];
+      cc += ze + cs;
+      if (i == il) { s_tile[0] = ze + cs; s_tile[1] = we + cc; }
+    }
+  }
+  __syncthreads();
+  sD = s_tile[0];
+  sZ = s_tile[1];
+  __syncthreads();
+}
+
+// Y of the thread's rows (running prefixes from base_z / base_y) -> fp32 in
+// shared memory -> coalesced stores of y and zeros into yacc
+template <bool DL>
+__device__ __forceinline__ void k3q_store(const K3Post& a, int t, int64_t s, int64_t L,
+                                          const long long* d, long long base_z, long long base_y,
+                                          double sc, float* sy) {
+  long long z = base_z, yv = base_y;
+#pragma unroll
+  for (int i = 0; i < K3Q_RPT; ++i) {
+    long long Y;
+    if (DL) { z += d[i]; yv += z; Y = yv; } else { Y = d[i]; }
+    sy[k3q_pad(threadIdx.x * K3Q_RPT + i)] = (float)((double)Y * sc);
+  }
+  __syncthreads();
+  float* dst = a.y + (int64_t)t * a.ldy + s;
+  long long* acc = a.yacc + (int64_t)t * a.rows + s;
+#pragma unroll
+  for (int i = 0; i < K3Q_RPT; ++i) {
+    const int k = i * K3Q_TPB + threadIdx.x;
+    if (k < L) {
+      dst[k] = sy[k3q_pad(k)];
+      acc[k] = 0;
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ float k3q_nonfinite(const K3Post& a, int t, int64_t r, float v, int nf) {
+  bool isn = false, pos = false, neg = false;
+  for (int k = 0; k < nf; ++k) {
+    const int64_t j = a.nf_cols[(int64_t)t * a.n + k];
+    const int64_t off = r * a.ld + j;
+    uint32_t u = a.planes[0][off];
+    if (a.P > 1) u |= (uint32_t)a.planes[1][off] << 8;
+    const int sh = 32 - 8 * a.P;
+    const int32_t q = a.sgn ? ((int32_t)(u << sh) >> sh) : (int32_t)u;
+    if (q == 0) continue;
+    const float xv = a.x[(int64_t)t * a.ldx + j];
+    if (isnan(xv)) isn = true;
+    else if ((q < 0) != (xv < 0.0f)) neg = true;
+    else pos = true;
+  }
+  if (isn || (pos && neg)) return __int_as_float(0x7fc00000);
+  if (pos) return __int_as_float(0x7f800000);
+  if (neg) return __int_as_float(0xff800000);
+  return v;
+}
+
+// columns with inf/nan x (rare): after the CTA's rows are stored
+__device__ __forceinline__ void k3q_fix_nonfinite(const K3Post& a, int t, int64_t r0, int64_t r1,
+                                                  int nf) {
+  __syncthreads();
+  for (int64_t r = r0 + threadIdx.x; r < r1; r += K3Q_TPB) {
+    float* dst = a.y + (int64_t)t * a.ldy + r;
+    *dst = k3q_nonfinite(a, t, r, *dst, nf);
+  }
+}
+
+template <bool DL>
+__global__ void __launch_bounds__(K3Q_TPB, 4) k3_post(K3Post a) {
+  cg::cluster_group cl = cg::this_cluster();
+  __shared__ long long sd[K3Q_SMEM];
   __shared__ long long sh[32];
+  __shared__ long long s_tile[2];
+  __shared__ long long s_tot[3];
+  __shared__ long long s_carry[2];
+  float* sy = reinterpret_cast<float*>(sd);
   const int t = blockIdx.y;
-  const int64_t r0 = (int64_t)blockIdx.x * K3D_SEG + threadIdx.x * K3D_RPT;
-  long long d[K3D_RPT], z[K3D_RPT], yl[K3D_RPT];
-#pragma unroll
-  for (int i = 0; i < K3D_RPT; ++i) d[i] = r0 + i < rows ? yacc[(int64_t)t * rows + r0 + i] : 0;
-  k3d_seg_prefix(d, z, yl, sh);
-  if (threadIdx.x == K3D_TPB - 1) {
-    seg[((int64_t)t * gridDim.x + blockIdx.x) * 2 + 0] = z[K3D_RPT - 1];    // sum of D
-    seg[((int64_t)t * gridDim.x + blockIdx.x) * 2 + 1] = yl[K3D_RPT - 1];   // sum of z_local
+  const int c = (int)cl.block_rank();
+  const int64_t per = cdiv(a.rows, K3Q_CL);
+  const int64_t r0 = min(a.rows, (int64_t)c * per), r1 = min(a.rows, r0 + per);
+  const long long add0 = DL ? a.y01[2 * t] : 0, add1 = DL ? a.y01[2 * t + 1] : 0;
+  const double sc = ldexp(a.scale, -a.e[t]);
+  const int nf = a.nf_count[t];
+  long long d[K3Q_RPT];
+  if (!DL) {
+    for (int64_t s = r0; s < r1; s += K3Q_TILE) {
+      const int64_t L = min((int64_t)K3Q_TILE, r1 - s);
+      k3q_load(a, t, s, L, 0, 0, d, sd);
+      k3q_store<false>(a, t, s, L, d, 0, 0, sc, sy);
+    }
+    if (nf > 0) {
+      k3q_fix_nonfinite(a, t, r0, r1, nf);
+      cl.sync();                     // every CTA has read nf_count[t]
+      if (c == 0 && threadIdx.x == 0) a.nf_count[t] = 0;
+    }
+    return;
   }
-}
-
-// segment carries in place, (sum D, sum z) -> (Z_in, Y_in): one block per RHS,
-// one thread per segment (nseg <= K3D_SEG), two block scans:
-//   Z_in(k) = sum_{j<k} sumD_j,  Y_in(k) = sum_{j<k} (K3D_SEG Z_in(j) + sumz_j)
-__global__ void __launch_bounds__(K3D_SEG) k3d_seg_carry(long long* __restrict__ seg, int nseg) {
-  __shared__ long long sh[32];
-  const int t = blockIdx.x, k = threadIdx.x;
-  long long* p = seg + ((int64_t)t * nseg + k) * 2;
-  const long long sd = k < nseg ? p[0] : 0, sz = k < nseg ? p[1] : 0;
-  const long long zin = k3d_block_incl(sd, sh) - sd;
-  const long long term = (long long)K3D_SEG * zin + sz;
-  const long long yin = k3d_block_incl(term, sh) - term;
-  if (k < nseg) {
-    p[0] = zin;
-    p[1] = yin;
+  const bool one = r1 - r0 <= K3Q_TILE;          // the rows stay in registers
+  long long ze = 0, we = 0, sD = 0, sZ = 0;
+  long long SD = 0, SZ = 0;
+  for (int64_t s = r0; s < r1; s += K3Q_TILE) {
+    const int64_t L = min((int64_t)K3Q_TILE, r1 - s);
+    k3q_load(a, t, s, L, add0, add1, d, sd);
+    k3q_scan(d, L, sh, s_tile, ze, we, sD, sZ);
+    SZ += sZ + L * SD;
+    SD += sD;
   }
-}
-
-__global__ void __launch_bounds__(K3D_TPB) k3d_seg_apply(const long long* __restrict__ yacc,
-                                                         int64_t rows, const long long* __restrict__ seg,
-                                                         const int* __restrict__ e, double scale,
-                                                         float* __restrict__ y, int64_t ldy) {
-  __shared__ long long sh[32];
-  const int t = blockIdx.y;
-  const int64_t r0 = (int64_t)blockIdx.x * K3D_SEG + threadIdx.x * K3D_RPT;
-  long long d[K3D_RPT], z[K3D_RPT], yl[K3D_RPT];
-#pragma unroll
-  for (int i = 0; i < K3D_RPT; ++i) d[i] = r0 + i < rows ? yacc[(int64_t)t * rows + r0 + i] : 0;
-  k3d_seg_prefix(d, z, yl, sh);
-  const long long* c = seg + ((int64_t)t * gridDim.x + blockIdx.x) * 2;
-  const long long zin = c[0], yin = c[1];
-  const double sc = ldexp(scale, -e[t]);
-#pragma unroll
-  for (int i = 0; i < K3D_RPT; ++i) {
-    const long long Y = yl[i] + (long long)(threadIdx.x * K3D_RPT + i + 1) * zin + yin;
-    if (r0 + i < rows) y[(int64_t)t * ldy + r0 + i] = (float)((double)Y * sc);
+  if (threadIdx.x == 0) { s_tot[0] = SD; s_tot[1] = SZ; s_tot[2] = r1 - r0; }
+  cl.sync();
+  // lane r of warp 0 reads the triple of peer r < c (parallel DSMEM loads);
+  // lane 0 folds them in rank order
+  if (threadIdx.x < 32) {
+    long long pd = 0, pz = 0, pl = 0;
+    if ((int)threadIdx.x < c) {
+      const long long* p = cl.map_shared_rank(s_tot, (int)threadIdx.x);
+      pd = p[0];
+      pz = p[1];
+      pl = p[2];
+    }
+    long long zi = 0, yi = 0;
+    for (int r = 0; r < c; ++r) {
+      const long long d_ = __shfl_sync(0xffffffffu, pd, r);
+      const long long z_ = __shfl_sync(0xffffffffu, pz, r);
+      const long long l_ = __shfl_sync(0xffffffffu, pl, r);
+      yi += l_ * zi + z_;
+      zi += d_;
+    }
+    if (threadIdx.x == 0) { s_carry[0] = zi; s_carry[1] = yi; }
   }
+  k3_cluster_arrive_relaxed();     // this CTA is done reading its peers
+  __syncthreads();
+  long long Zin = s_carry[0], Yin = s_carry[1];
+  for (int64_t s = r0; s < r1; s += K3Q_TILE) {
+    const int64_t L = min((int64_t)K3Q_TILE, r1 - s);
+    if (!one) {
+      k3q_load(a, t, s, L, add0, add1, d, sd);
+      k3q_scan(d, L, sh, s_tile, ze, we, sD, sZ);
+    }
+    // row s + off + i: Z = Zin + ze + cs_i, Y = Yin + (off + i + 1) Zin + we + sum_{i'<=i} (ze + cs_i')
+    const int64_t off = (int64_t)threadIdx.x * K3Q_RPT;
+    k3q_store<true>(a, t, s, L, d, Zin + ze, Yin + off * Zin + we, sc, sy);
+    Yin += L * Zin + sZ;
+    Zin += sD;
+  }
+  if (nf > 0) k3q_fix_nonfinite(a, t, r0, r1, nf);
+  k3_cluster_wait();               // peers read s_tot through DSMEM until here
+  if (c == 0 && threadIdx.x == 0 && nf > 0) a.nf_count[t] = 0;   // every CTA read it above
 }
 
 // ------------------------------------------------------------ host side
@@ -826,6 +1042,29 @@ static int make_map_u8(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t
                    es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(INVOP_E_CUDA, "cuTensorMapEncodeTiled failed");
+  return INVOP_OK;
+}
+
+// k3_prep / k3_post run as clusters of 16 CTAs (non-portable size) per
+// right-hand side
+template <typename Kern, typename Arg>
+static int launch_cluster16(Kern kern, const Arg& arg, int nr, int threads, cudaStream_t s) {
+  static_assert(K3P_CL == 16 && K3Q_CL == 16, "cluster size");
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e != cudaSuccess) return cuda_fail(e, "cluster attribute");
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(16, (unsigned)nr);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 16;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  INVOP_CUDA(cudaLaunchKernelEx(&cfg, kern, arg));
   return INVOP_OK;
 }
 
@@ -908,11 +1147,10 @@ static int k3d_build(invop_plan* p, cudaStream_t s) {
   return INVOP_OK;
 }
 
-// the DL kernel serves a batched apply when its residual tiles were built,
-// the row prefix sum covers the rows (<= 1024 segments) and no INVOP_K3_CFG
-// variant selects a byte-plane configuration
+// the DL kernel serves a batched apply when its residual tiles were built and
+// no INVOP_K3_CFG variant selects a byte-plane configuration
 bool k3_uses_dl(const invop_plan* p) {
-  if (p->k3d_ready <= 0 || cdiv(p->rows, K3D_SEG) > K3D_SEG) return false;
+  if (p->k3d_ready <= 0) return false;
   int tiles = K3_TILES, stages = K3_STAGES;
   if (const char* v = getenv("INVOP_K3_CFG")) sscanf(v, "%d,%d", &tiles, &stages);
   return tiles == K3_TILES && stages == K3_STAGES;
@@ -966,44 +1204,32 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
   if (const char* v = getenv("INVOP_K3_SPLITS")) best = std::max(min_split, atoi(v));
   const int kpu = (int)cdiv(kblocks, best);
   const int splits = (int)cdiv(kblocks, kpu);   // no empty K ranges
-  // workspace: digits | exponents | int64 partial sums
-  size_t b_bytes = (size_t)K3_ND * K3_NR * ldb;
-  size_t e_off = round_up(b_bytes, 256);
-  size_t flag_off = e_off + 256;                          // e[64] ints | flag
-  size_t max_off = flag_off + 256;                        // max|x_t| bits [nrhs]
-  size_t acc_off = round_up(max_off + (size_t)nrhs * 4, 256);
+  // workspace: digits | exponents | non-finite counts | int64 row sums |
+  // non-finite column lists. The row sums are zero between applies (k3_post
+  // resets them behind its read), so K-split partials add atomically.
+  const size_t b_bytes = (size_t)K3_ND * K3_NR * ldb;
+  const size_t e_off = round_up(b_bytes, 256);
+  const size_t nfc_off = e_off + 256;
+  const size_t y01_off = nfc_off + 256;                   // [64][2] int64
+  const size_t acc_off = y01_off + 1024;
+  const size_t acc_bytes = (size_t)K3_NR * p->rows * 8;
+  const size_t nfl_off = round_up(acc_off + acc_bytes, 256);
+  const size_t ws_bytes = nfl_off + (size_t)K3_NR * p->n * 4;
   int krc = k3d_build(p, s);
   if (krc != INVOP_OK && krc != INVOP_E_UNSUPPORTED) return krc;
   const bool dl = k3_uses_dl(p);
-  size_t acc_bytes = splits > 1 ? (size_t)K3_NR * p->rows * 8 : 0;
-  if (dl)   // + segment carries of the row prefix sums
-    acc_bytes = (size_t)K3_NR * p->rows * 8 + (size_t)K3_NR * cdiv(p->rows, K3D_SEG) * 16;
-  int rc = ensure_scratch(&p->k3_ws, &p->k3_ws_bytes, acc_off + acc_bytes);
-  if (rc) return rc;
-  unsigned int* maxbits = (unsigned int*)((char*)p->k3_ws + max_off);
-  int* flag = (int*)((char*)p->k3_ws + flag_off);
-  // max|x_t| of every right-hand side in one launch. inf/nan in x needs the
-  // reference's zero-mantissa skip (fp32 masked kernels): the flag travels to
-  // page-locked host memory behind an event while the tensor-core apply is
-  // enqueued speculatively; the host reads it once the event fires (the GPU
-  // is busy with the apply meanwhile) and, if set, enqueues the masked apply,
-  // which overwrites y in stream order.
-  if (!p->k3_flag_host) {
-    INVOP_CUDA(cudaHostAlloc((void**)&p->k3_flag_host, 64, cudaHostAllocDefault));
-    INVOP_CUDA(cudaEventCreateWithFlags(&p->k3_flag_event, cudaEventDisableTiming));
+  if (p->k3_ws_bytes < ws_bytes || !p->k3_ws) {
+    int rc = ensure_scratch(&p->k3_ws, &p->k3_ws_bytes, ws_bytes);
+    if (rc) return rc;
+    INVOP_CUDA(cudaMemsetAsync(p->k3_ws, 0, ws_bytes, s));
   }
-  {
-    INVOP_CUDA(cudaMemsetAsync((char*)p->k3_ws + flag_off, 0, max_off - flag_off + (size_t)nrhs * 4, s));
-    dim3 g((unsigned)std::min<int64_t>(cdiv(p->n, 256), 64), (unsigned)nrhs);
-    k3_xmax<<<g, 256, 0, s>>>(x, p->n, ldx, maxbits, flag);
-    INVOP_LAUNCHED(1);
-    INVOP_CUDA(cudaMemcpyAsync(p->k3_flag_host, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
-    INVOP_CUDA(cudaEventRecord(p->k3_flag_event, s));
-  }
-  if (rc) return rc;
   int8_t* B = (int8_t*)p->k3_ws;
   int* e = (int*)((char*)p->k3_ws + e_off);
+  int* nfc = (int*)((char*)p->k3_ws + nfc_off);
+  long long* y01 = (long long*)((char*)p->k3_ws + y01_off);
   long long* yacc = (long long*)((char*)p->k3_ws + acc_off);
+  int* nfl = (int*)((char*)p->k3_ws + nfl_off);
+  int rc = INVOP_OK;
   if (!dl && !p->k3_maps_ready) {
     const int64_t rtiles = round_up(cdiv(p->rows, K3_BM), 2);   // row tiles (even)
     const int64_t tile_bytes = rtiles * (p->ld / K3_BK) * K3_A_TILE;
@@ -1027,17 +1253,23 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
   if (rc) return rc;
   for (int64_t t0 = 0; t0 < nrhs; t0 += K3_NR) {
     const int nr = (int)std::min<int64_t>(K3_NR, nrhs - t0);
-    k3_digits<<<(unsigned)std::min<int64_t>(cdiv((int64_t)K3_NR * ldb / 16, 256), sms * 16), 256, 0, s>>>(
-        x + t0 * ldx, p->n, ldx, nr, maxbits + t0, e, B, ldb);
-    INVOP_LAUNCHED(2);   // k3_digits + k3_batched
-    if (splits > 1) INVOP_CUDA(cudaMemsetAsync(yacc, 0, acc_bytes, s));
+    // 1. max|x_t| per right-hand side, exponents, digits, non-finite columns
+    K3Prep pr;
+    pr.x = x + t0 * ldx; pr.n = p->n; pr.ldx = ldx; pr.nrhs = nr;
+    pr.B = B; pr.ldb = ldb; pr.e = e; pr.nf_count = nfc; pr.nf_cols = nfl;
+    pr.planes[0] = p->planes[0];
+    pr.planes[1] = p->planes[p->P > 1 ? 1 : 0];
+    pr.ld = p->ld; pr.rows = p->rows; pr.P = p->P; pr.sgn = p->is_signed;
+    pr.rows01 = dl ? 1 : 0; pr.y01 = y01;
+    rc = launch_cluster16(k3_prep, pr, K3_NR, K3P_TPB, s);
+    if (rc) return rc;
+    // 2. the tensor-core pass: exact int64 row sums into yacc
     K3Args a;
     a.idx1 = p->k3d_idx1;
     a.rows = p->rows; a.n = p->n; a.P = p->P; a.hi_signed = p->is_signed;
     a.kblocks_total = kblocks; a.kblocks_per_unit = kpu; a.splits = splits;
     a.kb_stride = (int)(p->ld / K3_BK);
-    a.pairs = pairs; a.nrhs = nr; a.e = e; a.scale = p->scale;
-    a.y = y + t0 * ldy; a.ldy = ldy; a.yacc = yacc;
+    a.pairs = pairs; a.nrhs = nr; a.yacc = yacc;
     int grid = (int)std::min<int64_t>(sms, pairs * splits);
     const CUtensorMap* A0 = (const CUtensorMap*)(dl ? p->k3d_mapA[0] : p->k3_mapA[0]);
     const CUtensorMap* A1 = (const CUtensorMap*)(dl ? p->k3d_mapA[1] : p->k3_mapA[1]);
@@ -1053,28 +1285,21 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
       default: return fail(INVOP_E_VALUE, "unsupported INVOP_K3_CFG");
     }
     if (rc) return rc;
-    if (dl) {
-      // rows 0/1 from the codes, then the double prefix sum along rows
-      dim3 g01((unsigned)cdiv(cdiv(p->n, 16), 256), (unsigned)nr);
-      k3d_rows01<<<g01, 256, 0, s>>>(p->planes[0], p->planes[p->P > 1 ? 1 : 0], p->P, p->is_signed,
-                                     p->n, p->ld, p->rows, B, ldb, yacc);
-      const int nseg = (int)cdiv(p->rows, K3D_SEG);
-      long long* seg = yacc + (size_t)K3_NR * p->rows;
-      dim3 gs((unsigned)nseg, (unsigned)nr);
-      k3d_seg_sums<<<gs, K3D_TPB, 0, s>>>(yacc, p->rows, seg);
-      k3d_seg_carry<<<nr, (unsigned)round_up(nseg, 32), 0, s>>>(seg, nseg);
-      k3d_seg_apply<<<gs, K3D_TPB, 0, s>>>(yacc, p->rows, seg, e, p->scale, y + t0 * ldy, ldy);
-      INVOP_LAUNCHED(4);
-    } else if (splits > 1) {
-      int64_t tot = (int64_t)nr * p->rows;
-      k3_finalize<<<(unsigned)std::min<int64_t>(cdiv(tot, 256), sms * 8), 256, 0, s>>>(
-          yacc, p->rows, nr, e, p->scale, y + t0 * ldy, ldy);
-      INVOP_LAUNCHED(1);
-    }
+    // 3. rows 0/1 + double prefix (DL), scaling, non-finite columns, y
+    K3Post q;
+    q.yacc = yacc; q.rows = p->rows; q.n = p->n; q.ld = p->ld;
+    q.planes[0] = p->planes[0];
+    q.planes[1] = p->planes[p->P > 1 ? 1 : 0];
+    q.P = p->P; q.sgn = p->is_signed;
+    q.e = e; q.scale = p->scale;
+    q.nf_count = nfc; q.nf_cols = nfl; q.y01 = y01;
+    q.x = x + t0 * ldx; q.ldx = ldx;
+    q.y = y + t0 * ldy; q.ldy = ldy;
+    rc = dl ? launch_cluster16(k3_post<true>, q, nr, K3Q_TPB, s)
+            : launch_cluster16(k3_post<false>, q, nr, K3Q_TPB, s);
+    if (rc) return rc;
+    INVOP_LAUNCHED(3);   // k3_prep + k3_batched + k3_post
   }
-  INVOP_CHECK_LAUNCH("k3 epilogue");
-  INVOP_CUDA(cudaEventSynchronize(p->k3_flag_event));
-  if (*(volatile int*)p->k3_flag_host) return apply_fast_launch(p, x, ldx, y, ldy, nrhs, s);
   return INVOP_OK;
 }
 

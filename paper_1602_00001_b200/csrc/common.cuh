@@ -31,8 +31,6 @@ struct invop_plan {
   float* partial = nullptr; size_t partial_bytes = 0;
   int* counters = nullptr; size_t counters_n = 0;
   void* dev_x = nullptr; size_t dev_x_bytes = 0;
-  int* k3_flag_host = nullptr;      // K3: non-finite-x flag, page-locked
-  cudaEvent_t k3_flag_event = nullptr;
 
   void* dev_y = nullptr; size_t dev_y_bytes = 0;
   double* host_pinned = nullptr; size_t host_pinned_bytes = 0;

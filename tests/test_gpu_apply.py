@@ -480,7 +480,7 @@ def test_batched_tensor_core_apply(invop, O, rows, n, lo, hi, k):
     Yo = O.ordered_apply(mant, 4, X.astype(np.float32).astype(np.float64))
     for t in range(k):
         assert relerr(Y[t], Yo[t]) <= F32_TOL, t
-    # non-finite x goes through the masked fp32 kernels
+    # non-finite x: applied exactly per column by k3_post
     X2 = X.copy()
     X2[3, 5] = np.inf
     Y2 = dplan.apply_device(torch.tensor(X2, device="cuda", dtype=torch.float32), mode=0).cpu().numpy()
@@ -692,8 +692,8 @@ def test_k3_row_residuals(invop, O, rows, N, k, splits, monkeypatch):
     for t in (0, k // 2, k - 1):
         yo = O.ordered_apply(mant, 4, Xr[t])
         assert relerr(Y_dl[t], yo) <= F32_TOL
-    # non-finite x: the speculative tensor-core result is replaced by the
-    # masked fp32 apply (reference zero skip) in stream order
+    # non-finite x: those columns are applied exactly by k3_post (reference
+    # zero skip), the other right-hand sides are untouched
     monkeypatch.setenv("INVOP_K3_DL", "1")
     X2 = X.copy()
     X2[1, 7] = np.inf
@@ -704,6 +704,91 @@ def test_k3_row_residuals(invop, O, rows, N, k, splits, monkeypatch):
     assert relerr(Y2[1][fin], Yo2[fin]) <= F32_TOL
     yo0 = O.ordered_apply(mant, 4, Xr[0])
     assert relerr(Y2[0], yo0) <= F32_TOL
+
+
+def _nonfinite_match(y, yo, tol=F32_TOL):
+    assert np.array_equal(np.isnan(y), np.isnan(yo))
+    inf = np.isinf(yo)
+    assert np.array_equal(np.isinf(y), inf)
+    assert np.array_equal(np.sign(y[inf]), np.sign(yo[inf]))
+    fin = np.isfinite(yo)
+    if fin.any():
+        assert relerr(y[fin], yo[fin]) <= tol
+
+
+@pytest.mark.parametrize("dl", [True, False])
+def test_k3_nonfinite_columns(invop, O, dl, monkeypatch):
+    """inf/nan in x on the tensor-core route: those columns enter the digits as
+    0 and k3_post applies them exactly like the reference loop (zero
+    mantissas skipped: _native.pyx:32-46) — per right-hand side, on the device,
+    without touching the other right-hand sides."""
+    import torch
+
+    rows, N, k = 300, 4096, 24
+    rng = np.random.default_rng(4242 + dl)
+    if dl:
+        mant = np.abs(_smooth_rows(rng, rows, N, 10000, False))
+    else:
+        mant = rng.integers(-30000, 30001, size=(rows, N))
+    mant[::3, 5] = 0                    # column 5: zero in every third row
+    mant[1::2, 9] = 0
+    mant[:, 11] = 0                     # column 11: all zero
+    monkeypatch.setenv("INVOP_K3_DL", "1" if dl else "0")
+    dplan = invop._plan.DevicePlan.from_mantissas(mant, 4, row0=0, n=N)
+    X = rng.standard_normal((k, N)).astype(np.float32)
+    X[2, 5] = np.inf
+    X[3, 5], X[3, 9] = -np.inf, np.inf          # both signs where both are non-zero
+    X[4, 7] = np.nan
+    X[5, :] = np.nan                            # every column non-finite
+    X[6, 11] = np.nan                           # only meets zero mantissas
+    X[7, 5], X[7, 9] = np.inf, np.inf
+    Y = dplan.apply_device(torch.tensor(X, device="cuda"), mode=0).cpu().numpy()
+    assert dplan.apply_kernel(k) == ("k3_batched_dl" if dl else "k3_batched")
+    Xr = X.astype(np.float64)
+    for t in range(k):
+        _nonfinite_match(Y[t], O.ordered_apply(mant, 4, Xr[t]))
+    assert np.isfinite(Y[6]).all()
+    # the next apply (finite x) is unaffected: yacc was reset behind the read
+    X[:8] = rng.standard_normal((8, N))
+    Y2 = dplan.apply_device(torch.tensor(X, device="cuda"), mode=0).cpu().numpy()
+    for t in (2, 3, 5, 20):
+        assert relerr(Y2[t], O.ordered_apply(mant, 4, X[t].astype(np.float64))) <= F32_TOL
+
+
+def test_k3_apply_captures_in_cuda_graph(invop, O):
+    """The batched apply is stream-ordered with no host synchronisation (the
+    non-finite path stays on the device), so it can be captured in a CUDA
+    graph; replays equal eager applies."""
+    import torch
+
+    rows, N, k = 256, 8192, 64
+    rng = np.random.default_rng(99)
+    mant = np.abs(_smooth_rows(rng, rows, N, 10000, False))
+    dplan = invop._plan.DevicePlan.from_mantissas(mant, 4, row0=0, n=N)
+    X = torch.tensor(rng.standard_normal((k, N)), device="cuda", dtype=torch.float32)
+    Y = torch.empty((k, rows), device="cuda", dtype=torch.float32)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        dplan.apply_device(X, Y, mode=0)                 # warm-up: layout + workspace
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    eager = Y.clone()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        dplan.apply_device(X, Y, mode=0)
+    Y.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert Y.cpu().numpy().tobytes() == eager.cpu().numpy().tobytes()
+    X.copy_(torch.tensor(rng.standard_normal((k, N)), dtype=torch.float32))
+    X[1, 3] = float("inf")
+    g.replay()
+    torch.cuda.synchronize()
+    Xr = X.cpu().numpy().astype(np.float64)
+    Yc = Y.cpu().numpy()
+    for t in (0, 1, 63):
+        _nonfinite_match(Yc[t], O.ordered_apply(mant, 4, Xr[t]))
 
 
 def test_dl_chained_applies_are_stream_ordered(invop):
