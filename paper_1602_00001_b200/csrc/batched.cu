@@ -147,6 +147,13 @@ __device__ __forceinline__ void mma_commit_elect(uint32_t bar) {
           bar)
       : "memory");
 }
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    bar)
@@ -253,13 +260,22 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
           const uint32_t fb = smem_u32(&full[st]);
           if (DL) {
             int i1[TILES];
+#ifdef K3_PROBE_NOB
+            uint32_t mask = 0, bytes = TILES * K3_A_TILE;
+#else
             uint32_t mask = 0, bytes = TILES * K3_A_TILE + K3_ND * K3_B_TILE;
+#endif
 #pragma unroll
             for (int ti = 0; ti < TILES; ++ti) {
               i1[ti] = a.idx1[(int64_t)(row0 / K3_BM + ti) * a.kb_stride + kb];
               if (i1[ti] >= 0) { mask |= 1u << ti; bytes += K3_A_TILE; }
             }
             s_mask[st] = mask;
+#ifdef K3_PROBE_NOTMA
+            k3_arrive(fb);
+            if (++st == STAGES) { st = 0; ph ^= 1; }
+            continue;
+#endif
             k3_expect_tx(fb, bytes);
             if (P == 2 && TILES == 2) {
               // stage: [digit-0 tile 0][digit-0 tile 1][digit-1 tile 0][digit-1 tile 1]
@@ -288,7 +304,9 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
             }
           }
           // the three digit tiles are consecutive rows of B: one 192-row box
+#ifndef K3_PROBE_NOB
           tma_2d(sb + A_BYTES, &mapB, kb * K3_BK, 0, fb, pol_b);
+#endif
           if (++st == STAGES) { st = 0; ph ^= 1; }
         }
       }
@@ -316,6 +334,11 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
           const uint64_t dzero = desc_sw64(smem_u32(zero_tile));
           const uint32_t id_lo = idesc_i8(DL ? 1 : 0), id_hi = idesc_i8(DL ? 1 : a.hi_signed);
           const uint32_t mask = DL ? s_mask[st] : 0xffffffffu;
+#ifdef K3_PROBE_NOMMA
+          if (true) {
+            (void)dbase; (void)id_lo; (void)id_hi; (void)mask;
+          } else
+#endif
           if constexpr (DL && P == 2 && K3_ND == 3) {
             // straight-line issue with N = 192: the three digit tiles of B
             // are contiguous in shared memory and the weight classes of a
@@ -325,6 +348,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
             // MMAs of the N = 64 form; the tensor core re-reads A per MMA).
             // Class 3 is started by a zero tile at the unit's first K block.
             const uint32_t id0 = idesc_i8(1, K3_ND * K3_NR);
+#ifdef K3_MMA_ELECT_EACH
 #pragma unroll
             for (int kk = 0; kk < K3_BK / 32; ++kk) {
               const uint32_t cont = (i > 0 || kk > 0) ? 1u : 0u;
@@ -342,6 +366,32 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
                 }
               }
             }
+#else
+            // one elected thread issues the whole stage (no per-MMA election)
+            if (elect_one()) {
+#pragma unroll
+              for (int kk = 0; kk < K3_BK / 32; ++kk) {
+                const uint32_t cont = (i > 0 || kk > 0) ? 1u : 0u;
+                const uint64_t db = dbase + (uint64_t)((A_BYTES + kk * 32) >> 4);
+#pragma unroll
+                for (int ti = 0; ti < TILES; ++ti) {
+                  const uint32_t t0 = tmem + (uint32_t)(ti * NACC * K3_NR);
+                  const uint64_t a0 = dbase + (uint64_t)((ti * K3_A_TILE + kk * 32) >> 4);
+                  if (!cont)                                  // class 3 = A x 0
+                    mma_i8(t0 + 3 * K3_NR, a0, dzero + (uint64_t)((kk * 32) >> 4), id_hi, 0u);
+                  mma_i8(t0, a0, db, id0, cont);
+                  if ((mask >> ti) & 1u) {
+                    const uint64_t a1 = dbase + (uint64_t)(((TILES + ti) * K3_A_TILE + kk * 32) >> 4);
+                    mma_i8(t0 + 1 * K3_NR, a1, db, id0, 1u);
+                  }
+                }
+              }
+              mma_commit(smem_u32(&empty[st]));          // stage free once these MMAs complete
+            }
+            __syncwarp();
+            if (++st == STAGES) { st = 0; ph ^= 1; }
+            continue;
+#endif
           } else
 #pragma unroll
           for (int kk = 0; kk < K3_BK / 32; ++kk) {
@@ -370,12 +420,20 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
               }
             }
           }
+#ifdef K3_PROBE_NOMMA
+          if (lane == 0) k3_arrive(smem_u32(&empty[st]));
+#else
           mma_commit_elect(smem_u32(&empty[st]));   // stage free once these MMAs complete
+#endif
         }
         __syncwarp();
         if (++st == STAGES) { st = 0; ph ^= 1; }
       }
+#ifdef K3_PROBE_NOMMA
+      if (lane == 0) k3_arrive(smem_u32(&tfull));
+#else
       mma_commit_elect(smem_u32(&tfull));
+#endif
       __syncwarp();
     }
   } else {
@@ -386,6 +444,9 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
       const int64_t pair = u / a.splits;
       k3_wait(smem_u32(&tfull), (uint32_t)(ucount & 1));
       tc_fence_after();
+#ifdef K3_PROBE_NOEPI
+      if (true) {} else
+#endif
 #pragma unroll 1
       for (int ti = 0; ti < TILES; ++ti) {
         const int64_t row = pair * TILES * K3_BM + ti * K3_BM + q * 32 + lane;
@@ -424,6 +485,284 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// ------------------------------------------------------------ DL kernel on SM pairs
+// k3_dl2: the residual-tile apply with tcgen05.mma.cta_group::2 (config 5's
+// route). Probes of the one-SM kernel (k3_batched<2,2,5,true>) put it at
+// 0.92 ms while the TMA pipeline alone streams in 0.77 ms and the MMAs alone
+// (real operand addresses) take 0.66 ms: the two share the SM's shared
+// memory, and every N = 192 MMA re-reads the 6 KB x-digit operand for each
+// 128-row tile. On an SM pair one MMA covers M = 256 rows (128 per SM) and
+// each SM holds and reads only half of B (96 of the 192 digit rows), so the
+// B bytes an SM stages and the tensor core reads per row are halved, and the
+// leader issues one MMA where two were issued before.
+//   cluster (2,1,1); CTA r of cluster c owns row tiles 4q+2r, 4q+2r+1 of quad q
+//   per stage and CTA: [digit-0 pair 16 KB][digit-1 slot 0][digit-1 slot 1][B half 6 KB]
+//   A digit-1 slot is loaded when either SM's tile needs it (the SM without a
+//   digit-1 tile loads the all-zero tile stored after the compact ones), so
+//   one MMA serves both SMs.
+//   full[s] (leader): both producers arrive with their own transaction bytes;
+//   empty[s], tfull (each CTA): the leader's commit multicasts to both;
+//   tempty (leader): the epilogue warps of both CTAs arrive.
+constexpr int K3Q2_STAGES = 5;
+constexpr int K3Q2_BH = (K3_ND * K3_NR / 2) * K3_BK;          // 6 KB: half the digit rows
+constexpr int K3Q2_STAGE = 2 * K3_A_TILE + 2 * K3_A_TILE + K3Q2_BH;
+constexpr size_t K3Q2_SMEM = 1024 + (size_t)K3Q2_STAGES * K3Q2_STAGE + K3_B_TILE;
+
+__device__ __forceinline__ uint32_t k3_cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t k3_mapa(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void k3_cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void k3_expect_tx_cluster(uint32_t bar_cl, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(bar_cl),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void k3_arrive_cluster_relaxed(uint32_t bar_cl) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cl) : "memory");
+}
+__device__ __forceinline__ void k3_arrive_cluster(uint32_t bar_cl) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cl) : "memory");
+}
+__device__ __forceinline__ void tma_2d_pair(uint32_t dst, const CUtensorMap* map, int x, int y,
+                                            uint32_t bar_cl, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar_cl), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void mma_i8_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          bar),
+      "h"((uint16_t)0x3)
+      : "memory");
+}
+// kind::i8 instruction descriptor for the SM-pair MMA (M = 256)
+__host__ __device__ constexpr uint32_t idesc_i8_pair(int n) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+}
+
+struct K3PairArgs {
+  int64_t rows;
+  int kblocks_total, kb_stride, kblocks_per_unit, splits;
+  int64_t quads;            // ceil(rows / 512)
+  int nrhs;
+  long long* yacc;
+  const int* idx1;          // [rtiles][kbs] compact digit-1 index, -1 if absent
+  int zero1;                // index of the all-zero digit-1 tile
+};
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(K3_THREADS, 1)
+    k3_dl2(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapA1,
+           const __grid_constant__ CUtensorMap mapBh, K3PairArgs a) {
+  constexpr int NACC = 4;
+  extern __shared__ __align__(1024) unsigned char k3s[];
+  unsigned char* base = (unsigned char*)(((uintptr_t)k3s + 1023) & ~(uintptr_t)1023);
+  unsigned char* zero_tile = base + (size_t)K3Q2_STAGES * K3Q2_STAGE;
+  __shared__ __align__(8) uint64_t full[K3Q2_STAGES], empty[K3Q2_STAGES], tfull, tempty;
+  __shared__ uint32_t tmem_slot;
+  __shared__ uint32_t s_mask[K3Q2_STAGES];
+  for (int i = threadIdx.x; i < K3_B_TILE / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(zero_tile)[i] = make_uint4(0, 0, 0, 0);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  const uint32_t rank = k3_cluster_rank();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < K3Q2_STAGES; ++i) {
+      k3_mbar_init(smem_u32(&full[i]), 1);        // the leader's producer arrives for both CTAs
+      k3_mbar_init(smem_u32(&empty[i]), 1);
+    }
+    k3_mbar_init(smem_u32(&tfull), 1);
+    k3_mbar_init(smem_u32(&tempty), 8);           // 4 epilogue warps per CTA (leader's copy is used)
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        smem_u32(&tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  k3_cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+  const int64_t units = a.quads * a.splits;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (both CTAs)
+    if (lane == 0) {
+      uint64_t pol_a, pol_b;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_a));
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_b));
+      int st = 0;
+      uint32_t ph = 0;
+      int64_t it = 0;
+      for (int64_t u = cid; u < units; u += ncl) {
+        const int64_t quad = u / a.splits;
+        const int split = (int)(u - quad * a.splits);
+        const int kb0 = split * a.kblocks_per_unit;
+        const int kb1 = min(a.kblocks_total, kb0 + a.kblocks_per_unit);
+        const int64_t rt_own = quad * 4 + rank * 2, rt_peer = quad * 4 + (rank ^ 1) * 2;
+        const int nkb = kb1 - kb0, rot = cid % nkb;
+        for (int i = 0; i < nkb; ++i, ++it) {
+          const int kb = kb0 + (i + rot) % nkb;
+          if (it >= K3Q2_STAGES) k3_wait(smem_u32(&empty[st]), ph ^ 1);
+          const uint32_t sb = smem_u32(base + (size_t)st * K3Q2_STAGE);
+          const uint32_t fb = k3_mapa(smem_u32(&full[st]), 0);      // the leader's barrier
+          int own1[2];
+          uint32_t mask = 0;
+#pragma unroll
+          for (int ti = 0; ti < 2; ++ti) {
+            own1[ti] = a.idx1[(rt_own + ti) * a.kb_stride + kb];
+            const int peer1 = a.idx1[(rt_peer + ti) * a.kb_stride + kb];
+            if (own1[ti] >= 0 || peer1 >= 0) mask |= 1u << ti;
+          }
+          if (rank == 0) s_mask[st] = mask;
+#ifdef K3P2_NOTMA
+          if (rank == 0) k3_arrive(smem_u32(&full[st]));
+          if (++st == K3Q2_STAGES) { st = 0; ph ^= 1; }
+          continue;
+#endif
+          // the leader expects both CTAs' bytes (the peer's loads may land
+          // first: the transaction count may go negative until then)
+          if (rank == 0) k3_expect_tx(smem_u32(&full[st]), 2 * (2 * K3_A_TILE + K3Q2_BH + __popc(mask) * K3_A_TILE));
+          tma_2d_pair(sb, &mapA0, 0, (int)(k3d_tile0(rt_own, kb, a.kb_stride) * K3_BM), fb, pol_a);
+#pragma unroll
+          for (int ti = 0; ti < 2; ++ti)
+            if ((mask >> ti) & 1u)
+              tma_2d_pair(sb + (2 + ti) * K3_A_TILE, &mapA1, 0,
+                          (own1[ti] >= 0 ? own1[ti] : a.zero1) * K3_BM, fb, pol_a);
+          tma_2d_pair(sb + 4 * K3_A_TILE, &mapBh, kb * K3_BK, (int)rank * (K3_ND * K3_NR / 2), fb, pol_b);
+          if (++st == K3Q2_STAGES) { st = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (leader only)
+    if (rank == 0) {
+      const uint64_t dzero = desc_sw64(smem_u32(zero_tile));
+      const uint32_t id64 = idesc_i8_pair(K3_NR), id192 = idesc_i8_pair(K3_ND * K3_NR);
+      int st = 0;
+      uint32_t ph = 0;
+      int64_t ucount = 0;
+      for (int64_t u = cid; u < units; u += ncl, ++ucount) {
+        const int64_t quad = u / a.splits;
+        const int split = (int)(u - quad * a.splits);
+        const int kb0 = split * a.kblocks_per_unit;
+        const int kb1 = min(a.kblocks_total, kb0 + a.kblocks_per_unit);
+        if (ucount > 0) k3_wait(smem_u32(&tempty), (uint32_t)((ucount - 1) & 1));
+        tc_fence_after();
+        const int nkb = kb1 - kb0;
+        for (int i = 0; i < nkb; ++i) {
+          k3_wait(smem_u32(&full[st]), ph);
+          tc_fence_after();
+          const uint32_t mask = s_mask[st];
+          const uint64_t dbase = desc_sw64(smem_u32(base + (size_t)st * K3Q2_STAGE));
+#ifdef K3P2_NOMMA
+          if (lane == 0) { k3_arrive(smem_u32(&empty[st])); k3_arrive_cluster_relaxed(k3_mapa(smem_u32(&empty[st]), 1)); }
+          (void)mask; (void)dbase; (void)dzero; (void)id64; (void)id192;
+          __syncwarp();
+          if (++st == K3Q2_STAGES) { st = 0; ph ^= 1; }
+          continue;
+#endif
+          if (elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < K3_BK / 32; ++kk) {
+              const uint32_t cont = (i > 0 || kk > 0) ? 1u : 0u;
+              const uint64_t db = dbase + (uint64_t)((4 * K3_A_TILE + kk * 32) >> 4);
+#pragma unroll
+              for (int ti = 0; ti < 2; ++ti) {
+                const uint32_t t0 = tmem + (uint32_t)(ti * NACC * K3_NR);
+                const uint64_t a0 = dbase + (uint64_t)((ti * K3_A_TILE + kk * 32) >> 4);
+                if (!cont) mma_i8_pair(t0 + 3 * K3_NR, a0, dzero + (uint64_t)((kk * 32) >> 4), id64, 0u);
+                mma_i8_pair(t0, a0, db, id192, cont);
+                if ((mask >> ti) & 1u) {
+                  const uint64_t a1 = dbase + (uint64_t)(((2 + ti) * K3_A_TILE + kk * 32) >> 4);
+                  mma_i8_pair(t0 + 1 * K3_NR, a1, db, id192, 1u);
+                }
+              }
+            }
+            mma_commit_pair(smem_u32(&empty[st]));   // both CTAs' stage st is free
+          }
+          __syncwarp();
+          if (++st == K3Q2_STAGES) { st = 0; ph ^= 1; }
+        }
+#ifdef K3P2_NOMMA
+        if (lane == 0) { k3_arrive(smem_u32(&tfull)); k3_arrive_cluster(k3_mapa(smem_u32(&tfull), 1)); }
+#else
+        if (elect_one()) mma_commit_pair(smem_u32(&tfull));
+#endif
+        __syncwarp();
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (both CTAs)
+    const int q = warp & 3;
+    const uint32_t tempty_leader = k3_mapa(smem_u32(&tempty), 0);
+    int64_t ucount = 0;
+    for (int64_t u = cid; u < units; u += ncl, ++ucount) {
+      const int64_t quad = u / a.splits;
+      k3_wait(smem_u32(&tfull), (uint32_t)(ucount & 1));
+      tc_fence_after();
+#pragma unroll 1
+      for (int ti = 0; ti < 2; ++ti) {
+        const int64_t row = (quad * 4 + rank * 2 + ti) * K3_BM + q * 32 + lane;
+#pragma unroll 1
+        for (int c0 = 0; c0 < K3_NR; c0 += 16) {
+          int32_t r[NACC][16];
+#pragma unroll
+          for (int w = 0; w < NACC; ++w)
+            tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)((ti * NACC + w) * K3_NR + c0), r[w]);
+          tmem_wait_ld();
+          if (row < a.rows) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int t = c0 + j;
+              if (t >= a.nrhs) break;
+              long long v = 0;
+#pragma unroll
+              for (int w = 0; w < NACC; ++w) v += (long long)r[w][j] * (1LL << (8 * w));
+              if (a.splits == 1)
+                a.yacc[(int64_t)t * a.rows + row] = v;
+              else
+                atomicAdd((unsigned long long*)&a.yacc[(int64_t)t * a.rows + row], (unsigned long long)v);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) k3_arrive_cluster(tempty_leader);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  k3_cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
 }
 
@@ -1084,8 +1423,53 @@ static int launch_k3(const CUtensorMap& a0, const CUtensorMap& a1, const CUtenso
   return INVOP_OK;
 }
 
+// SM pairs that can be resident at once (a persistent grid must not exceed
+// it: TPC/GPC fragmentation leaves fewer than sms / 2 pairs)
+static int k3_pair_slots() {
+  static int slots = 0;
+  if (!slots) {
+    if (cudaFuncSetAttribute(k3_dl2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3Q2_SMEM) !=
+        cudaSuccess)
+      return num_sms() / 2;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(num_sms());
+    cfg.blockDim = dim3(K3_THREADS);
+    cfg.dynamicSmemBytes = K3Q2_SMEM;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, k3_dl2, &cfg) != cudaSuccess || n <= 0) n = num_sms() / 2;
+    slots = std::min(n, num_sms() / 2);
+  }
+  return slots;
+}
+
+static int launch_k3_dl2(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& bh,
+                         const K3PairArgs& args, int clusters, cudaStream_t s) {
+  cudaError_t e = cudaFuncSetAttribute(k3_dl2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3Q2_SMEM);
+  if (e != cudaSuccess) return cuda_fail(e, "k3_dl2 smem attribute");
+  k3_dl2<<<2 * clusters, K3_THREADS, K3Q2_SMEM, s>>>(a0, a1, bh, args);
+  INVOP_CHECK_LAUNCH("k3_dl2");
+  return INVOP_OK;
+}
+
 // residual tiles for the K3 DL path; declined (k3d_ready = -1) when some
 // residual needs a third digit or the layout would not be smaller
+// row tiles of the residual layout: a multiple of 4 (SM pairs take quads)
+static int64_t k3d_rtiles(const invop_plan* p) { return round_up(cdiv(p->rows, K3_BM), 4); }
+
+// one thread per (row-tile pair slot of a quad, K block): 1 if either SM's tile has digit 1
+__global__ void k3d_union(const int* __restrict__ idx1, int64_t rtiles, int64_t kbs,
+                          int64_t* __restrict__ n1u) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int c = 0;
+  if (t < rtiles / 2 * kbs) {
+    const int64_t slot = t / kbs, kb = t - slot * kbs;     // slot = quad * 2 + ti
+    const int64_t quad = slot >> 1, ti = slot & 1;
+    c = (idx1[(quad * 4 + ti) * kbs + kb] >= 0 || idx1[(quad * 4 + 2 + ti) * kbs + kb] >= 0) ? 1 : 0;
+  }
+  c = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd((unsigned long long*)n1u, (unsigned long long)c);
+}
+
 static int k3d_build(invop_plan* p, cudaStream_t s) {
   if (p->k3d_ready) return p->k3d_ready > 0 ? INVOP_OK : INVOP_E_UNSUPPORTED;
   p->k3d_ready = -1;
@@ -1098,7 +1482,7 @@ static int k3d_build(invop_plan* p, cudaStream_t s) {
   a.rows = p->rows;
   a.ld = p->ld;
   a.kbs = p->ld / K3_BK;
-  a.rtiles = round_up(cdiv(p->rows, K3_BM), 2);
+  a.rtiles = k3d_rtiles(p);
   const int64_t tiles = a.rtiles * a.kbs;
   int* tilew = nullptr;
   int64_t* n1d = nullptr;
@@ -1119,15 +1503,25 @@ static int k3d_build(invop_plan* p, cudaStream_t s) {
     INVOP_CUDA(cudaStreamSynchronize(s));
     if (tiles + p->k3d_n1 < (int64_t)p->P * tiles) {
       INVOP_CUDA(cudaMalloc(&p->k3d_tiles[0], (size_t)tiles * K3_A_TILE));
-      INVOP_CUDA(cudaMalloc(&p->k3d_tiles[1], (size_t)std::max<int64_t>(p->k3d_n1, 1) * K3_A_TILE));
+      // compact digit-1 tiles + one all-zero tile (the SM-pair kernel loads it
+      // for an SM whose tile has no digit-1 plane while its peer's has)
+      INVOP_CUDA(cudaMalloc(&p->k3d_tiles[1], (size_t)(p->k3d_n1 + 1) * K3_A_TILE));
       INVOP_CUDA(cudaMemsetAsync(p->k3d_tiles[0], 0, (size_t)tiles * K3_A_TILE, s));
+      INVOP_CUDA(cudaMemsetAsync(p->k3d_tiles[1] + (size_t)p->k3d_n1 * K3_A_TILE, 0, K3_A_TILE, s));
       k3d_write<<<(unsigned)cdiv(thr, 256), 256, 0, s>>>(a, p->k3d_idx1, p->k3d_tiles[0],
                                                          p->k3d_tiles[1]);
       rc = make_map_u8((CUtensorMap*)p->k3d_mapA[0], p->k3d_tiles[0], K3_BK,
                        (uint64_t)tiles * K3_BM, K3_BK, K3_BK, p->P == 2 ? 2 * K3_BM : K3_BM);
       if (!rc)
         rc = make_map_u8((CUtensorMap*)p->k3d_mapA[1], p->k3d_tiles[1], K3_BK,
-                         (uint64_t)std::max<int64_t>(p->k3d_n1, 1) * K3_BM, K3_BK, K3_BK, K3_BM);
+                         (uint64_t)(p->k3d_n1 + 1) * K3_BM, K3_BK, K3_BK, K3_BM);
+      // digit-1 MMAs the SM-pair kernel issues: (quad, K block, slot) where
+      // either SM's tile has a digit-1 plane
+      if (!rc) {
+        INVOP_CUDA(cudaMemsetAsync(n1d, 0, 8, s));
+        k3d_union<<<(unsigned)cdiv(a.rtiles / 2 * a.kbs, 256), 256, 0, s>>>(p->k3d_idx1, a.rtiles, a.kbs, n1d);
+        INVOP_CUDA(cudaMemcpyAsync(&p->k3d_n1u, n1d, 8, cudaMemcpyDeviceToHost, s));
+      }
       cudaError_t ce = cudaStreamSynchronize(s);
       if (!rc && ce != cudaSuccess) rc = cuda_fail(ce, "k3d build");
       if (!rc) p->k3d_ready = 1;
@@ -1146,6 +1540,9 @@ static int k3d_build(invop_plan* p, cudaStream_t s) {
   }
   return INVOP_OK;
 }
+
+// the residual tiles go to the SM-pair kernel (k3_dl2) unless INVOP_K3_PAIR=0
+static bool k3_pair_enabled() { return layout_flag("INVOP_K3_PAIR", true); }
 
 // the DL kernel serves a batched apply when its residual tiles were built and
 // no INVOP_K3_CFG variant selects a byte-plane configuration
@@ -1171,13 +1568,18 @@ int64_t k3_tensor_ops(const invop_plan* p, int64_t nrhs) {
   const int64_t kbs = p->ld / K3_BK;
   const int64_t rtiles = round_up(cdiv(p->rows, K3_BM), 2);
   const int64_t per_tile_kb = 2LL * K3_BM * (K3_ND * K3_NR) * K3_BK;   // one plane x all digits
-  if (k3_uses_dl(p)) return batches * per_tile_kb * (rtiles * kbs + p->k3d_n1);
+  if (k3_uses_dl(p)) {
+    const int64_t rt = k3d_rtiles(p);
+    // SM pairs: digit-1 MMAs wherever either SM's tile needs one (k3d_union)
+    if (k3_pair_enabled()) return batches * per_tile_kb * (rt * kbs + 2 * p->k3d_n1u);
+    return batches * per_tile_kb * (rt * kbs + p->k3d_n1);
+  }
   return batches * per_tile_kb * p->P * rtiles * kbs;
 }
 
 int64_t k3d_bytes(const invop_plan* p) {
   if (!k3_uses_dl(p)) return -1;   // DL kernel not used
-  const int64_t tiles = round_up(cdiv(p->rows, K3_BM), 2) * (p->ld / K3_BK);
+  const int64_t tiles = k3d_rtiles(p) * (p->ld / K3_BK);
   return (tiles + p->k3d_n1) * K3_A_TILE + tiles * 4;
 }
 
@@ -1188,22 +1590,31 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
   // variant: row tiles per unit (share B) and pipeline depth
   int tiles = K3_TILES, stages = K3_STAGES;
   if (const char* v = getenv("INVOP_K3_CFG")) sscanf(v, "%d,%d", &tiles, &stages);
-  const int64_t pairs = cdiv(p->rows, tiles * K3_BM);
   const int sms = num_sms();
+  int krc = k3d_build(p, s);
+  if (krc != INVOP_OK && krc != INVOP_E_UNSUPPORTED) return krc;
+  const bool dl = k3_uses_dl(p);
+  const bool pair = dl && k3_pair_enabled();
+  // work items: row-tile pairs on one SM, quads of row tiles on an SM pair
+  const int64_t pairs = pair ? cdiv(p->rows, 4 * K3_BM) : cdiv(p->rows, tiles * K3_BM);
+  const int slots = pair ? k3_pair_slots() : sms;
   // K splits: each unit spans <= 32768 columns; then pick the split count that
-  // best fills the SMs in whole waves
+  // best fills the SMs (SM pairs) in whole waves
   int min_split = (int)cdiv(kblocks, K3_KMAX / K3_BK);
   int best = min_split;
   double best_eff = -1.0;
   for (int sp = min_split; sp <= std::max(min_split, 16); ++sp) {
     int64_t units = pairs * sp;
-    double eff = (double)units / ((double)cdiv(units, sms) * sms);
+    double eff = (double)units / ((double)cdiv(units, slots) * slots);
     eff -= 0.005 * sp;   // atomics and partial tiles cost a little
     if (eff > best_eff + 1e-9) { best_eff = eff; best = sp; }
   }
   if (const char* v = getenv("INVOP_K3_SPLITS")) best = std::max(min_split, atoi(v));
   const int kpu = (int)cdiv(kblocks, best);
   const int splits = (int)cdiv(kblocks, kpu);   // no empty K ranges
+  if (getenv("INVOP_K3_DEBUG"))
+    fprintf(stderr, "k3: %s slots %d work %lld splits %d units %lld\n", pair ? "pair" : "single", slots,
+            (long long)pairs, splits, (long long)(pairs * splits));
   // workspace: digits | exponents | non-finite counts | int64 row sums |
   // non-finite column lists. The row sums are zero between applies (k3_post
   // resets them behind its read), so K-split partials add atomically.
@@ -1215,9 +1626,6 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
   const size_t acc_bytes = (size_t)K3_NR * p->rows * 8;
   const size_t nfl_off = round_up(acc_off + acc_bytes, 256);
   const size_t ws_bytes = nfl_off + (size_t)K3_NR * p->n * 4;
-  int krc = k3d_build(p, s);
-  if (krc != INVOP_OK && krc != INVOP_E_UNSUPPORTED) return krc;
-  const bool dl = k3_uses_dl(p);
   if (p->k3_ws_bytes < ws_bytes || !p->k3_ws) {
     int rc = ensure_scratch(&p->k3_ws, &p->k3_ws_bytes, ws_bytes);
     if (rc) return rc;
@@ -1249,7 +1657,8 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
     p->k3_maps_ready = 1;
   }
   CUtensorMap mapB;
-  rc = make_map_u8(&mapB, B, ldb, (uint64_t)K3_ND * K3_NR, ldb, K3_BK, K3_ND * K3_NR);
+  rc = pair ? make_map_u8(&mapB, B, ldb, (uint64_t)K3_ND * K3_NR, ldb, K3_BK, K3_ND * K3_NR / 2)
+            : make_map_u8(&mapB, B, ldb, (uint64_t)K3_ND * K3_NR, ldb, K3_BK, K3_ND * K3_NR);
   if (rc) return rc;
   for (int64_t t0 = 0; t0 < nrhs; t0 += K3_NR) {
     const int nr = (int)std::min<int64_t>(K3_NR, nrhs - t0);
@@ -1270,12 +1679,22 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
     a.kblocks_total = kblocks; a.kblocks_per_unit = kpu; a.splits = splits;
     a.kb_stride = (int)(p->ld / K3_BK);
     a.pairs = pairs; a.nrhs = nr; a.yacc = yacc;
-    int grid = (int)std::min<int64_t>(sms, pairs * splits);
+    int grid = (int)std::min<int64_t>(slots, pairs * splits);
     const CUtensorMap* A0 = (const CUtensorMap*)(dl ? p->k3d_mapA[0] : p->k3_mapA[0]);
     const CUtensorMap* A1 = (const CUtensorMap*)(dl ? p->k3d_mapA[1] : p->k3_mapA[1]);
     const int key = dl ? 999 : p->P * 100 + tiles * 10 + stages;
     switch (key) {
-      case 999: rc = launch_k3<2, 2, K3_DL_STAGES, true>(*A0, *A1, mapB, a, grid, s); break;
+      case 999:
+        if (pair) {
+          K3PairArgs pa;
+          pa.rows = p->rows; pa.kblocks_total = kblocks; pa.kb_stride = (int)(p->ld / K3_BK);
+          pa.kblocks_per_unit = kpu; pa.splits = splits; pa.quads = pairs; pa.nrhs = nr;
+          pa.yacc = yacc; pa.idx1 = p->k3d_idx1; pa.zero1 = (int)p->k3d_n1;
+          rc = launch_k3_dl2(*A0, *A1, mapB, pa, grid, s);
+        } else {
+          rc = launch_k3<2, 2, K3_DL_STAGES, true>(*A0, *A1, mapB, a, grid, s);
+        }
+        break;
       case 124: rc = launch_k3<1, 2, 4>(*A0, *A1, mapB, a, grid, s); break;
       case 116: rc = launch_k3<1, 1, 6>(*A0, *A1, mapB, a, grid, s); break;
       case 224: rc = launch_k3<2, 2, 4>(*A0, *A1, mapB, a, grid, s); break;

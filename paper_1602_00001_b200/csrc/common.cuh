@@ -58,6 +58,7 @@ struct invop_plan {
   uint8_t* k3d_tiles[2] = {nullptr, nullptr};
   int* k3d_idx1 = nullptr;
   int64_t k3d_n1 = 0;
+  int64_t k3d_n1u = 0;               // (quad, K block, slot) with a digit-1 tile on either SM
   int k3d_ready = 0;
 };
 
