@@ -230,6 +230,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  asm volatile("griddepcontrol.wait;" ::: "memory");       // programmatic dependent of k3_prep
   const uint32_t tmem = tmem_slot;
   const int64_t units = a.pairs * a.splits;
 
@@ -606,6 +607,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(K3_THREADS, 1)
   __syncthreads();
   k3_cluster_sync_all();
   tc_fence_after();
+  // launched as a programmatic dependent of k3_prep: the prologue above
+  // overlaps its tail; B (the x digits) and yacc are read after this
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint32_t tmem = tmem_slot;
   const int64_t units = a.quads * a.splits;
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
@@ -808,7 +812,7 @@ __global__ void k3_tile_planes(const uint8_t* __restrict__ in, int64_t rows, int
 //     loads beside the digits), reduced across the cluster, and k3_post adds
 //     the corrections D_0 += Y_0, D_1 += Y_1 - 2 Y_0 (y01[t]).
 constexpr int K3P_CL = 16;            // non-portable cluster size (opt-in at launch)
-constexpr int K3P_TPB = 256;
+constexpr int K3P_TPB = 128;          // 1024 CTAs of 128 threads: one wave at 64 registers
 constexpr int K3P_SWEEP = K3P_TPB * 16;
 
 struct K3Prep {
@@ -862,7 +866,11 @@ __device__ __forceinline__ void k3p_load16(const float* xt, int64_t jb, int64_t 
   }
 }
 
-__global__ void __launch_bounds__(K3P_TPB, 4) k3_prep(K3Prep a) {
+__global__ void __launch_bounds__(K3P_TPB, 8) k3_prep(K3Prep a) {
+  // programmatic dependent of the preceding grid (x may be its output; B, e
+  // and y01 are still read by the previous apply until it completes)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
   cg::cluster_group cl = cg::this_cluster();
   __shared__ float s_warp[K3P_TPB / 32];
   __shared__ long long s_w01[K3P_TPB / 32][2];
@@ -1270,6 +1278,8 @@ __device__ __forceinline__ void k3q_fix_nonfinite(const K3Post& a, int t, int64_
 
 template <bool DL>
 __global__ void __launch_bounds__(K3Q_TPB, 4) k3_post(K3Post a) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");       // the tensor-core pass is complete
+  asm volatile("griddepcontrol.launch_dependents;");
   cg::cluster_group cl = cg::this_cluster();
   __shared__ long long sd[K3Q_SMEM];
   __shared__ long long sh[32];
@@ -1384,25 +1394,28 @@ static int make_map_u8(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t
   return INVOP_OK;
 }
 
-// k3_prep / k3_post run as clusters of 16 CTAs (non-portable size) per
-// right-hand side
+// k3_prep / k3_post run as one cluster of CL CTAs per right-hand side
+// (CL = 16 is a non-portable size, opted in here)
 template <typename Kern, typename Arg>
-static int launch_cluster16(Kern kern, const Arg& arg, int nr, int threads, cudaStream_t s) {
-  static_assert(K3P_CL == 16 && K3Q_CL == 16, "cluster size");
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  if (e != cudaSuccess) return cuda_fail(e, "cluster attribute");
+static int launch_cluster(Kern kern, const Arg& arg, int nr, int threads, int cl, cudaStream_t s) {
+  if (cl > 8) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return cuda_fail(e, "cluster attribute");
+  }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(16, (unsigned)nr);
+  cfg.gridDim = dim3((unsigned)cl, (unsigned)nr);
   cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = 16;
+  at[0].val.clusterDim.x = (unsigned)cl;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   INVOP_CUDA(cudaLaunchKernelEx(&cfg, kern, arg));
   return INVOP_OK;
 }
@@ -1446,8 +1459,17 @@ static int launch_k3_dl2(const CUtensorMap& a0, const CUtensorMap& a1, const CUt
                          const K3PairArgs& args, int clusters, cudaStream_t s) {
   cudaError_t e = cudaFuncSetAttribute(k3_dl2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3Q2_SMEM);
   if (e != cudaSuccess) return cuda_fail(e, "k3_dl2 smem attribute");
-  k3_dl2<<<2 * clusters, K3_THREADS, K3Q2_SMEM, s>>>(a0, a1, bh, args);
-  INVOP_CHECK_LAUNCH("k3_dl2");
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * clusters);
+  cfg.blockDim = dim3(K3_THREADS);
+  cfg.dynamicSmemBytes = K3Q2_SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  INVOP_CUDA(cudaLaunchKernelEx(&cfg, k3_dl2, a0, a1, bh, args));
   return INVOP_OK;
 }
 
@@ -1670,7 +1692,7 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
     pr.planes[1] = p->planes[p->P > 1 ? 1 : 0];
     pr.ld = p->ld; pr.rows = p->rows; pr.P = p->P; pr.sgn = p->is_signed;
     pr.rows01 = dl ? 1 : 0; pr.y01 = y01;
-    rc = launch_cluster16(k3_prep, pr, K3_NR, K3P_TPB, s);
+    rc = launch_cluster(k3_prep, pr, K3_NR, K3P_TPB, K3P_CL, s);
     if (rc) return rc;
     // 2. the tensor-core pass: exact int64 row sums into yacc
     K3Args a;
@@ -1714,8 +1736,8 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
     q.nf_count = nfc; q.nf_cols = nfl; q.y01 = y01;
     q.x = x + t0 * ldx; q.ldx = ldx;
     q.y = y + t0 * ldy; q.ldy = ldy;
-    rc = dl ? launch_cluster16(k3_post<true>, q, nr, K3Q_TPB, s)
-            : launch_cluster16(k3_post<false>, q, nr, K3Q_TPB, s);
+    rc = dl ? launch_cluster(k3_post<true>, q, nr, K3Q_TPB, K3Q_CL, s)
+            : launch_cluster(k3_post<false>, q, nr, K3Q_TPB, K3Q_CL, s);
     if (rc) return rc;
     INVOP_LAUNCHED(3);   // k3_prep + k3_batched + k3_post
   }
