@@ -594,6 +594,7 @@ struct OrdArgs {
   const uint8_t* planes[8];
   int64_t rows, n, ld;
   double scale;
+  double neg_scale52;   // -(2^52 * scale), exact
   const double* x;
   int64_t ldx;
   double* y;
@@ -755,13 +756,22 @@ __global__ void __launch_bounds__(128) k2_ordered(OrdArgs a) {
             }
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-              double v;
-              if (SIGNED)   // 2^52 + 2^51 + (s + 2^31) - (2^52 + 2^51 + 2^31)
-                v = __dadd_rn(__hiloint2double(0x43380000, (int)((uint32_t)uv[i] ^ 0x80000000u)),
-                              -6755401588539392.0);
-              else          // 2^52 + u - 2^52
-                v = __dadd_rn(__hiloint2double(0x43300000, uv[i]), -4503599627370496.0);
-              d[4 * wd + i] = __dmul_rn(v, a.scale);
+              // fl(|v| * 10^-m) in ONE fp64 operation: V = 2^52 + |v| is built
+              // from bits, and fma(V, s, -2^52 s) = round((2^52 + |v|) s - 2^52 s)
+              // = round(|v| s) exactly, because 2^52 s is exact (a power-of-two
+              // multiple of the double s). The sign is applied to the rounded
+              // coefficient (rounding to nearest is sign-symmetric), as the
+              // reference applies it to its products (_native.pyx:43-46).
+              if (SIGNED) {
+                const int32_t sv = uv[i];
+                const int32_t sm = sv >> 31;
+                const uint32_t av = (uint32_t)((sv ^ sm) - sm);
+                const double c = __fma_rn(__hiloint2double(0x43300000, (int)av), a.scale, a.neg_scale52);
+                d[4 * wd + i] = __hiloint2double(__double2hiint(c) ^ (int)((uint32_t)sm & 0x80000000u),
+                                                 __double2loint(c));
+              } else {
+                d[4 * wd + i] = __fma_rn(__hiloint2double(0x43300000, uv[i]), a.scale, a.neg_scale52);
+              }
             }
           }
         } else {
@@ -840,11 +850,15 @@ int apply_ordered_launch(const invop_plan* p, const double* x, int64_t ldx, doub
     OrdArgs a;
     for (int b = 0; b < 8; ++b) a.planes[b] = p->planes[b < p->P ? b : 0];
     a.rows = p->rows; a.n = p->n; a.ld = p->ld; a.scale = p->scale;
+    a.neg_scale52 = -ldexp(p->scale, 52);
     a.x = x + k0 * ldx; a.ldx = ldx;
     a.y = y + k0 * ldy; a.ldy = ldy;
     a.accumulate = accumulate ? 1 : 0;
     int rc;
-    switch (p->P * 2 + p->is_signed) {
+    // non-negative codes in signed planes decode identically as unsigned
+    // (the cheaper coefficient path)
+    const int sgn = p->is_signed && p->min_val < 0 ? 1 : 0;
+    switch (p->P * 2 + sgn) {
       case 2: rc = launch_ord_p<1, false>(a, KR, s); break;
       case 3: rc = launch_ord_p<1, true>(a, KR, s); break;
       case 4: rc = launch_ord_p<2, false>(a, KR, s); break;
