@@ -571,8 +571,9 @@ def run_ours(args, world, rank, local):
             "ordered_fp64": {"value": k * 1e3 / ord_ms, "unit": UNIT, "kernel_ms": ord_ms,
                              "operator_bytes": ord_bytes,
                              "achieved_gbs": (ord_bytes + k * N * 8 + k * rows * 8) / (ord_ms * 1e-3) / 1e9,
-                             "note": "k2_ordered, bitwise equal to the reference apply; bytes = the "
-                                     "byte planes it streams"},
+                             "kernel": L.lib.invop_apply_kernel(h, k, L.MODE_ORDERED).decode(),
+                             "note": "bitwise equal to the reference apply; bytes = the byte planes "
+                                     "it streams"},
             "fp32_vs_fp64_relerr": err,
             "setup_s": {"factor": t_factor, "construct_and_encode": t_setup - t_factor},
             "op_counters": {"multiplications": mults, "additions": adds},

@@ -6,7 +6,7 @@ reference package `invop` (/root/reference/pkg/src/invop/__init__.py:10-59).
     q = invop.quantize(invop.invert(op), digits)      # device construct + K1
     plan = invop.build_plan(q)                          # compressed device layout
     y, counters = invop.apply(plan, x)                  # K2, bitwise == reference
-    y32, _ = invop.apply(plan, x, precision="f32")      # K2 fp32 grouped sum
+    y32, _ = invop.apply(plan, x, precision="f32")      # K2 fp32 I/O, exact integer sums
 
 All arithmetic runs in libinvop_b200.so (CUDA, sm_100a) through a C ABI
 (include/invop_b200.h); importing the package without the built library

@@ -14,10 +14,16 @@ exactly like the reference and scatters them into codes on the device.
 
 `apply(plan, x)` defaults to the reference contract: fp64, every output row
 accumulated in ascending column order, bitwise equal to the reference's
-`apply` and `apply_naive_quantized`. `precision="f32"` selects the fp32
-grouped-sum kernel (sum of integer mantissas times x, one multiplication by
-10^-m per row). Device tensors in give device tensors out, without a host
-synchronisation.
+`apply` and `apply_naive_quantized`. `precision="f32"` selects the fp32 I/O kernels,
+which compute every row as an EXACT integer dot product of the mantissas with
+x in 23-bit fixed point (one multiplication by 10^-m 2^-e per row). Exact
+integer sums make the reference's grouping by distinct |mantissa| (one
+multiplication per group, the paper's operation-count argument) unnecessary
+for accuracy, and on the GPU a multiply costs no more than the add it would
+save, so the device never groups: the `OpCounters` returned are the
+reference's PLANNED counts (G distinct values per column, E entries), computed
+on the device from the codes, not operations the kernels executed. Device
+tensors in give device tensors out, without a host synchronisation.
 """
 
 from __future__ import annotations
@@ -199,7 +205,8 @@ def apply(plan, x, *, precision: str = "f64") -> tuple:
     """Execute the plan on x. Returns (y, OpCounters).
 
     precision="f64" (default): bitwise equal to the reference apply.
-    precision="f32": fp32 grouped-sum kernel (max relative error ~1e-6).
+    precision="f32": fp32 I/O, exact integer row sums (max relative error ~1e-6).
+    The counters are the reference's planned counts (applyplan.py:92-98).
     x may be a host vector (numpy / list; result is a float64 numpy array,
     like the reference) or a CUDA tensor (result stays on the device).
     """

@@ -127,7 +127,7 @@ extern "C" const char* invop_apply_kernel(const invop_plan* p, int64_t nrhs, int
   if (!p) return "";
   if (mode == INVOP_MODE_ORDERED) return "k2_ordered";
   switch (fast_route(p, nrhs)) {
-    case ROUTE_K3: return k3_uses_dl(p) ? "k3_batched_dl" : "k3_batched";
+    case ROUTE_K3: return k3_uses_pair(p) ? "k3_dl2" : (k3_uses_dl(p) ? "k3_batched_dl" : "k3_batched");
     case ROUTE_DL: return "k2_dl";
     case ROUTE_HL: return "k2_hl";
     default: return stream_selected(p, nrhs) ? "k2_stream" : "k2_fast";
@@ -282,15 +282,16 @@ extern "C" int invop_apply_host(invop_plan* p, const double* x, double* y, int64
     int rc = ensure_scratch(&p->dev_x, &p->dev_x_bytes, xb + 64);
     if (rc) return rc;
     void* xdev = nullptr;
-    const bool pdl = host_alias(x, &xdev);
-    if (pdl) {
+    // x pulled by a kernel (the apply below is launched as its programmatic
+    // dependent, like every k2_dl launch) or copied by the copy engine
+    if (host_alias(x, &xdev)) {
       k_pull_x<<<(unsigned)std::min<int64_t>(cdiv(p->n, 512), 64), 256, 0, s>>>(
           (const double*)xdev, (double*)p->dev_x, p->n);
       INVOP_LAUNCHED(1);
     } else {
       INVOP_CUDA(cudaMemcpyAsync(p->dev_x, x, xb, cudaMemcpyHostToDevice, s));
     }
-    rc = apply_dl_launch(p, p->dev_x, ydev, true, s, pdl);
+    rc = apply_dl_launch(p, p->dev_x, ydev, true, s);
     if (rc == INVOP_OK) {
       INVOP_CUDA(cudaStreamSynchronize(s));
       return INVOP_OK;

@@ -1575,6 +1575,9 @@ bool k3_uses_dl(const invop_plan* p) {
   return tiles == K3_TILES && stages == K3_STAGES;
 }
 
+// the residual-tile apply runs on SM pairs (k3_dl2)
+bool k3_uses_pair(const invop_plan* p) { return k3_uses_dl(p) && k3_pair_enabled(); }
+
 // lazily built layouts of the batched apply (DL residual tiles)
 int k3_prepare(invop_plan* p, cudaStream_t s) {
   const int rc = k3d_build(p, s);

@@ -113,12 +113,12 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
                          int64_t nrhs, cudaStream_t s);
 int64_t k3d_bytes(const invop_plan* p);
 bool k3_uses_dl(const invop_plan* p);
+bool k3_uses_pair(const invop_plan* p);
 int64_t k3_tensor_ops(const invop_plan* p, int64_t nrhs);
 int k3_prepare(invop_plan* p, cudaStream_t s);
 int hl_build(invop_plan* p, cudaStream_t s);
 int dl_build(invop_plan* p, cudaStream_t s);
-int apply_dl_launch(invop_plan* p, const void* x, void* y, bool f64io, cudaStream_t s,
-                    bool pdl = false);
+int apply_dl_launch(invop_plan* p, const void* x, void* y, bool f64io, cudaStream_t s);
 int apply_hl_launch(invop_plan* p, const float* x, float* y, cudaStream_t s);
 int apply_ordered_launch(const invop_plan* p, const double* x, int64_t ldx, double* y,
                          int64_t ldy, int64_t nrhs, cudaStream_t s, bool accumulate = false);

@@ -780,7 +780,7 @@ static cudaError_t dl_launch(const DlArgs& a, int grid, size_t smem, bool pdl, c
   return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
-int apply_dl_launch(invop_plan* p, const void* x, void* y, bool f64io, cudaStream_t s, bool pdl) {
+int apply_dl_launch(invop_plan* p, const void* x, void* y, bool f64io, cudaStream_t s) {
   DlArgs a;
   a.data = p->dl_data;
   a.uoff = p->dl_uoff;

@@ -389,7 +389,7 @@ def test_config5_full_size(invop, O):
     Yo32 = O.ordered_apply(dev_mant, cfg.digits, Xr)             # [64, len(rows)]
     Xt = torch.tensor(X, device="cuda", dtype=torch.float32)
     Y = dplan.apply_device(Xt, mode=0).cpu().numpy()
-    assert dplan.apply_kernel(64) == "k3_batched_dl"
+    assert dplan.apply_kernel(64) == "k3_dl2"
     for t in range(64):
         assert relerr(Y[t][rows], Yo32[t]) <= F32_TOL, t
     for t in (0, 31, 63):
@@ -682,12 +682,18 @@ def test_k3_row_residuals(invop, O, rows, N, k, splits, monkeypatch):
         monkeypatch.setenv("INVOP_K3_SPLITS", str(splits))
     monkeypatch.setenv("INVOP_K3_DL", "1")
     Y_dl = dplan.apply_device(Xt, mode=0).cpu().numpy()
-    assert dplan.apply_kernel(k) == "k3_batched_dl"
+    assert dplan.apply_kernel(k) == "k3_dl2"                     # SM pairs (default)
+    monkeypatch.setenv("INVOP_K3_PAIR", "0")
+    Y_one = dplan.apply_device(Xt, mode=0).cpu().numpy()
+    assert dplan.apply_kernel(k) == "k3_batched_dl"              # one SM per row-tile pair
+    monkeypatch.delenv("INVOP_K3_PAIR")
     dplan2 = invop._plan.DevicePlan.from_mantissas(mant, 4, row0=0, n=N)
     monkeypatch.setenv("INVOP_K3_DL", "0")
     Y_pl = dplan2.apply_device(Xt, mode=0).cpu().numpy()
     assert dplan2.apply_kernel(k) == "k3_batched"
+    # exact integer sums: the three routes give the same bits
     assert Y_dl.tobytes() == Y_pl.tobytes()
+    assert Y_one.tobytes() == Y_pl.tobytes()
     Xr = X.astype(np.float32).astype(np.float64)
     for t in (0, k // 2, k - 1):
         yo = O.ordered_apply(mant, 4, Xr[t])
@@ -743,7 +749,7 @@ def test_k3_nonfinite_columns(invop, O, dl, monkeypatch):
     X[6, 11] = np.nan                           # only meets zero mantissas
     X[7, 5], X[7, 9] = np.inf, np.inf
     Y = dplan.apply_device(torch.tensor(X, device="cuda"), mode=0).cpu().numpy()
-    assert dplan.apply_kernel(k) == ("k3_batched_dl" if dl else "k3_batched")
+    assert dplan.apply_kernel(k) == ("k3_dl2" if dl else "k3_batched")
     Xr = X.astype(np.float64)
     for t in range(k):
         _nonfinite_match(Y[t], O.ordered_apply(mant, 4, Xr[t]))

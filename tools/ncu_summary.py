@@ -14,6 +14,14 @@ KEYS = [
     "launch__grid_size", "launch__block_size", "smsp__inst_executed.sum",
     "smsp__issue_active.avg.pct_of_peak_sustained_active",
     "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "lts__t_bytes.sum", "lts__t_sectors_srcunit_tex_op_read.sum",
+    "lts__t_sectors_srcunit_tex.avg.pct_of_peak_sustained_elapsed",
+    "sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_active",
+    "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+    "sm__inst_executed_pipe_tensor_subpipe_imma.sum",
+    "l1tex__data_bank_reads.avg.pct_of_peak_sustained_elapsed",
+    "l1tex__data_bank_writes.avg.pct_of_peak_sustained_elapsed",
+    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
 ]
 
 
@@ -22,12 +30,14 @@ def main():
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True, check=True).stdout
     r = list(csv.reader(raw.splitlines()))
-    h, units, v = r[0], r[1], r[2]
+    h, units = r[0], r[1]
     print(title)
-    for k in KEYS:
-        if k in h:
-            i = h.index(k)
-            print("%-64s %s %s" % (k, v[i], units[i]))
+    for v in r[2:]:
+        for k in KEYS:
+            if k in h and v[h.index(k)] not in ("", "n/a"):
+                i = h.index(k)
+                print("%-64s %s %s" % (k, v[i], units[i]))
+        print()
     stalls = {}
     for i, k in enumerate(h):
         p = "smsp__pcsamp_warps_issue_stalled_"
