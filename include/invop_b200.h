@@ -148,7 +148,11 @@ int invop_plan_csc(invop_plan* plan, int64_t* col_ptr, int64_t* group_abs_mantis
    applyplan.py:175-191, _native.pyx:15-49).
    x: device [nrhs x n] (ldx), y: device [nrhs x rows] (ldy), both of `dtype`.
    mode INVOP_MODE_ORDERED requires dtype INVOP_F64.
-   y is overwritten (the reference zero-fills then accumulates, :181). */
+   y is overwritten (the reference zero-fills then accumulates, :181).
+   The first call on a plan builds its lazily created layouts (row residuals,
+   tensor-core tiles) and synchronises; every later call is stream-ordered,
+   asynchronous and capturable in a CUDA graph — including the tensor-core
+   route with inf/nan in x (the zero-mantissa skip is applied on the device). */
 int invop_apply(const invop_plan* plan, const void* x, int64_t ldx, void* y, int64_t ldy,
                 int64_t nrhs, int dtype, int mode, void* stream);
 
@@ -179,7 +183,8 @@ int invop_plan_apply_bytes(invop_plan* plan, int64_t nrhs, int mode, int64_t* by
 int invop_plan_tensor_ops(invop_plan* plan, int64_t nrhs, int mode, int64_t* ops, void* stream);
 
 /* Name of the kernel an apply of `nrhs` right-hand sides in `mode` launches
-   ("k2_hl", "k2_stream", "k2_fast", "k3_batched", "k2_ordered", ...), for
+   ("k2_dl", "k2_hl", "k2_stream", "k2_fast", "k3_dl2", "k3_batched_dl",
+   "k3_batched", "k2_ordered"), for
    benchmark labels; static string, "" for a NULL plan. */
 const char* invop_apply_kernel(const invop_plan* plan, int64_t nrhs, int mode);
 
