@@ -188,6 +188,15 @@ int invop_plan_tensor_ops(invop_plan* plan, int64_t nrhs, int mode, int64_t* ops
    benchmark labels; static string, "" for a NULL plan. */
 const char* invop_apply_kernel(const invop_plan* plan, int64_t nrhs, int mode);
 
+/* The reference's grouped apply as written (_native.pyx:15-49) on device CSC
+   tables (invop_plan_csc): one multiplication per (column, distinct value),
+   an fp64 atomic add per entry into y (zeroed first; add order differs from
+   the reference, so NOT bitwise). A design comparison, not an apply route:
+   it streams 16 B per group + 5 B per entry. All pointers are device memory. */
+int invop_apply_grouped_csc(int64_t n, const int64_t* col_ptr, const double* group_coeff,
+                            const int64_t* group_ptr, const int32_t* entry_rows,
+                            const int8_t* entry_signs, const double* x, double* y, void* stream);
+
 /* Row-sharded multi-GPU apply (new — the reference is one
    process). Each rank holds the plan of its rows [row_offsets[rank],
    row_offsets[rank+1]) of the operator; x: device [nrhs x n] (ldx), the full

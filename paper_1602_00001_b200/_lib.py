@@ -61,6 +61,7 @@ SIGNATURES = {
     "invop_plan_get_planes": [_vp, _vp, _vp],
     "invop_plan_from_planes": [_vp, _int, _int, _i64, _i64, _i64, _int, _vp, C.POINTER(_vp)],
     "invop_plan_csc": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _pi64, _pi64, _vp],
+    "invop_apply_grouped_csc": [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "invop_apply": [_vp, _vp, _i64, _vp, _i64, _i64, _int, _int, _vp],
     "invop_apply_host": [_vp, _vp, _vp, _i64, _int, _vp],
     "invop_apply_sharded": [_vp, _vp, _vp, _vp, _i64, _vp, _i64, _i64, _int, _int, _vp],
