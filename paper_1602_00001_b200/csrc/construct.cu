@@ -21,12 +21,15 @@
 // Work: ~4 nx^3 ny flops per right-hand side, i.e. 4 n^5 for the whole inverse
 // of an n x n grid, versus (2/3+2) N^3 = (8/3) n^6 for dense LU + solve.
 #include "common.cuh"
+#include <cooperative_groups.h>
 #include <algorithm>
 #include <vector>
 #include <cmath>
 #include <cstring>
 
 namespace invop {
+
+namespace cg = cooperative_groups;
 
 constexpr int K4_T = 32;        // right-hand sides (rows of L^-1) per tile
 constexpr int K4_THREADS = 256;
@@ -104,6 +107,108 @@ __global__ void __launch_bounds__(1024) k4_factor(const double* __restrict__ dia
     }
     __syncthreads();
   }
+}
+
+// --------------------------------------------------------------- factor on a cluster
+// The same block LU and the same per-element arithmetic as k4_factor (so the
+// same bits), with the nx x nx Schur block distributed over a cluster of CL
+// CTAs, K4C_R rows each, held in shared memory for the whole factorisation
+// (one CTA kept it in global memory for nx > 160 and ran 1.4 s at config 5).
+// Per pivot p: one cluster barrier (every CTA finished pivot p-1, so row p is
+// final), every CTA copies row p from its owner through DSMEM into a
+// double-buffered pivot row, scales it by 1/D[p][p] locally and eliminates its
+// own rows; the owner writes the scaled row p back lazily at pivot p+1 (after
+// the next barrier, when no CTA reads it any more). D_{k+1} is built from the
+// CTA's own rows of D_k^-1 (elementwise), so block steps need no exchange.
+constexpr int K4C_R = 16;        // rows per CTA
+constexpr int K4C_THREADS = 256;
+
+__global__ void __launch_bounds__(K4C_THREADS) k4_factor_cl(
+    const double* __restrict__ diag, const double* __restrict__ ww, const double* __restrict__ we,
+    const double* __restrict__ ws, const double* __restrict__ wn, int nx, int ny, int nxp,
+    double tol, double* __restrict__ dinv, double* __restrict__ qmat, int* status) {
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ double shc[];
+  double* D = shc;                                  // [K4C_R][nxp] own rows
+  double* prow = shc + (size_t)K4C_R * nxp;         // [2][nxp] pivot row copies
+  const int c = (int)cl.block_rank();
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int n = nx;
+  const int r0 = c * K4C_R;                         // first global row of this CTA
+  for (int k = 0; k < ny; ++k) {
+    // D_k rows r0 .. r0+R (own), from the CTA's own rows of D_{k-1}^-1
+    for (int idx = tid; idx < K4C_R * n; idx += nt) {
+      const int li = idx / n, j = idx - li * n, i = r0 + li;
+      if (i >= n) continue;
+      const int64_t p = (int64_t)k * nx + i;
+      double v = 0.0;
+      if (i == j) v = diag[p];
+      else if (j == i - 1) v = -we[p - 1];
+      else if (j == i + 1) v = -ww[p + 1];
+      if (k > 0) {
+        const double lo = -wn[(int64_t)(k - 1) * nx + i];
+        const double up = -ws[(int64_t)k * nx + j];
+        v = __dsub_rn(v, __dmul_rn(__dmul_rn(lo, D[(size_t)li * nxp + j]), up));
+      }
+      D[(size_t)li * nxp + j] = v;
+    }
+    // Gauss-Jordan, pivots in order (diagonally dominant M-matrix: no pivoting)
+    for (int piv = 0; piv < n; ++piv) {
+      cl.sync();                                    // pivot piv-1 done everywhere
+      const int owner = piv / K4C_R, lrow = piv - owner * K4C_R;
+      double* pr = prow + (size_t)(piv & 1) * nxp;
+      // lazy write-back of the previous scaled pivot row (its owner only)
+      if (piv > 0 && (piv - 1) / K4C_R == c) {
+        const double* pp = prow + (size_t)((piv - 1) & 1) * nxp;
+        const int lq = (piv - 1) - c * K4C_R;
+        const double inv_q = 1.0 / pp[piv - 1];
+        for (int j = tid; j < n; j += nt)
+          D[(size_t)lq * nxp + j] = (j == piv - 1) ? inv_q : pp[j] * inv_q;
+      }
+      const double* src = cl.map_shared_rank(D + (size_t)lrow * nxp, owner);
+      for (int j = tid; j < n; j += nt) pr[j] = src[j];
+      __syncthreads();
+      const double pv = pr[piv];
+      if (!(fabs(pv) >= tol)) {
+        if (tid == 0 && c == 0) *status = 1;
+        cl.sync();                                  // uniform: every CTA saw the same pivot
+        return;
+      }
+      const double inv_p = 1.0 / pv;
+      for (int idx = tid; idx < K4C_R * n; idx += nt) {
+        const int li = idx / n, j = idx - li * n, i = r0 + li;
+        if (i >= n || i == piv) continue;
+        const double f = D[(size_t)li * nxp + piv];
+        // same arithmetic as k4_factor: the pivot row is scaled first
+        if (j != piv) D[(size_t)li * nxp + j] -= f * (pr[j] * inv_p);
+      }
+      __syncthreads();
+      for (int li = tid; li < K4C_R; li += nt) {
+        const int i = r0 + li;
+        if (i < n && i != piv) D[(size_t)li * nxp + piv] = -D[(size_t)li * nxp + piv] * inv_p;
+      }
+    }
+    cl.sync();
+    if ((n - 1) / K4C_R == c) {                     // the last pivot row's write-back
+      const double* pp = prow + (size_t)((n - 1) & 1) * nxp;
+      const int lq = (n - 1) - c * K4C_R;
+      const double inv_q = 1.0 / pp[n - 1];
+      for (int j = tid; j < n; j += nt) D[(size_t)lq * nxp + j] = (j == n - 1) ? inv_q : pp[j] * inv_q;
+    }
+    __syncthreads();
+    // store own rows of Dinv_k and Q_k (zero padded to nxp)
+    double* dk = dinv + (size_t)k * nxp * nxp;
+    double* qk = qmat + (size_t)k * nxp * nxp;
+    for (int idx = tid; idx < K4C_R * nxp; idx += nt) {
+      const int li = idx / nxp, j = idx - li * nxp, i = r0 + li;
+      if (i >= nxp) continue;
+      const double v = (i < n && j < n) ? D[(size_t)li * nxp + j] : 0.0;
+      dk[(size_t)i * nxp + j] = v;
+      const double up = (k + 1 < ny && j < n) ? -ws[(int64_t)(k + 1) * nx + j] : 0.0;
+      qk[(size_t)i * nxp + j] = v * up;
+    }
+  }
+  cl.sync();                                        // peers may read our D until here
 }
 
 // --------------------------------------------------------------- sweeps
@@ -387,6 +492,43 @@ extern "C" int invop_operator_factor(invop_operator* op, void* stream) {
   size_t blk = (size_t)nxp * nxp * sizeof(double);
   INVOP_CUDA(cudaMalloc(&op->dinv, blk * op->ny));
   INVOP_CUDA(cudaMalloc(&op->qmat, blk * op->ny));
+  double tol_c = 1e-13 * op->max_entry;  // PIVOT_RTOL of dense.py:16
+  const char* kc = getenv("INVOP_K4_CLUSTER");
+  if (nxp <= 16 * K4C_R && !(kc && *kc == '0')) {
+    // Schur block distributed over a cluster (one cluster barrier per pivot)
+    const int clsz = (int)(nxp / K4C_R);
+    int* status = nullptr;
+    INVOP_CUDA(cudaMalloc(&status, sizeof(int)));
+    INVOP_CUDA(cudaMemsetAsync(status, 0, sizeof(int), s));
+    const size_t csm = ((size_t)K4C_R + 2) * nxp * sizeof(double);
+    if (clsz > 8) INVOP_CUDA(cudaFuncSetAttribute(k4_factor_cl, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    INVOP_CUDA(cudaFuncSetAttribute(k4_factor_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(csm, 48 * 1024)));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(clsz);
+    cfg.blockDim = dim3(K4C_THREADS);
+    cfg.dynamicSmemBytes = csm;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = clsz;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e1 = cudaLaunchKernelEx(&cfg, k4_factor_cl, (const double*)op->diag, (const double*)op->ww,
+                                        (const double*)op->we, (const double*)op->ws,
+                                        (const double*)op->wn, (int)op->nx, (int)op->ny, (int)nxp, tol_c,
+                                        op->dinv, op->qmat, status);
+    int h = 0;
+    cudaMemcpyAsync(&h, status, sizeof(int), cudaMemcpyDeviceToHost, s);
+    cudaError_t e = cudaStreamSynchronize(s);
+    cudaFree(status);
+    if (e1 != cudaSuccess) return cuda_fail(e1, "k4_factor_cl launch");
+    if (e != cudaSuccess) return cuda_fail(e, "k4_factor_cl");
+    if (h) return fail(INVOP_E_SINGULAR, "block pivot below 1e-13*max|entry|; operator is singular");
+    op->factored = 1;
+    return INVOP_OK;
+  }
   size_t smem = blk + nxp * sizeof(double);
   int use_smem = smem <= 200 * 1024;
   double* gwork = nullptr;

@@ -307,6 +307,18 @@ def test_construct_matches_scipy(invop, O):
         assert (q.decode().cpu().numpy() == want).all()
 
 
+@pytest.mark.parametrize("nx,ny", [(13, 13), (40, 17), (100, 9), (128, 6), (250, 4), (256, 3), (24, 24)])
+def test_factor_cluster_matches_single_cta(invop, nx, ny, monkeypatch):
+    """The cluster-distributed block factorisation performs the single-CTA
+    kernel's arithmetic element for element: same inverse rows, bit for bit."""
+    st = invop.variable_interior(nx, seed=nx) if nx == ny else invop.uniform_interior(nx, ny)
+    rows = np.array([0, 1, nx * ny // 2, nx * ny - 1])
+    a = invop.DeviceOperator(st).factor().inverse_rows().cpu().numpy()[rows]
+    monkeypatch.setenv("INVOP_K4_CLUSTER", "0")
+    b = invop.DeviceOperator(st).factor().inverse_rows().cpu().numpy()[rows]
+    assert a.tobytes() == b.tobytes()
+
+
 # ------------------------------------------------------------------ full-size configs
 def _sample_rows(st, N, count, seed):
     """`count` random rows plus the centre row (the largest entries), the
