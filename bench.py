@@ -323,6 +323,10 @@ def run_reference(args, world, rank):
                          "host_cpus": os.cpu_count()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     })
+    # the reference arm never touches this repo's native library
+    from paper_1602_00001_b200 import _lib as _L
+
+    line["b200_library_loaded"] = _L.loaded()
     print(json.dumps(line), flush=True)
 
 
