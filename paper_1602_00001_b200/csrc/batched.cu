@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  asm volatile("griddepcontrol.wait;" ::: "memory");       // programmatic dependent of k3_prep
+  asm volatile("griddepcontrol.wait;" ::: "memory");       // programmatic dependent of k3_digits
   const uint32_t tmem = tmem_slot;
   const int64_t units = a.pairs * a.splits;
 
@@ -489,6 +489,612 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
   }
 }
 
+// ------------------------------------------------------------ tiled planes
+// K3 streams 128-row x 64-column tiles. In the row-major planes a tile is 128
+// separate 64-byte pieces (one per row, ld bytes apart): every TMA box then
+// touches 128 DRAM pages. The tensor-core path therefore reads a tiled copy of
+// the planes, built once per plan: tile (rt, kb) = rows [128 rt, 128 rt+128) x
+// columns [64 kb, 64 kb+64) stored as one contiguous 8 KB block, tiles of a row
+// tile consecutive along K, so a row tile's whole K range is one contiguous run.
+__global__ void k3_tile_planes(const uint8_t* __restrict__ in, int64_t rows, int64_t ld,
+                               uint8_t* __restrict__ out, int64_t rtiles) {
+  const int64_t kbt = ld / K3_BK;
+  const int64_t total16 = rtiles * kbt * (K3_A_TILE / 16);
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total16;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t tile = k / (K3_A_TILE / 16);
+    const int within = (int)(k - tile * (K3_A_TILE / 16));
+    const int r = within >> 2, c16 = within & 3;
+    const int64_t rt = tile / kbt, kb = tile - rt * kbt;
+    const int64_t row = rt * K3_BM + r;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (row < rows) v = *reinterpret_cast<const uint4*>(in + row * ld + kb * K3_BK + c16 * 16);
+    *reinterpret_cast<uint4*>(out + tile * K3_A_TILE + r * K3_BK + c16 * 16) = v;
+  }
+}
+
+// ------------------------------------------------------------ x preparation
+// Two single-phase kernels (no cluster barriers; a programmatic dependent
+// launch chain hides the boundary), grid (column chunks, 64 right-hand sides):
+//  k3_xmax: max |x_tj| over the finite entries -> atomicMax on the float bits
+//    (maxbits[t], non-negative floats order like their bits); columns whose x
+//    is inf/nan are listed instead (nf_cols[t][.]): the reference skips zero
+//    mantissas (_native.pyx:32-46), so those columns are applied exactly by
+//    k3_post and enter the digits as 0;
+//  k3_digits: e_t (max|x_t| 2^e_t < 2^22) and the balanced base-256 digits of
+//    X = rint(x 2^e_t) into B[l][t][j] (int8), 16 columns per thread, three
+//    16-byte stores; right-hand sides t >= nrhs get zeros. DL: plan rows 0
+//    and 1 are stored as zero residuals; their exact sums Y_0, Y_1 come from
+//    the byte-plane codes and the same X (16-byte plane loads beside the
+//    digits), added atomically into y01[t] (k3_post folds them into D_0, D_1).
+// maxbits, nf_count and y01 are zero on entry: k3_post resets them.
+constexpr int K3X_COLS = 8192;        // columns per k3_xmax CTA
+constexpr int K3X_TPB = 256;
+constexpr int K3G_TPB = 256;          // k3_digits: 16 columns per thread
+constexpr int K3G_COLS = K3G_TPB * 16;
+
+struct K3Prep {
+  const float* x;
+  int64_t n, ldx;
+  int nrhs;
+  int8_t* B;
+  int64_t ldb;
+  int* e;
+  unsigned int* maxbits;      // [64]
+  int* nf_count;
+  int* nf_cols;
+  const uint8_t* planes[2];   // rows 0/1 codes (DL)
+  int64_t ld, rows;
+  int P, sgn, rows01;
+  unsigned long long* y01;    // [64][2] exact sums of plan rows 0, 1 (DL)
+};
+
+__device__ __forceinline__ int k3_exponent(float m) {
+  int ex = 0;
+  if (m > 0.0f && isfinite(m)) frexpf(m, &ex);
+  return (m > 0.0f && isfinite(m)) ? 22 - ex : 0;   // max|x_t| * 2^e_t < 2^22
+}
+
+__device__ __forceinline__ int32_t k3_code16(uint32_t lo, uint32_t hi, int bb, int P, int sgn) {
+  uint32_t u = (lo >> bb) & 255u;
+  if (P > 1) u |= ((hi >> bb) & 255u) << 8;
+  const int sh = 32 - 8 * P;
+  return sgn ? ((int32_t)(u << sh) >> sh) : (int32_t)u;
+}
+
+__global__ void __launch_bounds__(K3X_TPB) k3_xmax(K3Prep a) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");       // x may be the previous apply's y
+  asm volatile("griddepcontrol.launch_dependents;");
+  __shared__ float s_warp[K3X_TPB / 32];
+  const int t = blockIdx.y;
+  if (t >= a.nrhs) return;
+  const float* xt = a.x + (int64_t)t * a.ldx;
+  const int64_t j0 = (int64_t)blockIdx.x * K3X_COLS, j1 = min(a.n, j0 + K3X_COLS);
+  float m = 0.0f;
+  const bool vec = ((((uintptr_t)xt) | (uintptr_t)(a.ldx * 4)) & 15) == 0;
+  if (vec) {
+    // all of the thread's loads first (coalesced 16-byte loads, 8 in flight),
+    // then the scan: an atomic in the load loop would serialise the loads
+    constexpr int U = K3X_COLS / (4 * K3X_TPB);
+    float4 f[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t j = j0 + 4 * ((int64_t)threadIdx.x + (int64_t)u * K3X_TPB);
+      if (j + 4 <= j1) {
+        f[u] = *reinterpret_cast<const float4*>(xt + j);
+      } else {
+        f[u].x = j < j1 ? xt[j] : 0.0f;
+        f[u].y = j + 1 < j1 ? xt[j + 1] : 0.0f;
+        f[u].z = j + 2 < j1 ? xt[j + 2] : 0.0f;
+        f[u].w = j + 3 < j1 ? xt[j + 3] : 0.0f;
+      }
+    }
+    bool bad = false;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const float v[4] = {f[u].x, f[u].y, f[u].z, f[u].w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        bad |= !isfinite(v[i]);
+        m = fmaxf(m, isfinite(v[i]) ? fabsf(v[i]) : 0.0f);
+      }
+    }
+    if (bad) {                       // rare: list the non-finite columns
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const float v[4] = {f[u].x, f[u].y, f[u].z, f[u].w};
+        const int64_t j = j0 + 4 * ((int64_t)threadIdx.x + (int64_t)u * K3X_TPB);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (!isfinite(v[i]) && j + i < j1) {
+            const int k = atomicAdd(&a.nf_count[t], 1);
+            a.nf_cols[(int64_t)t * a.n + k] = (int)(j + i);
+          }
+      }
+    }
+  } else {
+    for (int64_t j = j0 + threadIdx.x; j < j1; j += K3X_TPB) {
+      const float v = xt[j];
+      if (isfinite(v)) {
+        m = fmaxf(m, fabsf(v));
+      } else {
+        const int k = atomicAdd(&a.nf_count[t], 1);
+        a.nf_cols[(int64_t)t * a.n + k] = (int)j;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) s_warp[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float v = 0.0f;
+#pragma unroll
+    for (int w = 0; w < K3X_TPB / 32; ++w) v = fmaxf(v, s_warp[w]);
+    atomicMax(&a.maxbits[t], __float_as_uint(v));
+  }
+}
+
+__global__ void __launch_bounds__(K3G_TPB, 6) k3_digits(K3Prep a) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");       // k3_xmax complete
+  asm volatile("griddepcontrol.launch_dependents;");
+  __shared__ long long s_w01[K3G_TPB / 32][2];
+  const int t = blockIdx.y;
+  const bool live = t < a.nrhs;
+  const float* xt = a.x + (int64_t)t * a.ldx;
+  const int et = live ? k3_exponent(__uint_as_float(a.maxbits[t])) : 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.e[t] = et;
+  // 2^e_t as two float factors (e_t may exceed 127 for tiny x): x * 2^e_t is
+  // exact for the in-range products, the same value ldexpf returns
+  const int e1 = et > 126 ? 126 : (et < -126 ? -126 : et), e2 = et - e1;
+  const float f1 = __int_as_float((127 + e1) << 23), f2 = __int_as_float((127 + e2) << 23);
+  const int64_t jb = (int64_t)blockIdx.x * K3G_COLS + (int64_t)threadIdx.x * 16;
+  long long s0 = 0, s1 = 0;
+  if (jb < a.ldb) {
+    float xv[16];
+    if (live && jb + 16 <= a.n && (((uintptr_t)(xt + jb)) & 15) == 0) {
+#pragma unroll
+      for (int i = 0; i < 16; i += 4) {
+        const float4 f = *reinterpret_cast<const float4*>(xt + jb + i);
+        xv[i] = f.x; xv[i + 1] = f.y; xv[i + 2] = f.z; xv[i + 3] = f.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) xv[i] = (live && jb + i < a.n) ? xt[jb + i] : 0.0f;
+    }
+    int X[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) X[i] = isfinite(xv[i]) ? __float2int_rn((xv[i] * f1) * f2) : 0;
+    uint32_t w[3][4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint32_t b0 = 0, b1 = 0, b2 = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int Xv = X[4 * q + i];
+        const int d0 = ((Xv + 128) & 255) - 128;
+        const int X1 = (Xv - d0) >> 8;
+        const int d1 = ((X1 + 128) & 255) - 128;
+        const int d2 = (X1 - d1) >> 8;
+        b0 |= ((uint32_t)d0 & 255u) << (8 * i);
+        b1 |= ((uint32_t)d1 & 255u) << (8 * i);
+        b2 |= ((uint32_t)d2 & 255u) << (8 * i);
+      }
+      w[0][q] = b0; w[1][q] = b1; w[2][q] = b2;
+    }
+#pragma unroll
+    for (int l = 0; l < 3; ++l)
+      *reinterpret_cast<uint4*>(a.B + (int64_t)(l * K3_NR + t) * a.ldb + jb) =
+          make_uint4(w[l][0], w[l][1], w[l][2], w[l][3]);
+    if (a.rows01 && live) {
+      // plane rows are ld >= ldb bytes with zero padding: 16-byte loads
+      const uint4 p00 = *reinterpret_cast<const uint4*>(a.planes[0] + jb);
+      const uint4 p01 = *reinterpret_cast<const uint4*>(a.planes[1] + jb);
+      const bool two = a.rows > 1;
+      const uint4 p10 = two ? *reinterpret_cast<const uint4*>(a.planes[0] + a.ld + jb) : make_uint4(0, 0, 0, 0);
+      const uint4 p11 = two ? *reinterpret_cast<const uint4*>(a.planes[1] + a.ld + jb) : make_uint4(0, 0, 0, 0);
+      const uint32_t A0[4] = {p00.x, p00.y, p00.z, p00.w}, A1[4] = {p01.x, p01.y, p01.z, p01.w};
+      const uint32_t B0[4] = {p10.x, p10.y, p10.z, p10.w}, B1[4] = {p11.x, p11.y, p11.z, p11.w};
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int q = i >> 2, bb = 8 * (i & 3);
+        s0 += (long long)k3_code16(A0[q], A1[q], bb, a.P, a.sgn) * X[i];
+        s1 += (long long)k3_code16(B0[q], B1[q], bb, a.P, a.sgn) * X[i];
+      }
+    }
+  }
+  if (a.rows01 && live) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    }
+    if ((threadIdx.x & 31) == 0) { s_w01[threadIdx.x >> 5][0] = s0; s_w01[threadIdx.x >> 5][1] = s1; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      long long v0 = 0, v1 = 0;
+#pragma unroll
+      for (int w = 0; w < K3G_TPB / 32; ++w) { v0 += s_w01[w][0]; v1 += s_w01[w][1]; }
+      atomicAdd(&a.y01[2 * t], (unsigned long long)v0);
+      atomicAdd(&a.y01[2 * t + 1], (unsigned long long)v1);
+    }
+  }
+}
+
+// cluster barrier halves: arrive without a release fence (only register or
+// shared-memory state the peers already consumed is involved) / wait
+__device__ __forceinline__ void k3_cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void k3_cluster_wait() {
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+}
+
+// ------------------------------------------------------------ K3 on row residuals
+// Residual of plan row r (plan-local): e_r = v_r - 2 v_{r-1} + v_{r-2} for
+// r >= 2; rows 0 and 1 are stored as zero and their sums computed exactly from
+// the codes (k3d_rows01), so D_0 = Y_0, D_1 = Y_1 - 2 Y_0 and Y is the double
+// prefix sum of D along rows (k3d_scan). Digits are balanced base-256.
+__device__ __forceinline__ int32_t k3d_code(const uint8_t* const* planes, int P, int sgn,
+                                            int64_t off) {
+  uint32_t u = 0;
+  for (int b = 0; b < P; ++b) u |= (uint32_t)planes[b][off] << (8 * b);
+  const int sh = 32 - 8 * P;
+  return sgn ? ((int32_t)(u << sh) >> sh) : (int32_t)u;
+}
+
+struct K3DBuild {
+  const uint8_t* planes[2];
+  int P, sgn;
+  int64_t rows, ld;
+  int64_t kbs, rtiles;
+};
+
+// digit-0 tiles: the two row tiles of a pair at the same K block are adjacent,
+// so one 256-row TMA box loads both
+__host__ __device__ inline int64_t k3d_tile0(int64_t rt, int64_t kb, int64_t kbs) {
+  return ((rt >> 1) * kbs + kb) * 2 + (rt & 1);
+}
+
+__device__ __forceinline__ int32_t k3d_resid(const K3DBuild& a, int64_t r, int64_t j) {
+  if (r < 2 || r >= a.rows) return 0;
+  const int64_t off = r * a.ld + j;
+  return k3d_code(a.planes, a.P, a.sgn, off) - 2 * k3d_code(a.planes, a.P, a.sgn, off - a.ld) +
+         k3d_code(a.planes, a.P, a.sgn, off - 2 * a.ld);
+}
+
+// one thread per (row, K block): digit count of its 64 residuals -> tile max
+__global__ void k3d_width(K3DBuild a, int* __restrict__ tilew, int* __restrict__ wmax) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= a.rows * a.kbs) return;
+  const int64_t r = t / a.kbs, kb = t - r * a.kbs;
+  int w = 1;
+  for (int q = 0; q < K3_BK; ++q) {
+    int32_t e = k3d_resid(a, r, kb * K3_BK + q);
+    int n = 1;
+    for (;;) {
+      const int32_t d = ((e + 128) & 255) - 128;
+      e = (e - d) >> 8;
+      if (e == 0) break;
+      ++n;
+    }
+    w = max(w, n);
+  }
+  atomicMax(&tilew[(r / K3_BM) * a.kbs + kb], w);
+  atomicMax(wmax, w);
+}
+
+// compact index of the tiles that need a digit-1 plane (one block)
+__global__ void k3d_index(int64_t tiles, const int* __restrict__ tilew, int* __restrict__ idx1,
+                          int64_t* __restrict__ n1) {
+  __shared__ int64_t part[1024];
+  const int t = threadIdx.x, T = blockDim.x;
+  const int64_t per = (tiles + T - 1) / T;
+  const int64_t a0 = t * per, a1 = min(tiles, a0 + per);
+  int64_t c = 0;
+  for (int64_t i = a0; i < a1; ++i) c += tilew[i] >= 2;
+  part[t] = c;
+  __syncthreads();
+  if (t == 0) {
+    int64_t acc = 0;
+    for (int i = 0; i < T; ++i) { const int64_t v = part[i]; part[i] = acc; acc += v; }
+    *n1 = acc;
+  }
+  __syncthreads();
+  int64_t acc = part[t];
+  for (int64_t i = a0; i < a1; ++i) idx1[i] = tilew[i] >= 2 ? (int)acc++ : -1;
+}
+
+// one thread per (row, K block): write the residual digits into the tiles
+__global__ void k3d_write(K3DBuild a, const int* __restrict__ idx1, uint8_t* __restrict__ t0,
+                          uint8_t* __restrict__ t1) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= a.rows * a.kbs) return;
+  const int64_t r = t / a.kbs, kb = t - r * a.kbs;
+  const int64_t tile = (r / K3_BM) * a.kbs + kb;
+  const int i1 = idx1[tile];
+  uint8_t* d0 = t0 + k3d_tile0(r / K3_BM, kb, a.kbs) * K3_A_TILE + (r % K3_BM) * K3_BK;
+  uint8_t* d1 = i1 >= 0 ? t1 + (int64_t)i1 * K3_A_TILE + (r % K3_BM) * K3_BK : nullptr;
+  for (int q0 = 0; q0 < K3_BK; q0 += 16) {
+    uint32_t w0[4] = {0, 0, 0, 0}, w1[4] = {0, 0, 0, 0};
+    for (int q = 0; q < 16; ++q) {
+      const int32_t e = k3d_resid(a, r, kb * K3_BK + q0 + q);
+      const int32_t g0 = ((e + 128) & 255) - 128;
+      const int32_t g1 = (e - g0) >> 8;
+      w0[q >> 2] |= ((uint32_t)g0 & 255u) << (8 * (q & 3));
+      w1[q >> 2] |= ((uint32_t)g1 & 255u) << (8 * (q & 3));
+    }
+    *reinterpret_cast<uint4*>(d0 + q0) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
+    if (d1) *reinterpret_cast<uint4*>(d1 + q0) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
+  }
+}
+
+// ------------------------------------------------------------ k3_post
+// From the exact int64 row sums the tensor-core pass accumulated in yacc to
+// fp32 y; one cluster of K3Q_CL CTAs per right-hand side (grid (K3Q_CL, nrhs)),
+// each CTA a contiguous block of rows in tiles of K3Q_TILE. Global memory is
+// touched only by coalesced row-strided accesses; a padded shared-memory
+// transpose gives every thread K3Q_RPT consecutive rows for the scans.
+//  * DL: yacc holds D = E X for the second-order row residuals (+ k3_digits's
+//    rows 0/1 corrections). Y is the double prefix sum of D along rows: per
+//    tile two block scans (thread sums of d, then of the thread-local second
+//    prefix), each CTA publishes (sum D, sum z, length) in shared memory and
+//    folds its predecessors' triples (DSMEM) into its carry-in
+//    (composition of consecutive blocks A, B: sumZ = sumZ_A + sumZ_B +
+//    len_B sumD_A);
+//  * byte planes: yacc holds Y itself;
+//  * y = fl32(Y 10^-m 2^-e_t); columns whose x is inf/nan (k3_xmax's list)
+//    are applied as the reference loop would (zero mantissas skipped): nan if
+//    any non-zero v_ij meets a nan or both infinite signs occur, else +-inf;
+//  * yacc is reset to zero behind the read, ready for the next apply's
+//    atomic K-split partials (no memset launch).
+constexpr int K3Q_CL = 16;             // non-portable cluster size (opt-in at launch)
+constexpr int K3Q_TPB = 256;
+constexpr int K3Q_RPT = 16;
+constexpr int K3Q_TILE = K3Q_TPB * K3Q_RPT;
+constexpr int K3Q_SMEM = K3Q_TILE + K3Q_TILE / 16;   // 8-byte words, one pad per 16
+
+__device__ __forceinline__ int k3q_pad(int k) { return k + (k >> 4); }
+
+struct K3Post {
+  long long* yacc;
+  int64_t rows, n, ld;
+  const uint8_t* planes[2];
+  int P, sgn;
+  const int* e;
+  double scale;
+  int* nf_count;
+  const int* nf_cols;
+  long long* y01;                 // k3_digits's exact sums of plan rows 0, 1 (reset here)
+  unsigned int* maxbits;          // k3_xmax's max|x_t| bits (reset here)
+  const float* x;
+  int64_t ldx;
+  float* y;
+  int64_t ldy;
+};
+
+__device__ __forceinline__ long long k3q_block_excl(long long v, long long* sh) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  long long inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long u = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += u;
+  }
+  if (lane == 31) sh[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    long long s = lane < K3Q_TPB / 32 ? sh[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long u = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += u;
+    }
+    sh[lane] = s;
+  }
+  __syncthreads();
+  const long long r = inc - v + (w > 0 ? sh[w - 1] : 0);
+  __syncthreads();
+  return r;
+}
+
+// tile s (L valid rows) -> d[]: coalesced row-strided loads into padded
+// shared memory, then this thread's K3Q_RPT consecutive rows
+__device__ __forceinline__ void k3q_load(const K3Post& a, int t, int64_t s, int64_t L,
+                                         long long add0, long long add1, long long* d,
+                                         long long* sd) {
+  const long long* src = a.yacc + (int64_t)t * a.rows + s;
+#pragma unroll
+  for (int i = 0; i < K3Q_RPT; ++i) {
+    const int k = i * K3Q_TPB + threadIdx.x;
+    long long v = k < L ? src[k] : 0;
+    if (s + k == 0) v += add0;          // plan rows 0 and 1 (DL corrections; 0 otherwise)
+    if (s + k == 1) v += add1;
+    sd[k3q_pad(k)] = v;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < K3Q_RPT; ++i) d[i] = sd[k3q_pad(threadIdx.x * K3Q_RPT + i)];
+  __syncthreads();
+}
+
+// d[] -> the thread's exclusive block prefixes: ze (first prefix) and we
+// (second prefix, relative to the tile start); tile sums via the thread
+// holding the tile's last valid row
+__device__ __forceinline__ void k3q_scan(const long long* d, int64_t L, long long* sh,
+                                         long long* s_tile, long long& ze, long long& we,
+                                         long long& sD, long long& sZ) {
+  long long S = 0, C = 0;
+#pragma unroll
+  for (int i = 0; i < K3Q_RPT; ++i) { S += d[i]; C += S; }
+  ze = k3q_block_excl(S, sh);
+  const long long W = (long long)K3Q_RPT * ze + C;   // sum of the thread's second prefix
+  we = k3q_block_excl(W, sh);
+  const int64_t last = L - 1;
+  if ((int64_t)threadIdx.x == last / K3Q_RPT) {
+    const int il = (int)(last % K3Q_RPT);
+    long long cs = 0, cc = 0;
+#pragma unroll
+    for (int i = 0; i < K3Q_RPT; ++i) {
+      cs += d[i];
+      cc += ze + cs;
+      if (i == il) { s_tile[0] = ze + cs; s_tile[1] = we + cc; }
+    }
+  }
+  __syncthreads();
+  sD = s_tile[0];
+  sZ = s_tile[1];
+  __syncthreads();
+}
+
+// Y of the thread's rows (running prefixes from base_z / base_y) -> fp32 in
+// shared memory -> coalesced stores of y and zeros into yacc
+template <bool DL>
+__device__ __forceinline__ void k3q_store(const K3Post& a, int t, int64_t s, int64_t L,
+                                          const long long* d, long long base_z, long long base_y,
+                                          double sc, float* sy) {
+  long long z = base_z, yv = base_y;
+#pragma unroll
+  for (int i = 0; i < K3Q_RPT; ++i) {
+    long long Y;
+    if (DL) { z += d[i]; yv += z; Y = yv; } else { Y = d[i]; }
+    sy[k3q_pad(threadIdx.x * K3Q_RPT + i)] = (float)((double)Y * sc);
+  }
+  __syncthreads();
+  float* dst = a.y + (int64_t)t * a.ldy + s;
+  long long* acc = a.yacc + (int64_t)t * a.rows + s;
+#pragma unroll
+  for (int i = 0; i < K3Q_RPT; ++i) {
+    const int k = i * K3Q_TPB + threadIdx.x;
+    if (k < L) {
+      dst[k] = sy[k3q_pad(k)];
+      acc[k] = 0;
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ float k3q_nonfinite(const K3Post& a, int t, int64_t r, float v, int nf) {
+  bool isn = false, pos = false, neg = false;
+  for (int k = 0; k < nf; ++k) {
+    const int64_t j = a.nf_cols[(int64_t)t * a.n + k];
+    const int64_t off = r * a.ld + j;
+    uint32_t u = a.planes[0][off];
+    if (a.P > 1) u |= (uint32_t)a.planes[1][off] << 8;
+    const int sh = 32 - 8 * a.P;
+    const int32_t q = a.sgn ? ((int32_t)(u << sh) >> sh) : (int32_t)u;
+    if (q == 0) continue;
+    const float xv = a.x[(int64_t)t * a.ldx + j];
+    if (isnan(xv)) isn = true;
+    else if ((q < 0) != (xv < 0.0f)) neg = true;
+    else pos = true;
+  }
+  if (isn || (pos && neg)) return __int_as_float(0x7fc00000);
+  if (pos) return __int_as_float(0x7f800000);
+  if (neg) return __int_as_float(0xff800000);
+  return v;
+}
+
+// columns with inf/nan x (rare): after the CTA's rows are stored
+__device__ __forceinline__ void k3q_fix_nonfinite(const K3Post& a, int t, int64_t r0, int64_t r1,
+                                                  int nf) {
+  __syncthreads();
+  for (int64_t r = r0 + threadIdx.x; r < r1; r += K3Q_TPB) {
+    float* dst = a.y + (int64_t)t * a.ldy + r;
+    *dst = k3q_nonfinite(a, t, r, *dst, nf);
+  }
+}
+
+template <bool DL>
+__global__ void __launch_bounds__(K3Q_TPB, 4) k3_post(K3Post a) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");       // the tensor-core pass is complete
+  asm volatile("griddepcontrol.launch_dependents;");
+  cg::cluster_group cl = cg::this_cluster();
+  __shared__ long long sd[K3Q_SMEM];
+  __shared__ long long sh[32];
+  __shared__ long long s_tile[2];
+  __shared__ long long s_tot[3];
+  __shared__ long long s_carry[2];
+  float* sy = reinterpret_cast<float*>(sd);
+  const int t = blockIdx.y;
+  const int c = (int)cl.block_rank();
+  const int64_t per = cdiv(a.rows, K3Q_CL);
+  const int64_t r0 = min(a.rows, (int64_t)c * per), r1 = min(a.rows, r0 + per);
+  const long long add0 = DL ? a.y01[2 * t] : 0;
+  const long long add1 = DL ? a.y01[2 * t + 1] - 2 * a.y01[2 * t] : 0;   // D_1 += Y_1 - 2 Y_0
+  if (c == 0 && threadIdx.x == 0) a.maxbits[t] = 0;     // read by k3_digits only (complete)
+  const double sc = ldexp(a.scale, -a.e[t]);
+  const int nf = a.nf_count[t];
+  long long d[K3Q_RPT];
+  if (!DL) {
+    for (int64_t s = r0; s < r1; s += K3Q_TILE) {
+      const int64_t L = min((int64_t)K3Q_TILE, r1 - s);
+      k3q_load(a, t, s, L, 0, 0, d, sd);
+      k3q_store<false>(a, t, s, L, d, 0, 0, sc, sy);
+    }
+    if (nf > 0) {
+      k3q_fix_nonfinite(a, t, r0, r1, nf);
+      cl.sync();                     // every CTA has read nf_count[t]
+      if (c == 0 && threadIdx.x == 0) a.nf_count[t] = 0;
+    }
+    return;
+  }
+  const bool one = r1 - r0 <= K3Q_TILE;          // the rows stay in registers
+  long long ze = 0, we = 0, sD = 0, sZ = 0;
+  long long SD = 0, SZ = 0;
+  for (int64_t s = r0; s < r1; s += K3Q_TILE) {
+    const int64_t L = min((int64_t)K3Q_TILE, r1 - s);
+    k3q_load(a, t, s, L, add0, add1, d, sd);
+    k3q_scan(d, L, sh, s_tile, ze, we, sD, sZ);
+    SZ += sZ + L * SD;
+    SD += sD;
+  }
+  if (threadIdx.x == 0) { s_tot[0] = SD; s_tot[1] = SZ; s_tot[2] = r1 - r0; }
+  cl.sync();
+  // lane r of warp 0 reads the triple of peer r < c (parallel DSMEM loads);
+  // lane 0 folds them in rank order
+  if (threadIdx.x < 32) {
+    long long pd = 0, pz = 0, pl = 0;
+    if ((int)threadIdx.x < c) {
+      const long long* p = cl.map_shared_rank(s_tot, (int)threadIdx.x);
+      pd = p[0];
+      pz = p[1];
+      pl = p[2];
+    }
+    long long zi = 0, yi = 0;
+    for (int r = 0; r < c; ++r) {
+      const long long d_ = __shfl_sync(0xffffffffu, pd, r);
+      const long long z_ = __shfl_sync(0xffffffffu, pz, r);
+      const long long l_ = __shfl_sync(0xffffffffu, pl, r);
+      yi += l_ * zi + z_;
+      zi += d_;
+    }
+    if (threadIdx.x == 0) { s_carry[0] = zi; s_carry[1] = yi; }
+  }
+  k3_cluster_arrive_relaxed();     // this CTA is done reading its peers
+  __syncthreads();
+  long long Zin = s_carry[0], Yin = s_carry[1];
+  for (int64_t s = r0; s < r1; s += K3Q_TILE) {
+    const int64_t L = min((int64_t)K3Q_TILE, r1 - s);
+    if (!one) {
+      k3q_load(a, t, s, L, add0, add1, d, sd);
+      k3q_scan(d, L, sh, s_tile, ze, we, sD, sZ);
+    }
+    // row s + off + i: Z = Zin + ze + cs_i, Y = Yin + (off + i + 1) Zin + we + sum_{i'<=i} (ze + cs_i')
+    const int64_t off = (int64_t)threadIdx.x * K3Q_RPT;
+    k3q_store<true>(a, t, s, L, d, Zin + ze, Yin + off * Zin + we, sc, sy);
+    Yin += L * Zin + sZ;
+    Zin += sD;
+  }
+  if (nf > 0) k3q_fix_nonfinite(a, t, r0, r1, nf);
+  k3_cluster_wait();               // peers read s_tot through DSMEM until here
+  if (c == 0 && threadIdx.x == 0) {  // every CTA read these above
+    if (nf > 0) a.nf_count[t] = 0;
+    a.y01[2 * t] = 0;
+    a.y01[2 * t + 1] = 0;
+  }
+}
+
 // ------------------------------------------------------------ DL kernel on SM pairs
 // k3_dl2: the residual-tile apply with tcgen05.mma.cta_group::2 (config 5's
 // route). Probes of the one-SM kernel (k3_batched<2,2,5,true>) put it at
@@ -607,7 +1213,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(K3_THREADS, 1)
   __syncthreads();
   k3_cluster_sync_all();
   tc_fence_after();
-  // launched as a programmatic dependent of k3_prep: the prologue above
+  // launched as a programmatic dependent of k3_digits: the prologue above
   // overlaps its tail; B (the x digits) and yacc are read after this
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint32_t tmem = tmem_slot;
@@ -770,596 +1376,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(K3_THREADS, 1)
   }
 }
 
-// ------------------------------------------------------------ tiled planes
-// K3 streams 128-row x 64-column tiles. In the row-major planes a tile is 128
-// separate 64-byte pieces (one per row, ld bytes apart): every TMA box then
-// touches 128 DRAM pages. The tensor-core path therefore reads a tiled copy of
-// the planes, built once per plan: tile (rt, kb) = rows [128 rt, 128 rt+128) x
-// columns [64 kb, 64 kb+64) stored as one contiguous 8 KB block, tiles of a row
-// tile consecutive along K, so a row tile's whole K range is one contiguous run.
-__global__ void k3_tile_planes(const uint8_t* __restrict__ in, int64_t rows, int64_t ld,
-                               uint8_t* __restrict__ out, int64_t rtiles) {
-  const int64_t kbt = ld / K3_BK;
-  const int64_t total16 = rtiles * kbt * (K3_A_TILE / 16);
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total16;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t tile = k / (K3_A_TILE / 16);
-    const int within = (int)(k - tile * (K3_A_TILE / 16));
-    const int r = within >> 2, c16 = within & 3;
-    const int64_t rt = tile / kbt, kb = tile - rt * kbt;
-    const int64_t row = rt * K3_BM + r;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (row < rows) v = *reinterpret_cast<const uint4*>(in + row * ld + kb * K3_BK + c16 * 16);
-    *reinterpret_cast<uint4*>(out + tile * K3_A_TILE + r * K3_BK + c16 * 16) = v;
-  }
-}
-
-// ------------------------------------------------------------ x preparation
-// k3_prep: one cluster of K3P_CL CTAs per right-hand side t (grid (K3P_CL, 64)),
-// each CTA a contiguous share of the columns, 16 consecutive columns per
-// thread (four 16-byte loads of x; the same registers feed both passes when
-// the share fits one sweep of the CTA, i.e. n <= K3P_CL * K3P_TPB * 16).
-//  1. max |x_tj| over the finite entries: block reduction, then across the
-//     cluster through distributed shared memory (one launch, no atomics);
-//     columns whose x is inf/nan are listed instead (nf_cols[t][.]): the
-//     reference skips zero mantissas (_native.pyx:32-46), so those columns
-//     are applied exactly by k3_post and enter the digits as 0;
-//  2. the exponent e_t (max|x_t| 2^e_t < 2^22) and the balanced base-256
-//     digits of X = rint(x 2^e_t) into B[l][t][j] (int8), three 16-byte
-//     stores per thread. Right-hand sides t >= nrhs get zeros;
-//  3. DL: plan rows 0 and 1 are stored as zero residuals; their exact sums
-//     Y_0, Y_1 come from the byte-plane codes and the same X (16-byte plane
-//     loads beside the digits), reduced across the cluster, and k3_post adds
-//     the corrections D_0 += Y_0, D_1 += Y_1 - 2 Y_0 (y01[t]).
-constexpr int K3P_CL = 16;            // non-portable cluster size (opt-in at launch)
-constexpr int K3P_TPB = 128;          // 1024 CTAs of 128 threads: one wave at 64 registers
-constexpr int K3P_SWEEP = K3P_TPB * 16;
-
-struct K3Prep {
-  const float* x;
-  int64_t n, ldx;
-  int nrhs;
-  int8_t* B;
-  int64_t ldb;
-  int* e;
-  int* nf_count;
-  int* nf_cols;
-  const uint8_t* planes[2];   // rows 0/1 codes (DL)
-  int64_t ld, rows;
-  int P, sgn, rows01;
-  long long* y01;             // [64][2] corrections of D_0, D_1 (DL)
-};
-
-__device__ __forceinline__ int k3_exponent(float m) {
-  int ex = 0;
-  if (m > 0.0f && isfinite(m)) frexpf(m, &ex);
-  return (m > 0.0f && isfinite(m)) ? 22 - ex : 0;   // max|x_t| * 2^e_t < 2^22
-}
-
-__device__ __forceinline__ int32_t k3_code16(uint32_t lo, uint32_t hi, int bb, int P, int sgn) {
-  uint32_t u = (lo >> bb) & 255u;
-  if (P > 1) u |= ((hi >> bb) & 255u) << 8;
-  const int sh = 32 - 8 * P;
-  return sgn ? ((int32_t)(u << sh) >> sh) : (int32_t)u;
-}
-
-// cluster barrier halves: arrive without a release fence (only register or
-// shared-memory state the peers already consumed is involved) / wait
-__device__ __forceinline__ void k3_cluster_arrive_relaxed() {
-  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void k3_cluster_wait() {
-  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
-}
-
-__device__ __forceinline__ void k3p_load16(const float* xt, int64_t jb, int64_t n, bool live,
-                                           float* xv) {
-  if (live && jb + 16 <= n && (((uintptr_t)(xt + jb)) & 15) == 0) {
-#pragma unroll
-    for (int i = 0; i < 16; i += 4) {
-      const float4 f = *reinterpret_cast<const float4*>(xt + jb + i);
-      xv[i] = f.x; xv[i + 1] = f.y; xv[i + 2] = f.z; xv[i + 3] = f.w;
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < 16; ++i) xv[i] = (live && jb + i < n) ? xt[jb + i] : 0.0f;
-  }
-}
-
-__global__ void __launch_bounds__(K3P_TPB, 8) k3_prep(K3Prep a) {
-  // programmatic dependent of the preceding grid (x may be its output; B, e
-  // and y01 are still read by the previous apply until it completes)
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;");
-  cg::cluster_group cl = cg::this_cluster();
-  __shared__ float s_warp[K3P_TPB / 32];
-  __shared__ long long s_w01[K3P_TPB / 32][2];
-  __shared__ float s_max, s_gmax;
-  __shared__ long long s_01[2];
-  const int t = blockIdx.y;
-  const int c = (int)cl.block_rank();
-  const bool live = t < a.nrhs;
-  const float* xt = a.x + (int64_t)t * a.ldx;
-  const int64_t per = round_up(cdiv(a.ldb, K3P_CL), 16);
-  const int64_t j0 = (int64_t)c * per, j1 = min(a.ldb, j0 + per);
-  const bool one = per <= K3P_SWEEP;           // x stays in registers
-  float m = 0.0f;                              // nf_count[t] is 0 on entry (k3_post resets it)
-  float xv[16];
-  for (int64_t jb = j0 + (int64_t)threadIdx.x * 16; jb < j1; jb += K3P_SWEEP) {
-    k3p_load16(xt, jb, a.n, live, xv);
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      if (isfinite(xv[i])) {
-        m = fmaxf(m, fabsf(xv[i]));
-      } else {
-        const int k = atomicAdd(&a.nf_count[t], 1);
-        a.nf_cols[(int64_t)t * a.n + k] = (int)(jb + i);
-      }
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) s_warp[threadIdx.x >> 5] = m;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    float v = 0.0f;
-#pragma unroll
-    for (int w = 0; w < K3P_TPB / 32; ++w) v = fmaxf(v, s_warp[w]);
-    s_max = v;
-  }
-  cl.sync();
-  // lane r of warp 0 reads peer r (parallel DSMEM loads), then a warp max
-  if (threadIdx.x < 32) {
-    float v = threadIdx.x < K3P_CL ? *cl.map_shared_rank(&s_max, (int)threadIdx.x) : 0.0f;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-    if (threadIdx.x == 0) s_gmax = v;
-  }
-  __syncthreads();
-  const float gm = s_gmax;
-  const int et = live ? k3_exponent(gm) : 0;
-  if (c == 0 && threadIdx.x == 0) a.e[t] = et;
-  long long s0 = 0, s1 = 0;
-  for (int64_t jb = j0 + (int64_t)threadIdx.x * 16; jb < j1; jb += K3P_SWEEP) {
-    if (!one) k3p_load16(xt, jb, a.n, live, xv);
-    int X[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) X[i] = isfinite(xv[i]) ? __float2int_rn(ldexpf(xv[i], et)) : 0;
-    uint32_t w[3][4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      uint32_t b0 = 0, b1 = 0, b2 = 0;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int Xv = X[4 * q + i];
-        const int d0 = ((Xv + 128) & 255) - 128;
-        const int X1 = (Xv - d0) >> 8;
-        const int d1 = ((X1 + 128) & 255) - 128;
-        const int d2 = (X1 - d1) >> 8;
-        b0 |= ((uint32_t)d0 & 255u) << (8 * i);
-        b1 |= ((uint32_t)d1 & 255u) << (8 * i);
-        b2 |= ((uint32_t)d2 & 255u) << (8 * i);
-      }
-      w[0][q] = b0; w[1][q] = b1; w[2][q] = b2;
-    }
-#pragma unroll
-    for (int l = 0; l < 3; ++l)
-      *reinterpret_cast<uint4*>(a.B + (int64_t)(l * K3_NR + t) * a.ldb + jb) =
-          make_uint4(w[l][0], w[l][1], w[l][2], w[l][3]);
-    if (a.rows01 && live) {
-      // plane rows are ld >= ldb bytes with zero padding: 16-byte loads
-      const uint4 p00 = *reinterpret_cast<const uint4*>(a.planes[0] + jb);
-      const uint4 p01 = *reinterpret_cast<const uint4*>(a.planes[1] + jb);
-      const bool two = a.rows > 1;
-      const uint4 p10 = two ? *reinterpret_cast<const uint4*>(a.planes[0] + a.ld + jb) : make_uint4(0, 0, 0, 0);
-      const uint4 p11 = two ? *reinterpret_cast<const uint4*>(a.planes[1] + a.ld + jb) : make_uint4(0, 0, 0, 0);
-      const uint32_t A0[4] = {p00.x, p00.y, p00.z, p00.w}, A1[4] = {p01.x, p01.y, p01.z, p01.w};
-      const uint32_t B0[4] = {p10.x, p10.y, p10.z, p10.w}, B1[4] = {p11.x, p11.y, p11.z, p11.w};
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int q = i >> 2, bb = 8 * (i & 3);
-        s0 += (long long)k3_code16(A0[q], A1[q], bb, a.P, a.sgn) * X[i];
-        s1 += (long long)k3_code16(B0[q], B1[q], bb, a.P, a.sgn) * X[i];
-      }
-    }
-  }
-  if (a.rows01) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-    }
-    if ((threadIdx.x & 31) == 0) { s_w01[threadIdx.x >> 5][0] = s0; s_w01[threadIdx.x >> 5][1] = s1; }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      long long v0 = 0, v1 = 0;
-#pragma unroll
-      for (int w = 0; w < K3P_TPB / 32; ++w) { v0 += s_w01[w][0]; v1 += s_w01[w][1]; }
-      s_01[0] = v0;
-      s_01[1] = v1;
-    }
-    cl.sync();
-    if (c == 0 && threadIdx.x < 32) {
-      long long y0 = 0, y1 = 0;
-      if (threadIdx.x < K3P_CL) {
-        const long long* p = cl.map_shared_rank(s_01, (int)threadIdx.x);
-        y0 = p[0];
-        y1 = p[1];
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        y0 += __shfl_xor_sync(0xffffffffu, y0, o);
-        y1 += __shfl_xor_sync(0xffffffffu, y1, o);
-      }
-      if (threadIdx.x == 0) {
-        a.y01[2 * t] = y0;
-        a.y01[2 * t + 1] = y1 - 2 * y0;
-      }
-    }
-  }
-  // peers read s_max / s_01 through DSMEM until here (values already consumed)
-  k3_cluster_arrive_relaxed();
-  k3_cluster_wait();
-}
-
-// ------------------------------------------------------------ K3 on row residuals
-// Residual of plan row r (plan-local): e_r = v_r - 2 v_{r-1} + v_{r-2} for
-// r >= 2; rows 0 and 1 are stored as zero and their sums computed exactly from
-// the codes (k3d_rows01), so D_0 = Y_0, D_1 = Y_1 - 2 Y_0 and Y is the double
-// prefix sum of D along rows (k3d_scan). Digits are balanced base-256.
-__device__ __forceinline__ int32_t k3d_code(const uint8_t* const* planes, int P, int sgn,
-                                            int64_t off) {
-  uint32_t u = 0;
-  for (int b = 0; b < P; ++b) u |= (uint32_t)planes[b][off] << (8 * b);
-  const int sh = 32 - 8 * P;
-  return sgn ? ((int32_t)(u << sh) >> sh) : (int32_t)u;
-}
-
-struct K3DBuild {
-  const uint8_t* planes[2];
-  int P, sgn;
-  int64_t rows, ld;
-  int64_t kbs, rtiles;
-};
-
-// digit-0 tiles: the two row tiles of a pair at the same K block are adjacent,
-// so one 256-row TMA box loads both
-__host__ __device__ inline int64_t k3d_tile0(int64_t rt, int64_t kb, int64_t kbs) {
-  return ((rt >> 1) * kbs + kb) * 2 + (rt & 1);
-}
-
-__device__ __forceinline__ int32_t k3d_resid(const K3DBuild& a, int64_t r, int64_t j) {
-  if (r < 2 || r >= a.rows) return 0;
-  const int64_t off = r * a.ld + j;
-  return k3d_code(a.planes, a.P, a.sgn, off) - 2 * k3d_code(a.planes, a.P, a.sgn, off - a.ld) +
-         k3d_code(a.planes, a.P, a.sgn, off - 2 * a.ld);
-}
-
-// one thread per (row, K block): digit count of its 64 residuals -> tile max
-__global__ void k3d_width(K3DBuild a, int* __restrict__ tilew, int* __restrict__ wmax) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= a.rows * a.kbs) return;
-  const int64_t r = t / a.kbs, kb = t - r * a.kbs;
-  int w = 1;
-  for (int q = 0; q < K3_BK; ++q) {
-    int32_t e = k3d_resid(a, r, kb * K3_BK + q);
-    int n = 1;
-    for (;;) {
-      const int32_t d = ((e + 128) & 255) - 128;
-      e = (e - d) >> 8;
-      if (e == 0) break;
-      ++n;
-    }
-    w = max(w, n);
-  }
-  atomicMax(&tilew[(r / K3_BM) * a.kbs + kb], w);
-  atomicMax(wmax, w);
-}
-
-// compact index of the tiles that need a digit-1 plane (one block)
-__global__ void k3d_index(int64_t tiles, const int* __restrict__ tilew, int* __restrict__ idx1,
-                          int64_t* __restrict__ n1) {
-  __shared__ int64_t part[1024];
-  const int t = threadIdx.x, T = blockDim.x;
-  const int64_t per = (tiles + T - 1) / T;
-  const int64_t a0 = t * per, a1 = min(tiles, a0 + per);
-  int64_t c = 0;
-  for (int64_t i = a0; i < a1; ++i) c += tilew[i] >= 2;
-  part[t] = c;
-  __syncthreads();
-  if (t == 0) {
-    int64_t acc = 0;
-    for (int i = 0; i < T; ++i) { const int64_t v = part[i]; part[i] = acc; acc += v; }
-    *n1 = acc;
-  }
-  __syncthreads();
-  int64_t acc = part[t];
-  for (int64_t i = a0; i < a1; ++i) idx1[i] = tilew[i] >= 2 ? (int)acc++ : -1;
-}
-
-// one thread per (row, K block): write the residual digits into the tiles
-__global__ void k3d_write(K3DBuild a, const int* __restrict__ idx1, uint8_t* __restrict__ t0,
-                          uint8_t* __restrict__ t1) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= a.rows * a.kbs) return;
-  const int64_t r = t / a.kbs, kb = t - r * a.kbs;
-  const int64_t tile = (r / K3_BM) * a.kbs + kb;
-  const int i1 = idx1[tile];
-  uint8_t* d0 = t0 + k3d_tile0(r / K3_BM, kb, a.kbs) * K3_A_TILE + (r % K3_BM) * K3_BK;
-  uint8_t* d1 = i1 >= 0 ? t1 + (int64_t)i1 * K3_A_TILE + (r % K3_BM) * K3_BK : nullptr;
-  for (int q0 = 0; q0 < K3_BK; q0 += 16) {
-    uint32_t w0[4] = {0, 0, 0, 0}, w1[4] = {0, 0, 0, 0};
-    for (int q = 0; q < 16; ++q) {
-      const int32_t e = k3d_resid(a, r, kb * K3_BK + q0 + q);
-      const int32_t g0 = ((e + 128) & 255) - 128;
-      const int32_t g1 = (e - g0) >> 8;
-      w0[q >> 2] |= ((uint32_t)g0 & 255u) << (8 * (q & 3));
-      w1[q >> 2] |= ((uint32_t)g1 & 255u) << (8 * (q & 3));
-    }
-    *reinterpret_cast<uint4*>(d0 + q0) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
-    if (d1) *reinterpret_cast<uint4*>(d1 + q0) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
-  }
-}
-
-// ------------------------------------------------------------ k3_post
-// From the exact int64 row sums the tensor-core pass accumulated in yacc to
-// fp32 y; one cluster of K3Q_CL CTAs per right-hand side (grid (K3Q_CL, nrhs)),
-// each CTA a contiguous block of rows in tiles of K3Q_TILE. Global memory is
-// touched only by coalesced row-strided accesses; a padded shared-memory
-// transpose gives every thread K3Q_RPT consecutive rows for the scans.
-//  * DL: yacc holds D = E X for the second-order row residuals (+ k3_prep's
-//    rows 0/1 corrections). Y is the double prefix sum of D along rows: per
-//    tile two block scans (thread sums of d, then of the thread-local second
-//    prefix), each CTA publishes (sum D, sum z, length) in shared memory and
-//    folds its predecessors' triples (DSMEM) into its carry-in
-//    (composition of consecutive blocks A, B: sumZ = sumZ_A + sumZ_B +
-//    len_B sumD_A);
-//  * byte planes: yacc holds Y itself;
-//  * y = fl32(Y 10^-m 2^-e_t); columns whose x is inf/nan (k3_prep's list)
-//    are applied as the reference loop would (zero mantissas skipped): nan if
-//    any non-zero v_ij meets a nan or both infinite signs occur, else +-inf;
-//  * yacc is reset to zero behind the read, ready for the next apply's
-//    atomic K-split partials (no memset launch).
-constexpr int K3Q_CL = 16;             // non-portable cluster size (opt-in at launch)
-constexpr int K3Q_TPB = 256;
-constexpr int K3Q_RPT = 16;
-constexpr int K3Q_TILE = K3Q_TPB * K3Q_RPT;
-constexpr int K3Q_SMEM = K3Q_TILE + K3Q_TILE / 16;   // 8-byte words, one pad per 16
-
-__device__ __forceinline__ int k3q_pad(int k) { return k + (k >> 4); }
-
-struct K3Post {
-  long long* yacc;
-  int64_t rows, n, ld;
-  const uint8_t* planes[2];
-  int P, sgn;
-  const int* e;
-  double scale;
-  int* nf_count;
-  const int* nf_cols;
-  const long long* y01;
-  const float* x;
-  int64_t ldx;
-  float* y;
-  int64_t ldy;
-};
-
-__device__ __forceinline__ long long k3q_block_excl(long long v, long long* sh) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  long long inc = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const long long u = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= o) inc += u;
-  }
-  if (lane == 31) sh[w] = inc;
-  __syncthreads();
-  if (w == 0) {
-    long long s = lane < K3Q_TPB / 32 ? sh[lane] : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const long long u = __shfl_up_sync(0xffffffffu, s, o);
-      if (lane >= o) s += u;
-    }
-    sh[lane] = s;
-  }
-  __syncthreads();
-  const long long r = inc - v + (w > 0 ? sh[w - 1] : 0);
-  __syncthreads();
-  return r;
-}
-
-// tile s (L valid rows) -> d[]: coalesced row-strided loads into padded
-// shared memory, then this thread's K3Q_RPT consecutive rows
-__device__ __forceinline__ void k3q_load(const K3Post& a, int t, int64_t s, int64_t L,
-                                         long long add0, long long add1, long long* d,
-                                         long long* sd) {
-  const long long* src = a.yacc + (int64_t)t * a.rows + s;
-#pragma unroll
-  for (int i = 0; i < K3Q_RPT; ++i) {
-    const int k = i * K3Q_TPB + threadIdx.x;
-    long long v = k < L ? src[k] : 0;
-    if (s + k == 0) v += add0;          // plan rows 0 and 1 (DL corrections; 0 otherwise)
-    if (s + k == 1) v += add1;
-    sd[k3q_pad(k)] = v;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < K3Q_RPT; ++i) d[i] = sd[k3q_pad(threadIdx.x * K3Q_RPT + i)];
-  __syncthreads();
-}
-
-// d[] -> the thread's exclusive block prefixes: ze (first prefix) and we
-// (second prefix, relative to the tile start); tile sums via the thread
-// holding the tile's last valid row
-__device__ __forceinline__ void k3q_scan(const long long* d, int64_t L, long long* sh,
-                                         long long* s_tile, long long& ze, long long& we,
-                                         long long& sD, long long& sZ) {
-  long long S = 0, C = 0;
-#pragma unroll
-  for (int i = 0; i < K3Q_RPT; ++i) { S += d[i]; C += S; }
-  ze = k3q_block_excl(S, sh);
-  const long long W = (long long)K3Q_RPT * ze + C;   // sum of the thread's second prefix
-  we = k3q_block_excl(W, sh);
-  const int64_t last = L - 1;
-  if ((int64_t)threadIdx.x == last / K3Q_RPT) {
-    const int il = (int)(last % K3Q_RPT);
-    long long cs = 0, cc = 0;
-#pragma unroll
-    for (int i = 0; i < K3Q_RPT; ++i) {
-      cs += d[i];
-      cc += ze + cs;
-      if (i == il) { s_tile[0] = ze + cs; s_tile[1] = we + cc; }
-    }
-  }
-  __syncthreads();
-  sD = s_tile[0];
-  sZ = s_tile[1];
-  __syncthreads();
-}
-
-// Y of the thread's rows (running prefixes from base_z / base_y) -> fp32 in
-// shared memory -> coalesced stores of y and zeros into yacc
-template <bool DL>
-__device__ __forceinline__ void k3q_store(const K3Post& a, int t, int64_t s, int64_t L,
-                                          const long long* d, long long base_z, long long base_y,
-                                          double sc, float* sy) {
-  long long z = base_z, yv = base_y;
-#pragma unroll
-  for (int i = 0; i < K3Q_RPT; ++i) {
-    long long Y;
-    if (DL) { z += d[i]; yv += z; Y = yv; } else { Y = d[i]; }
-    sy[k3q_pad(threadIdx.x * K3Q_RPT + i)] = (float)((double)Y * sc);
-  }
-  __syncthreads();
-  float* dst = a.y + (int64_t)t * a.ldy + s;
-  long long* acc = a.yacc + (int64_t)t * a.rows + s;
-#pragma unroll
-  for (int i = 0; i < K3Q_RPT; ++i) {
-    const int k = i * K3Q_TPB + threadIdx.x;
-    if (k < L) {
-      dst[k] = sy[k3q_pad(k)];
-      acc[k] = 0;
-    }
-  }
-  __syncthreads();
-}
-
-__device__ __forceinline__ float k3q_nonfinite(const K3Post& a, int t, int64_t r, float v, int nf) {
-  bool isn = false, pos = false, neg = false;
-  for (int k = 0; k < nf; ++k) {
-    const int64_t j = a.nf_cols[(int64_t)t * a.n + k];
-    const int64_t off = r * a.ld + j;
-    uint32_t u = a.planes[0][off];
-    if (a.P > 1) u |= (uint32_t)a.planes[1][off] << 8;
-    const int sh = 32 - 8 * a.P;
-    const int32_t q = a.sgn ? ((int32_t)(u << sh) >> sh) : (int32_t)u;
-    if (q == 0) continue;
-    const float xv = a.x[(int64_t)t * a.ldx + j];
-    if (isnan(xv)) isn = true;
-    else if ((q < 0) != (xv < 0.0f)) neg = true;
-    else pos = true;
-  }
-  if (isn || (pos && neg)) return __int_as_float(0x7fc00000);
-  if (pos) return __int_as_float(0x7f800000);
-  if (neg) return __int_as_float(0xff800000);
-  return v;
-}
-
-// columns with inf/nan x (rare): after the CTA's rows are stored
-__device__ __forceinline__ void k3q_fix_nonfinite(const K3Post& a, int t, int64_t r0, int64_t r1,
-                                                  int nf) {
-  __syncthreads();
-  for (int64_t r = r0 + threadIdx.x; r < r1; r += K3Q_TPB) {
-    float* dst = a.y + (int64_t)t * a.ldy + r;
-    *dst = k3q_nonfinite(a, t, r, *dst, nf);
-  }
-}
-
-template <bool DL>
-__global__ void __launch_bounds__(K3Q_TPB, 4) k3_post(K3Post a) {
-  asm volatile("griddepcontrol.wait;" ::: "memory");       // the tensor-core pass is complete
-  asm volatile("griddepcontrol.launch_dependents;");
-  cg::cluster_group cl = cg::this_cluster();
-  __shared__ long long sd[K3Q_SMEM];
-  __shared__ long long sh[32];
-  __shared__ long long s_tile[2];
-  __shared__ long long s_tot[3];
-  __shared__ long long s_carry[2];
-  float* sy = reinterpret_cast<float*>(sd);
-  const int t = blockIdx.y;
-  const int c = (int)cl.block_rank();
-  const int64_t per = cdiv(a.rows, K3Q_CL);
-  const int64_t r0 = min(a.rows, (int64_t)c * per), r1 = min(a.rows, r0 + per);
-  const long long add0 = DL ? a.y01[2 * t] : 0, add1 = DL ? a.y01[2 * t + 1] : 0;
-  const double sc = ldexp(a.scale, -a.e[t]);
-  const int nf = a.nf_count[t];
-  long long d[K3Q_RPT];
-  if (!DL) {
-    for (int64_t s = r0; s < r1; s += K3Q_TILE) {
-      const int64_t L = min((int64_t)K3Q_TILE, r1 - s);
-      k3q_load(a, t, s, L, 0, 0, d, sd);
-      k3q_store<false>(a, t, s, L, d, 0, 0, sc, sy);
-    }
-    if (nf > 0) {
-      k3q_fix_nonfinite(a, t, r0, r1, nf);
-      cl.sync();                     // every CTA has read nf_count[t]
-      if (c == 0 && threadIdx.x == 0) a.nf_count[t] = 0;
-    }
-    return;
-  }
-  const bool one = r1 - r0 <= K3Q_TILE;          // the rows stay in registers
-  long long ze = 0, we = 0, sD = 0, sZ = 0;
-  long long SD = 0, SZ = 0;
-  for (int64_t s = r0; s < r1; s += K3Q_TILE) {
-    const int64_t L = min((int64_t)K3Q_TILE, r1 - s);
-    k3q_load(a, t, s, L, add0, add1, d, sd);
-    k3q_scan(d, L, sh, s_tile, ze, we, sD, sZ);
-    SZ += sZ + L * SD;
-    SD += sD;
-  }
-  if (threadIdx.x == 0) { s_tot[0] = SD; s_tot[1] = SZ; s_tot[2] = r1 - r0; }
-  cl.sync();
-  // lane r of warp 0 reads the triple of peer r < c (parallel DSMEM loads);
-  // lane 0 folds them in rank order
-  if (threadIdx.x < 32) {
-    long long pd = 0, pz = 0, pl = 0;
-    if ((int)threadIdx.x < c) {
-      const long long* p = cl.map_shared_rank(s_tot, (int)threadIdx.x);
-      pd = p[0];
-      pz = p[1];
-      pl = p[2];
-    }
-    long long zi = 0, yi = 0;
-    for (int r = 0; r < c; ++r) {
-      const long long d_ = __shfl_sync(0xffffffffu, pd, r);
-      const long long z_ = __shfl_sync(0xffffffffu, pz, r);
-      const long long l_ = __shfl_sync(0xffffffffu, pl, r);
-      yi += l_ * zi + z_;
-      zi += d_;
-    }
-    if (threadIdx.x == 0) { s_carry[0] = zi; s_carry[1] = yi; }
-  }
-  k3_cluster_arrive_relaxed();     // this CTA is done reading its peers
-  __syncthreads();
-  long long Zin = s_carry[0], Yin = s_carry[1];
-  for (int64_t s = r0; s < r1; s += K3Q_TILE) {
-    const int64_t L = min((int64_t)K3Q_TILE, r1 - s);
-    if (!one) {
-      k3q_load(a, t, s, L, add0, add1, d, sd);
-      k3q_scan(d, L, sh, s_tile, ze, we, sD, sZ);
-    }
-    // row s + off + i: Z = Zin + ze + cs_i, Y = Yin + (off + i + 1) Zin + we + sum_{i'<=i} (ze + cs_i')
-    const int64_t off = (int64_t)threadIdx.x * K3Q_RPT;
-    k3q_store<true>(a, t, s, L, d, Zin + ze, Yin + off * Zin + we, sc, sy);
-    Yin += L * Zin + sZ;
-    Zin += sD;
-  }
-  if (nf > 0) k3q_fix_nonfinite(a, t, r0, r1, nf);
-  k3_cluster_wait();               // peers read s_tot through DSMEM until here
-  if (c == 0 && threadIdx.x == 0 && nf > 0) a.nf_count[t] = 0;   // every CTA read it above
-}
-
 // ------------------------------------------------------------ host side
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                     const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -1394,7 +1410,24 @@ static int make_map_u8(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t
   return INVOP_OK;
 }
 
-// k3_prep / k3_post run as one cluster of CL CTAs per right-hand side
+// a plain grid launched as a programmatic dependent of the preceding kernel
+template <typename Kern, typename Arg>
+static int launch_pdl(Kern kern, const Arg& arg, dim3 grid, int threads, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  INVOP_CUDA(cudaLaunchKernelEx(&cfg, kern, arg));
+  return INVOP_OK;
+}
+
+// k3_post runs as one cluster of CL CTAs per right-hand side
 // (CL = 16 is a non-portable size, opted in here)
 template <typename Kern, typename Arg>
 static int launch_cluster(Kern kern, const Arg& arg, int nr, int threads, int cl, cudaStream_t s) {
@@ -1441,6 +1474,7 @@ static int launch_k3(const CUtensorMap& a0, const CUtensorMap& a1, const CUtenso
 static int k3_pair_slots() {
   static int slots = 0;
   if (!slots) {
+    int n = num_sms() / 2;
     if (cudaFuncSetAttribute(k3_dl2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3Q2_SMEM) !=
         cudaSuccess)
       return num_sms() / 2;
@@ -1448,13 +1482,14 @@ static int k3_pair_slots() {
     cfg.gridDim = dim3(num_sms());
     cfg.blockDim = dim3(K3_THREADS);
     cfg.dynamicSmemBytes = K3Q2_SMEM;
-    int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, k3_dl2, &cfg) != cudaSuccess || n <= 0) n = num_sms() / 2;
-    slots = std::min(n, num_sms() / 2);
+    int m = 0;
+    if (cudaOccupancyMaxActiveClusters(&m, k3_dl2, &cfg) == cudaSuccess && m > 0) n = std::min(n, m);
+    slots = n;
   }
   return slots;
 }
 
+// launched as a programmatic dependent of k3_digits
 static int launch_k3_dl2(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& bh,
                          const K3PairArgs& args, int clusters, cudaStream_t s) {
   cudaError_t e = cudaFuncSetAttribute(k3_dl2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3Q2_SMEM);
@@ -1647,7 +1682,8 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
   const size_t e_off = round_up(b_bytes, 256);
   const size_t nfc_off = e_off + 256;
   const size_t y01_off = nfc_off + 256;                   // [64][2] int64
-  const size_t acc_off = y01_off + 1024;
+  const size_t maxb_off = y01_off + 1024;                 // [64] max|x_t| bits
+  const size_t acc_off = maxb_off + 256;
   const size_t acc_bytes = (size_t)K3_NR * p->rows * 8;
   const size_t nfl_off = round_up(acc_off + acc_bytes, 256);
   const size_t ws_bytes = nfl_off + (size_t)K3_NR * p->n * 4;
@@ -1660,6 +1696,7 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
   int* e = (int*)((char*)p->k3_ws + e_off);
   int* nfc = (int*)((char*)p->k3_ws + nfc_off);
   long long* y01 = (long long*)((char*)p->k3_ws + y01_off);
+  unsigned int* maxb = (unsigned int*)((char*)p->k3_ws + maxb_off);
   long long* yacc = (long long*)((char*)p->k3_ws + acc_off);
   int* nfl = (int*)((char*)p->k3_ws + nfl_off);
   int rc = INVOP_OK;
@@ -1690,13 +1727,28 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
     // 1. max|x_t| per right-hand side, exponents, digits, non-finite columns
     K3Prep pr;
     pr.x = x + t0 * ldx; pr.n = p->n; pr.ldx = ldx; pr.nrhs = nr;
-    pr.B = B; pr.ldb = ldb; pr.e = e; pr.nf_count = nfc; pr.nf_cols = nfl;
+    pr.B = B; pr.ldb = ldb; pr.e = e; pr.maxbits = maxb; pr.nf_count = nfc; pr.nf_cols = nfl;
     pr.planes[0] = p->planes[0];
     pr.planes[1] = p->planes[p->P > 1 ? 1 : 0];
     pr.ld = p->ld; pr.rows = p->rows; pr.P = p->P; pr.sgn = p->is_signed;
-    pr.rows01 = dl ? 1 : 0; pr.y01 = y01;
-    rc = launch_cluster(k3_prep, pr, K3_NR, K3P_TPB, K3P_CL, s);
+    pr.rows01 = dl ? 1 : 0; pr.y01 = (unsigned long long*)y01;
+    // 3. (arguments) rows 0/1 + double prefix (DL), scaling, non-finite
+    // columns, y
+    K3Post q;
+    q.yacc = yacc; q.rows = p->rows; q.n = p->n; q.ld = p->ld;
+    q.planes[0] = p->planes[0];
+    q.planes[1] = p->planes[p->P > 1 ? 1 : 0];
+    q.P = p->P; q.sgn = p->is_signed;
+    q.e = e; q.scale = p->scale;
+    q.nf_count = nfc; q.nf_cols = nfl; q.y01 = y01; q.maxbits = maxb;
+    q.x = x + t0 * ldx; q.ldx = ldx;
+    q.y = y + t0 * ldy; q.ldy = ldy;
+    int grid = (int)std::min<int64_t>(slots, pairs * splits);
+#if !defined(K3_PROBE_NOSIDE) && !defined(K3_PROBE_NOPREP)
+    rc = launch_pdl(k3_xmax, pr, dim3((unsigned)cdiv(p->n, K3X_COLS), K3_NR), K3X_TPB, s);
+    if (!rc) rc = launch_pdl(k3_digits, pr, dim3((unsigned)cdiv(ldb, K3G_COLS), K3_NR), K3G_TPB, s);
     if (rc) return rc;
+#endif
     // 2. the tensor-core pass: exact int64 row sums into yacc
     K3Args a;
     a.idx1 = p->k3d_idx1;
@@ -1704,7 +1756,6 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
     a.kblocks_total = kblocks; a.kblocks_per_unit = kpu; a.splits = splits;
     a.kb_stride = (int)(p->ld / K3_BK);
     a.pairs = pairs; a.nrhs = nr; a.yacc = yacc;
-    int grid = (int)std::min<int64_t>(slots, pairs * splits);
     const CUtensorMap* A0 = (const CUtensorMap*)(dl ? p->k3d_mapA[0] : p->k3_mapA[0]);
     const CUtensorMap* A1 = (const CUtensorMap*)(dl ? p->k3d_mapA[1] : p->k3_mapA[1]);
     const int key = dl ? 999 : p->P * 100 + tiles * 10 + stages;
@@ -1729,20 +1780,12 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
       default: return fail(INVOP_E_VALUE, "unsupported INVOP_K3_CFG");
     }
     if (rc) return rc;
-    // 3. rows 0/1 + double prefix (DL), scaling, non-finite columns, y
-    K3Post q;
-    q.yacc = yacc; q.rows = p->rows; q.n = p->n; q.ld = p->ld;
-    q.planes[0] = p->planes[0];
-    q.planes[1] = p->planes[p->P > 1 ? 1 : 0];
-    q.P = p->P; q.sgn = p->is_signed;
-    q.e = e; q.scale = p->scale;
-    q.nf_count = nfc; q.nf_cols = nfl; q.y01 = y01;
-    q.x = x + t0 * ldx; q.ldx = ldx;
-    q.y = y + t0 * ldy; q.ldy = ldy;
+#if !defined(K3_PROBE_NOSIDE) && !defined(K3_PROBE_NOPOST)
     rc = dl ? launch_cluster(k3_post<true>, q, nr, K3Q_TPB, K3Q_CL, s)
             : launch_cluster(k3_post<false>, q, nr, K3Q_TPB, K3Q_CL, s);
+#endif
     if (rc) return rc;
-    INVOP_LAUNCHED(3);   // k3_prep + k3_batched + k3_post
+    INVOP_LAUNCHED(4);   // k3_xmax + k3_digits + k3_batched / k3_dl2 + k3_post
   }
   return INVOP_OK;
 }
