@@ -396,12 +396,17 @@ def run_ours(args, world, rank, local):
     def launch_fast():
         L.lib.invop_apply(h, x32.data_ptr(), N, mine.data_ptr(), pad, k, L.F32, L.MODE_FAST, sptr)
 
-    def step():
-        launch_fast()
+    def step_eager():
+        # the stream is looked up per call: under graph capture it is the
+        # capture stream
+        sp = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        L.lib.invop_apply(h, x32.data_ptr(), N, mine.data_ptr(), pad, k, L.F32, L.MODE_FAST, sp)
         if world > 1:
             torch.distributed.all_gather_into_tensor(stage.view(-1), mine.reshape(-1))
             L.lib.invop_unshard(stage.data_ptr(), world, offs.ctypes.data, k, pad, Y.data_ptr(), N,
-                                L.F32, sptr)
+                                L.F32, sp)
+
+    step = step_eager
 
     L.check(L.lib.invop_apply(h, x32.data_ptr(), N, mine.data_ptr(), pad, k, L.F32, L.MODE_FAST,
                               sptr), "apply")
@@ -421,6 +426,40 @@ def run_ours(args, world, rank, local):
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
+    # N > 1: a step is three launches and a collective issued from Python; at a
+    # few GPUs the per-step host time exceeds the per-rank device time, so the
+    # step is captured once in a CUDA graph (apply + all-gather + unshard) and
+    # replayed. Kept eager if capture fails (the line says which). N = 1 stays
+    # eager: consecutive k2_dl applies overlap as programmatic dependents.
+    graph_used = False
+    graph_launches = 0
+    if (world > 1 or os.environ.get("INVOP_BENCH_GRAPH")) and not os.environ.get("INVOP_BENCH_NO_GRAPH"):
+        try:
+            g = torch.cuda.CUDAGraph()
+            cs = torch.cuda.Stream()
+            cs.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(cs):
+                step_eager()                       # warm the capture stream
+            torch.cuda.current_stream().wait_stream(cs)
+            torch.cuda.synchronize()
+            lcg = L.lib.invop_launch_count()
+            with torch.cuda.graph(g, stream=cs):
+                step_eager()
+            graph_launches = L.lib.invop_launch_count() - lcg      # library kernels per replay
+            torch.cuda.synchronize()
+            g.replay()
+            torch.cuda.synchronize()
+            step = g.replay
+            graph_used = True
+        except Exception as e:  # noqa: BLE001
+            print("bench: CUDA graph capture failed, eager steps (%s)" % e, file=sys.stderr)
+            torch.cuda.synchronize()
+        if world > 1:
+            ok = torch.tensor([1 if graph_used else 0], device=dev)
+            torch.distributed.all_reduce(ok, op=torch.distributed.ReduceOp.MIN)
+            if int(ok.item()) == 0:
+                step, graph_used = step_eager, False    # every rank the same way
+            torch.distributed.barrier()
 
     def timed(fn, reps, sync_each=False):
         """Device ms of `reps` calls of fn (CUDA events on the launching stream);
@@ -455,6 +494,8 @@ def run_ours(args, world, rank, local):
         lc0 = L.lib.invop_launch_count()
         ms = timed(step, args.steps)
         launches = L.lib.invop_launch_count() - lc0
+        if graph_used:                    # replays do not pass through the library
+            launches = graph_launches * args.steps
     if world > 1:
         torch.distributed.barrier()
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -571,6 +612,7 @@ def run_ours(args, world, rank, local):
             "e2e": {"value": k * e2e_steps / e2e_s, "unit": UNIT,
                     "h2d_bytes_per_step": e2e_h2d, "d2h_bytes_per_step": e2e_d2h, "path": e2e_path},
             "gpu_launches": launches,
+            "cuda_graph": graph_used,
             "clocks": clk.summary(),
             "ordered_fp64": {"value": k * 1e3 / ord_ms, "unit": UNIT, "kernel_ms": ord_ms,
                              "operator_bytes": ord_bytes,
