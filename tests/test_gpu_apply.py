@@ -532,6 +532,34 @@ def test_row_shards_reassemble_exactly(invop, O, key, shards):
     assert torch.equal(torch.cat(parts32), y32)
 
 
+@pytest.mark.parametrize("n,shards,k", [(64, 2, 64), (64, 3, 40), (50, 4, 17)])
+def test_row_shards_batched_reassemble_exactly(invop, O, n, shards, k):
+    """The multi-RHS (tensor-core, SM-pair) route on row shards: every shard
+    restarts its residual chain and takes its own rows 0/1 from the codes, and
+    the exact integer sums make the concatenated shards equal to the whole
+    operator's result bit for bit (config 5's multi-GPU split, small)."""
+    import torch
+    from paper_1602_00001_b200.sharded import shard_rows
+
+    st = invop.uniform_interior(n)
+    N = st.n
+    dop = invop.DeviceOperator(st).factor()
+    full = dop.quantized_rows(4)
+    rng = np.random.default_rng(n + shards + k)
+    X = torch.tensor(rng.standard_normal((k, N)), device="cuda", dtype=torch.float32)
+    Y = full.apply_device(X, mode=0)
+    assert full.apply_kernel(k) in ("k3_dl2", "k3_batched")
+    parts = []
+    for r in range(shards):
+        row0, rows = shard_rows(N, shards, r)
+        sh = dop.quantized_rows(4, row0, rows)
+        parts.append(sh.apply_device(X, mode=0))
+    assert torch.equal(torch.cat(parts, dim=1), Y)
+    Yo = O.ordered_apply(full.decode().cpu().numpy(), 4, X.cpu().numpy().astype(np.float64))
+    for t in (0, k - 1):
+        assert relerr(Y[t].cpu().numpy(), Yo[t]) <= F32_TOL
+
+
 @pytest.mark.parametrize("cons", [8, 16])
 @pytest.mark.parametrize("signed", [False, True])
 @pytest.mark.parametrize("N", [8192, 9000, 16384])
