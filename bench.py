@@ -117,11 +117,22 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ dist
+def _dist1() -> bool:
+    """INVOP_BENCH_DIST1=1: run the N>1 code path (NCCL all-gather, unshard,
+    graph capture) with a one-rank process group - the only way to exercise it
+    on a one-GPU box."""
+    return bool(os.environ.get("INVOP_BENCH_DIST1"))
+
+
 def dist_init(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world > 1 or (_dist1() and args.impl == "ours"):
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
         import torch
         import torch.distributed as dist
 
@@ -365,6 +376,9 @@ def run_ours(args, world, rank, local):
 
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
+    # the sharded step (apply + all-gather + unshard, graph capture, max over
+    # ranks); INVOP_BENCH_DIST1 takes it with a one-rank group as well
+    multi = world > 1 or _dist1()
     cfg = configs.get(args.config)
     st = cfg.operator()
     N = st.n
@@ -401,7 +415,7 @@ def run_ours(args, world, rank, local):
         # capture stream
         sp = C.c_void_p(torch.cuda.current_stream().cuda_stream)
         L.lib.invop_apply(h, x32.data_ptr(), N, mine.data_ptr(), pad, k, L.F32, L.MODE_FAST, sp)
-        if world > 1:
+        if multi:
             torch.distributed.all_gather_into_tensor(stage.view(-1), mine.reshape(-1))
             L.lib.invop_unshard(stage.data_ptr(), world, offs.ctypes.data, k, pad, Y.data_ptr(), N,
                                 L.F32, sp)
@@ -424,7 +438,7 @@ def run_ours(args, world, rank, local):
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
-    if world > 1:
+    if multi:
         torch.distributed.barrier()
     # N > 1: a step is three launches and a collective issued from Python; at a
     # few GPUs the per-step host time exceeds the per-rank device time, so the
@@ -433,7 +447,7 @@ def run_ours(args, world, rank, local):
     # eager: consecutive k2_dl applies overlap as programmatic dependents.
     graph_used = False
     graph_launches = 0
-    if (world > 1 or os.environ.get("INVOP_BENCH_GRAPH")) and not os.environ.get("INVOP_BENCH_NO_GRAPH"):
+    if (multi or os.environ.get("INVOP_BENCH_GRAPH")) and not os.environ.get("INVOP_BENCH_NO_GRAPH"):
         try:
             g = torch.cuda.CUDAGraph()
             cs = torch.cuda.Stream()
@@ -454,7 +468,7 @@ def run_ours(args, world, rank, local):
         except Exception as e:  # noqa: BLE001
             print("bench: CUDA graph capture failed, eager steps (%s)" % e, file=sys.stderr)
             torch.cuda.synchronize()
-        if world > 1:
+        if multi:
             ok = torch.tensor([1 if graph_used else 0], device=dev)
             torch.distributed.all_reduce(ok, op=torch.distributed.ReduceOp.MIN)
             if int(ok.item()) == 0:
@@ -489,14 +503,14 @@ def run_ours(args, world, rank, local):
 
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
-        if world > 1:
+        if multi:
             torch.distributed.barrier()
         lc0 = L.lib.invop_launch_count()
         ms = timed(step, args.steps)
         launches = L.lib.invop_launch_count() - lc0
         if graph_used:                    # replays do not pass through the library
             launches = graph_launches * args.steps
-    if world > 1:
+    if multi:
         torch.distributed.barrier()
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -521,7 +535,7 @@ def run_ours(args, world, rank, local):
     ord_ms = timed(launch_ordered, oreps) / oreps
 
     # ---- end to end with host buffers
-    if world == 1:
+    if not multi:
         xh = torch.from_numpy(np.ascontiguousarray(X)).pin_memory()        # fp64 host
         yh = torch.empty((k, rows), dtype=torch.float64).pin_memory()
 
@@ -545,14 +559,14 @@ def run_ours(args, world, rank, local):
     for _ in range(2):
         e2e_step()
     e2e_steps = max(10, min(args.steps, 1000 if k == 1 else 30))
-    if world > 1:
+    if multi:
         torch.distributed.barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         e2e_step()
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
-    if world > 1:
+    if multi:
         t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_s = float(t.item())
@@ -560,11 +574,11 @@ def run_ours(args, world, rank, local):
     # ---- result of this run: full Y (gathered), fp32 vs the ordered fp64 path
     step()
     torch.cuda.synchronize()
-    y32 = (Y if world > 1 else mine[:, :rows]).double()
+    y32 = (Y if multi else mine[:, :rows]).double()
     y32_local = mine[:, :rows].double()
     err = float(((y32_local - y64).abs().amax(dim=1) / y64.abs().amax(dim=1)).max().item())
     Yh = y32.cpu().numpy()
-    if world > 1:
+    if multi:
         t = torch.tensor([err], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         err = float(t.item())
@@ -575,7 +589,7 @@ def run_ours(args, world, rank, local):
     achieved = alg_bytes / (k_ms * 1e-3) / 1e9
     traffic = None
     prof = ROOT / "profiles" / ("ncu_cfg%d_%s.json" % (cfg.key, kname))
-    if prof.exists() and world == 1 and (not args.nrhs or args.nrhs == cfg.nrhs):
+    if prof.exists() and not multi and (not args.nrhs or args.nrhs == cfg.nrhs):
         try:
             traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
         except Exception:  # noqa: BLE001
@@ -583,7 +597,7 @@ def run_ours(args, world, rank, local):
 
     result = None
     if rank == 0:
-        mults, adds = plan.counts() if (world == 1 and N <= 16384) else (None, plan.counts()[1])
+        mults, adds = plan.counts() if (not multi and N <= 16384) else (None, plan.counts()[1])
         value = k * args.steps / (ms * 1e-3)
         result = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -636,7 +650,7 @@ def run_ours(args, world, rank, local):
                 "value": quantization_error(cfg, X.astype(np.float32), Yh), "digits": cfg.digits,
                 "vs": "direct sparse solve of the unquantized operator (scipy splu), same fp32 x; "
                       "max_i |y - y_exact| / max_i |y_exact|, worst RHS"}
-        if world == 1 and not args.no_cpu_baseline:
+        if not multi and not args.no_cpu_baseline:
             result["cpu_baseline"] = cpu_baseline(cfg, budget_s=args.cpu_budget)
     return result
 
@@ -661,7 +675,7 @@ def main():
         res = run_ours(args, world, rank, local)
         if rank == 0 and res is not None:
             print(json.dumps(res), flush=True)
-    if world > 1:
+    if world > 1 or (_dist1() and args.impl == "ours"):
         import torch.distributed as dist
 
         dist.barrier()
