@@ -20,10 +20,7 @@
 //
 //  * k2_ordered (INVOP_MODE_ORDERED): the bitwise contract of the reference —
 //    each output row accumulates t=(v*10^-m)*x_j in ascending j, fp64, no FMA,
-//    zero mantissas skipped (applyplan.py:4-8). One thread per row; each warp
-//    runs its own cp.async pipeline that stages a 32-row x 128-column tile of
-//    every byte plane in XOR-swizzled shared memory so the per-thread row walk
-//    is conflict-free LDS.128.
+//    zero mantissas skipped (applyplan.py:4-8). Lives in ordered.cu.
 #include "common.cuh"
 #include "ptx.cuh"
 #include <algorithm>
@@ -579,302 +576,6 @@ int apply_fast_launch(const invop_plan* p, const float* x, int64_t ldx, float* y
       case 7: rc = launch_fast_p<3, true>(a, KR, grid, s); break;
       case 8: rc = launch_fast_p<4, false>(a, KR, grid, s); break;
       default: rc = launch_fast_p<4, true>(a, KR, grid, s); break;
-    }
-    if (rc) return rc;
-    k0 += KR;
-  }
-  return INVOP_OK;
-}
-
-// --------------------------------------------------------------- k2_ordered
-constexpr int ORD_TILE = 128;   // columns per stage
-constexpr int ORD_STAGES = 4;
-
-struct OrdArgs {
-  const uint8_t* planes[8];
-  int64_t rows, n, ld;
-  double scale;
-  double neg_scale52;   // -(2^52 * scale), exact
-  const double* x;
-  int64_t ldx;
-  double* y;
-  int64_t ldy;
-  // accumulate mode (the reference seam's `out +=` contract, _native.pyx:43-46):
-  // each row's chain starts at y[row] instead of +0, and zero codes are
-  // skipped outright (the reference never adds them; -0 + +0 would be +0)
-  int accumulate;
-};
-
-__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N));
-}
-
-template <int P, bool SIGNED>
-__device__ __forceinline__ double code_to_double(const uint8_t* bytes) {
-  if (P <= 4 && !SIGNED) {
-    uint32_t u = 0;
-#pragma unroll
-    for (int b = 0; b < P; ++b) u |= (uint32_t)bytes[b] << (8 * b);
-    // 2^52 + u, exact
-    return __dadd_rn(__hiloint2double(0x43300000, (int)u), -4503599627370496.0);
-  } else {
-    uint64_t u = 0;
-#pragma unroll
-    for (int b = 0; b < P; ++b) u |= (uint64_t)bytes[b] << (8 * b);
-    int64_t v;
-    if (SIGNED && P < 8) {
-      const int sh = 64 - 8 * P;
-      v = (int64_t)(u << sh) >> sh;
-    } else {
-      v = (int64_t)u;
-    }
-    return (double)v;  // exact for |v| <= 2^53 (quantize guarantees it)
-  }
-}
-
-// KR right-hand sides per pass
-template <int P, bool SIGNED, int KR>
-__global__ void __launch_bounds__(128) k2_ordered(OrdArgs a) {
-  extern __shared__ __align__(128) unsigned char sm[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int CODE_BYTES = 32 * ORD_TILE;                 // per plane per stage
-  constexpr int X_BYTES = ORD_TILE * 8 * KR;                // per stage
-  constexpr int STAGE_BYTES = CODE_BYTES * P + X_BYTES;
-  unsigned char* wbase = sm + (size_t)warp * STAGE_BYTES * ORD_STAGES;
-  const uint32_t wbase_s = (uint32_t)__cvta_generic_to_shared(wbase);
-
-  const int64_t row0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * 32;
-  if (row0 >= a.rows) return;  // whole warp idle (warp-uniform)
-  const int64_t myrow = row0 + lane;
-  const int64_t ntiles = (a.n + ORD_TILE - 1) / ORD_TILE;
-
-  auto issue = [&](int64_t tile, int stage) {
-    if (tile < ntiles) {
-      const int64_t col0 = tile * ORD_TILE;
-      const uint32_t sb = wbase_s + stage * STAGE_BYTES;
-#pragma unroll
-      for (int b = 0; b < P; ++b) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          int cid = lane + 32 * i;         // 256 chunks = 32 rows x 8 chunks
-          int r = cid >> 3, c = cid & 7;
-          int64_t gr = row0 + r;
-          gr = gr < a.rows ? gr : a.rows - 1;
-          const uint8_t* src = a.planes[b] + gr * a.ld + col0 + c * 16;
-          uint32_t dst = sb + b * CODE_BYTES + r * 128 + ((c ^ (r & 7)) << 4);
-          cp_async16(dst, src);
-        }
-      }
-      // x tile: ORD_TILE doubles per rhs = 64 chunks of 16 B
-#pragma unroll
-      for (int k = 0; k < KR; ++k) {
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          int cid = lane + 32 * i;
-          int64_t col = col0 + cid * 2;
-          uint32_t dst = sb + P * CODE_BYTES + k * ORD_TILE * 8 + cid * 16;
-          if (col + 1 < a.n) {
-            cp_async16(dst, a.x + k * a.ldx + col);
-          } else {
-            // tail: scalar copy with zero fill (synchronous store)
-            double* d = reinterpret_cast<double*>(wbase + stage * STAGE_BYTES +
-                                                  P * CODE_BYTES + k * ORD_TILE * 8 + cid * 16);
-            d[0] = col < a.n ? a.x[k * a.ldx + col] : 0.0;
-            d[1] = 0.0;
-          }
-        }
-      }
-    }
-    cp_async_commit();
-  };
-
-#pragma unroll
-  for (int s = 0; s < ORD_STAGES - 1; ++s) issue(s, s);
-
-  double acc[KR];
-#pragma unroll
-  for (int k = 0; k < KR; ++k)
-    acc[k] = (a.accumulate && myrow < a.rows) ? a.y[k * a.ldy + myrow] : 0.0;
-  const int sr = lane;  // my row inside the tile
-  for (int64_t t = 0; t < ntiles; ++t) {
-    issue(t + ORD_STAGES - 1, (int)((t + ORD_STAGES - 1) % ORD_STAGES));
-    cp_async_wait<ORD_STAGES - 1>();
-    __syncwarp();
-    const unsigned char* sb = wbase + (t % ORD_STAGES) * STAGE_BYTES;
-    const double* xs = reinterpret_cast<const double*>(sb + P * CODE_BYTES);
-    const int64_t col0 = t * ORD_TILE;
-    const int cend = (int)min((int64_t)ORD_TILE, a.n - col0);
-    bool fin = true;
-#pragma unroll
-    for (int k = 0; k < KR; ++k)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) fin = fin && isfinite(xs[k * ORD_TILE + lane * 4 + i]);
-    const bool masked = a.accumulate || __any_sync(0xffffffffu, !fin);
-    // All 8 chunks of the tile unrolled, so the independent decode / product
-    // work of chunk c+1 overlaps the ordered DADD chain of chunk c.
-    // For finite x, adding (0*10^-m)*x_j = +-0 leaves the accumulator bitwise
-    // unchanged (it starts at +0 and x+(-x) rounds to +0), so the reference's
-    // zero skip only matters when the tile holds inf/nan: then the product of
-    // a zero code is replaced by +0.
-    // Straight-line tile (8 chunks of 16 codes, no guards: the padding past n
-    // holds zero codes and zero x, whose +0 products leave the accumulator
-    // unchanged), so ptxas can overlap the decode / products of later chunks
-    // with the ordered DADD chain of earlier ones. Two instantiations: with and
-    // without the inf/nan zero-skip select, chosen once per tile.
-    auto tile_pass = [&](auto masked_tag) {
-      constexpr bool MASKED = decltype(masked_tag)::value;
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      {
-        uint4 w[P];
-#pragma unroll
-        for (int b = 0; b < P; ++b)
-          w[b] = *reinterpret_cast<const uint4*>(sb + b * CODE_BYTES + sr * 128 +
-                                                 ((c ^ (sr & 7)) << 4));
-        double d[16];
-        if constexpr (P <= 4) {
-          // PRMT-assembled int32 codes, exact conversion by the 2^52 magic
-#pragma unroll
-          for (int wd = 0; wd < 4; ++wd) {
-            uint32_t wds[4];
-#pragma unroll
-            for (int b = 0; b < P; ++b) wds[b] = u4get(w[b], wd);
-            int32_t uv[4];
-            if (P == 4 && !SIGNED) {
-              const uint32_t t01 = prmt(wds[0], wds[1], 0x5140), t23 = prmt(wds[0], wds[1], 0x7362);
-              const uint32_t h01 = prmt(wds[P > 2 ? 2 : 0], wds[P > 3 ? 3 : 0], 0x5140);
-              const uint32_t h23 = prmt(wds[P > 2 ? 2 : 0], wds[P > 3 ? 3 : 0], 0x7362);
-              uv[0] = (int32_t)prmt(t01, h01, 0x5410); uv[1] = (int32_t)prmt(t01, h01, 0x7632);
-              uv[2] = (int32_t)prmt(t23, h23, 0x5410); uv[3] = (int32_t)prmt(t23, h23, 0x7632);
-            } else {
-              dec_int4<P, SIGNED>(wds, uv);
-            }
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              // fl(|v| * 10^-m) in ONE fp64 operation: V = 2^52 + |v| is built
-              // from bits, and fma(V, s, -2^52 s) = round((2^52 + |v|) s - 2^52 s)
-              // = round(|v| s) exactly, because 2^52 s is exact (a power-of-two
-              // multiple of the double s). The sign is applied to the rounded
-              // coefficient (rounding to nearest is sign-symmetric), as the
-              // reference applies it to its products (_native.pyx:43-46).
-              if (SIGNED) {
-                const int32_t sv = uv[i];
-                const int32_t sm = sv >> 31;
-                const uint32_t av = (uint32_t)((sv ^ sm) - sm);
-                const double c = __fma_rn(__hiloint2double(0x43300000, (int)av), a.scale, a.neg_scale52);
-                d[4 * wd + i] = __hiloint2double(__double2hiint(c) ^ (int)((uint32_t)sm & 0x80000000u),
-                                                 __double2loint(c));
-              } else {
-                d[4 * wd + i] = __fma_rn(__hiloint2double(0x43300000, uv[i]), a.scale, a.neg_scale52);
-              }
-            }
-          }
-        } else {
-#pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            uint8_t bytes[P];
-#pragma unroll
-            for (int b = 0; b < P; ++b) bytes[b] = (uint8_t)(u4get(w[b], q >> 2) >> (8 * (q & 3)));
-            d[q] = __dmul_rn(code_to_double<P, SIGNED>(bytes), a.scale);
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < KR; ++k) {
-          const double2* xk = reinterpret_cast<const double2*>(xs + k * ORD_TILE + c * 16);
-          double t[16];
-#pragma unroll
-          for (int q2 = 0; q2 < 8; ++q2) {
-            double2 xv = xk[q2];
-            t[2 * q2] = __dmul_rn(d[2 * q2], xv.x);
-            t[2 * q2 + 1] = __dmul_rn(d[2 * q2 + 1], xv.y);
-          }
-          if (MASKED) {
-            // the reference's zero skip (_native.pyx:32-46 never sees a zero
-            // mantissa): the chain does not advance on a zero code
-#pragma unroll
-            for (int q = 0; q < 16; ++q) acc[k] = d[q] != 0.0 ? __dadd_rn(acc[k], t[q]) : acc[k];
-          } else {
-#pragma unroll
-            for (int q = 0; q < 16; ++q) acc[k] = __dadd_rn(acc[k], t[q]);
-          }
-        }
-      }
-    }
-    };
-    if (masked) tile_pass(std::true_type{});
-    else tile_pass(std::false_type{});
-    __syncwarp();
-  }
-  cp_async_wait<0>();
-  if (myrow < a.rows) {
-#pragma unroll
-    for (int k = 0; k < KR; ++k) a.y[k * a.ldy + myrow] = acc[k];
-  }
-}
-
-template <int P, bool SIGNED, int KR>
-static int launch_ord_t(OrdArgs a, cudaStream_t s) {
-  constexpr int STAGE_BYTES = 32 * ORD_TILE * P + ORD_TILE * 8 * KR;
-  size_t per_warp = (size_t)STAGE_BYTES * ORD_STAGES;
-  // 2 warps (64 rows) per block: small blocks pack 2-3 per SM so all row
-  // warps of a 16K-row operator are resident in a single wave
-  int wpb = (int)std::max<size_t>(1, std::min<size_t>(2, (200 * 1024) / per_warp));
-  size_t smem = per_warp * wpb;
-  auto kern = k2_ordered<P, SIGNED, KR>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int64_t warps = cdiv(a.rows, 32);
-  int64_t grid = cdiv(warps, wpb);
-  kern<<<(unsigned)grid, wpb * 32, smem, s>>>(a);
-  INVOP_LAUNCHED(1);
-  INVOP_CHECK_LAUNCH("k2_ordered");
-  return INVOP_OK;
-}
-
-template <int P, bool SIGNED>
-static int launch_ord_p(OrdArgs a, int KR, cudaStream_t s) {
-  if (KR >= 4 && P <= 4) return launch_ord_t<P, SIGNED, 4>(a, s);
-  if (KR >= 2) return launch_ord_t<P, SIGNED, 2>(a, s);
-  return launch_ord_t<P, SIGNED, 1>(a, s);
-}
-
-int apply_ordered_launch(const invop_plan* p, const double* x, int64_t ldx, double* y,
-                         int64_t ldy, int64_t nrhs, cudaStream_t s, bool accumulate) {
-  if (p->rows == 0 || nrhs == 0) return INVOP_OK;
-  for (int64_t k0 = 0; k0 < nrhs;) {
-    int KR = nrhs - k0 >= 4 && p->P <= 4 ? 4 : (nrhs - k0 >= 2 ? 2 : 1);
-    OrdArgs a;
-    for (int b = 0; b < 8; ++b) a.planes[b] = p->planes[b < p->P ? b : 0];
-    a.rows = p->rows; a.n = p->n; a.ld = p->ld; a.scale = p->scale;
-    a.neg_scale52 = -ldexp(p->scale, 52);
-    a.x = x + k0 * ldx; a.ldx = ldx;
-    a.y = y + k0 * ldy; a.ldy = ldy;
-    a.accumulate = accumulate ? 1 : 0;
-    int rc;
-    // non-negative codes in signed planes decode identically as unsigned
-    // (the cheaper coefficient path)
-    const int sgn = p->is_signed && p->min_val < 0 ? 1 : 0;
-    switch (p->P * 2 + sgn) {
-      case 2: rc = launch_ord_p<1, false>(a, KR, s); break;
-      case 3: rc = launch_ord_p<1, true>(a, KR, s); break;
-      case 4: rc = launch_ord_p<2, false>(a, KR, s); break;
-      case 5: rc = launch_ord_p<2, true>(a, KR, s); break;
-      case 6: rc = launch_ord_p<3, false>(a, KR, s); break;
-      case 7: rc = launch_ord_p<3, true>(a, KR, s); break;
-      case 8: rc = launch_ord_p<4, false>(a, KR, s); break;
-      case 9: rc = launch_ord_p<4, true>(a, KR, s); break;
-      case 10: rc = launch_ord_p<5, false>(a, KR, s); break;
-      case 11: rc = launch_ord_p<5, true>(a, KR, s); break;
-      case 12: rc = launch_ord_p<6, false>(a, KR, s); break;
-      case 13: rc = launch_ord_p<6, true>(a, KR, s); break;
-      case 14: rc = launch_ord_p<7, false>(a, KR, s); break;
-      case 15: rc = launch_ord_p<7, true>(a, KR, s); break;
-      case 16: rc = launch_ord_p<8, false>(a, KR, s); break;
-      default: rc = launch_ord_p<8, true>(a, KR, s); break;
     }
     if (rc) return rc;
     k0 += KR;

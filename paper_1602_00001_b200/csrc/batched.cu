@@ -1395,19 +1395,27 @@ static PFN_encodeTiled encode_fn() {
   return fn;
 }
 
-static int make_map_u8(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer,
-                       uint64_t pitch, uint32_t box_inner, uint32_t box_outer) {
+int make_tensor_map_u8(void* map128, const void* ptr, uint64_t inner, uint64_t outer,
+                       uint64_t pitch, uint32_t box_inner, uint32_t box_outer, int swizzle_bytes) {
   PFN_encodeTiled enc = encode_fn();
   if (!enc) return fail(INVOP_E_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {inner, outer};
   cuuint64_t strides[1] = {pitch};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t es[2] = {1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(ptr), dims, strides, box,
-                   es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+  const CUtensorMapSwizzle sw = swizzle_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                      : CU_TENSOR_MAP_SWIZZLE_NONE;
+  CUresult r = enc((CUtensorMap*)map128, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(ptr),
+                   dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(INVOP_E_CUDA, "cuTensorMapEncodeTiled failed");
   return INVOP_OK;
+}
+
+static int make_map_u8(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer,
+                       uint64_t pitch, uint32_t box_inner, uint32_t box_outer) {
+  return make_tensor_map_u8(m, ptr, inner, outer, pitch, box_inner, box_outer, 64);
 }
 
 // a plain grid launched as a programmatic dependent of the preceding kernel

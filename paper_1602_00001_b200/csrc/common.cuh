@@ -60,6 +60,10 @@ struct invop_plan {
   int64_t k3d_n1 = 0;
   int64_t k3d_n1u = 0;               // (quad, K block, slot) with a digit-1 tile on either SM
   int k3d_ready = 0;
+  // ordered kernel (ordered.cu): one 128-byte-swizzled TMA descriptor per byte
+  // plane, cached with the geometry it was built for
+  alignas(64) unsigned char ord_maps[INVOP_MAX_PLANES][128];
+  const void* ord_maps_key = nullptr; int64_t ord_maps_geom[4] = {0, 0, 0, 0};
 };
 
 struct invop_operator {
@@ -111,6 +115,9 @@ bool batched_supported(const invop_plan* p, int64_t nrhs);
 bool stream_selected(const invop_plan* p, int64_t nrhs);
 int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, int64_t ldy,
                          int64_t nrhs, cudaStream_t s);
+// 2-D uint8 tensor map (inner = bytes along a row); swizzle_bytes 0, 64 or 128
+int make_tensor_map_u8(void* map128, const void* ptr, uint64_t inner, uint64_t outer,
+                       uint64_t pitch, uint32_t box_inner, uint32_t box_outer, int swizzle_bytes);
 int64_t k3d_bytes(const invop_plan* p);
 bool k3_uses_dl(const invop_plan* p);
 bool k3_uses_pair(const invop_plan* p);

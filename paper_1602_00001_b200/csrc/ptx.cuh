@@ -37,6 +37,17 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
       : "memory");
 }
 
+// 2-D tiled TMA load (tensor map in kernel parameter space), completing on an
+// mbarrier of this CTA
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* map, int x, int y,
+                                            uint32_t bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar), "l"(policy)
+      : "memory");
+}
+
 // acc + (int64)a * b as one IMAD.WIDE (keeps the compiler from hoisting a
 // sign-extended 64-bit copy of a loop-invariant operand and multiplying 64x64)
 __device__ __forceinline__ long long madw(int32_t a, int32_t b, long long c) {
