@@ -150,8 +150,9 @@ extern "C" int invop_apply(const invop_plan* p, const void* x, int64_t ldx, void
   if (mode == INVOP_MODE_ORDERED) {
     if (dtype != INVOP_F64)
       return fail(INVOP_E_VALUE, "ordered (bitwise) mode computes in fp64: dtype must be F64");
-    if (!aligned16(x) || (nrhs > 1 && (ldx & 1)))
-      return fail(INVOP_E_VALUE, "x must be 16-byte aligned with an even leading dimension");
+    // any 8-byte aligned x / leading dimension: x tiles that cannot be bulk
+    // copied are copied by the producer warp's lanes (ordered.cu)
+    if ((uintptr_t)x % 8 != 0) return fail(INVOP_E_VALUE, "x must be 8-byte aligned (fp64)");
     return apply_ordered_launch(p, (const double*)x, nrhs > 1 ? ldx : p->n, (double*)y,
                                 nrhs > 1 ? ldy : p->rows, nrhs, s);
   }

@@ -413,10 +413,14 @@ static int ord_get_maps(const invop_plan* cp, const unsigned char (**out)[128]) 
   return INVOP_OK;
 }
 
-template <int P, bool SIGNED, bool SX, int KR>
-static int launch_ord_t(const unsigned char (*maps)[128], OrdArgs a, cudaStream_t s) {
-  constexpr int NC = ord_nc(P), S = ord_stages(P, KR);
-  static_assert(S >= 2, "ordered kernel needs two stages");
+// stages such that two blocks share an SM (two consumers per scheduler)
+constexpr int ord_stages2(int P, int KR) {
+  return (112 * 1024) / ord_stage_bytes(P, KR) < 4 ? (112 * 1024) / ord_stage_bytes(P, KR) : 4;
+}
+
+template <int P, bool SIGNED, bool SX, int KR, int S>
+static int launch_ord_s(const unsigned char (*maps)[128], OrdArgs a, cudaStream_t s) {
+  constexpr int NC = ord_nc(P);
   const size_t smem = (size_t)ord_stage_bytes(P, KR) * S + 32 * S;
   auto kern = k2_ordered<P, SIGNED, SX, KR, NC, S>;
   INVOP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -427,6 +431,21 @@ static int launch_ord_t(const unsigned char (*maps)[128], OrdArgs a, cudaStream_
   INVOP_LAUNCHED(1);
   INVOP_CHECK_LAUNCH("k2_ordered");
   return INVOP_OK;
+}
+
+template <int P, bool SIGNED, bool SX, int KR>
+static int launch_ord_t(const unsigned char (*maps)[128], OrdArgs a, cudaStream_t s) {
+  constexpr int S = ord_stages(P, KR), S2 = ord_stages2(P, KR);
+  static_assert(S >= 2, "ordered kernel needs two stages");
+  // More row blocks than SMs: shallower rings so that two blocks are resident
+  // per SM (the second consumer on each scheduler fills the issue slots the
+  // first leaves open; a single consumer is latency-bound on its DADD chain).
+  if constexpr (KR == 1 && S2 >= 2 && S2 < S) {
+    static const int force = std::getenv("INVOP_ORD_DEEP") ? atoi(std::getenv("INVOP_ORD_DEEP")) : -1;
+    const bool two = force >= 0 ? force == 0 : cdiv(a.rows, ord_nc(P) * 32) > num_sms();
+    if (two) return launch_ord_s<P, SIGNED, SX, KR, S2>(maps, a, s);
+  }
+  return launch_ord_s<P, SIGNED, SX, KR, S>(maps, a, s);
 }
 
 template <int P, bool SIGNED, bool SX>

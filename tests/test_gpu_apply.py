@@ -900,3 +900,53 @@ def test_apply_sharded_c_abi_one_rank(invop):
                                          L.F32, L.MODE_FAST, C.c_void_p(dev.stream_ptr())) != 0
     finally:
         nccl.ncclCommDestroy(comm)
+
+
+# ------------------------------------------------------------------ ordered kernel (ordered.cu) paths
+@pytest.mark.parametrize("lo,hi", [(0, 60000), (-30000, 30000), (0, 4_000_000), (0, 12_000_000),
+                                   (-(2 ** 40), 2 ** 40)])
+def test_ordered_nonfinite_columns_across_tiles(invop, O, lo, hi):
+    """inf/nan in x switch single 128-column tiles to the zero-skip pass in the
+    middle of the pipelined row walk (first, adjacent, middle and tail tiles);
+    the result stays bitwise equal to the reference order."""
+    rng = np.random.default_rng(77 + hi % 1000)
+    n = 700                                       # 6 tiles, ragged tail, rows not a multiple of 128
+    mant = rng.integers(lo, hi + 1, size=(n, n))
+    mant[rng.random((n, n)) < 0.3] = 0
+    plan = invop.build_plan(qm(invop, mant, 3))
+    for cols in ([0], [127, 128], [300], [640, 699], [5, 260, 261, 650], list(range(0, 700, 97))):
+        x = rng.standard_normal(n)
+        for j, c in enumerate(cols):
+            x[c] = (np.inf, -np.inf, np.nan)[j % 3]
+        y, _ = invop.apply(plan, x)
+        yo = O.ordered_apply(mant, 3, x)
+        assert y.tobytes() == yo.tobytes(), cols
+
+
+def test_ordered_many_rhs_and_unaligned_x(invop, O):
+    """Ordered fp64 apply of 1, 2, 3, 4 and 7 right-hand sides (the 4-, 2- and
+    1-RHS passes), one of them with an inf column, and a device x that is only
+    8-byte aligned (the lane-copied x tiles)."""
+    import torch
+
+    rng = np.random.default_rng(2025)
+    for n, lo, hi in ((390, 0, 50000), (391, -3_000_000, 3_000_000)):   # odd n: odd leading dimension
+        mant = rng.integers(lo, hi + 1, size=(n, n))
+        mant[rng.random((n, n)) < 0.25] = 0
+        plan = invop.build_plan(qm(invop, mant, 4))
+        for k in (1, 2, 3, 4, 7):
+            X = rng.standard_normal((k, n))
+            if k >= 3:
+                X[1, 200] = np.inf
+            Y, _ = invop.apply_many(plan, torch.tensor(X, device="cuda"), precision="f64")
+            Y = Y.cpu().numpy()
+            for i in range(k):
+                assert Y[i].tobytes() == O.ordered_apply(mant, 4, X[i]).tobytes(), (k, i)
+        # x starting 8 bytes into an allocation
+        buf = torch.zeros(n + 1, device="cuda", dtype=torch.float64)
+        x = rng.standard_normal(n)
+        buf[1:] = torch.tensor(x, device="cuda")
+        xv = buf[1:]
+        assert xv.data_ptr() % 16 == 8
+        y = plan.device_plan.apply_device(xv.reshape(1, n)).cpu().numpy()[0]
+        assert y.tobytes() == O.ordered_apply(mant, 4, x).tobytes()
