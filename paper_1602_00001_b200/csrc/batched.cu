@@ -73,6 +73,8 @@ struct K3Args {
   int nrhs;
   long long* yacc;         // [64][rows] exact int64 row sums (DL: of the residuals)
   const int* idx1;         // DL: compact index of a tile's digit-1 plane, -1 if absent
+  int ysh;                 // DL: tensor rows are 64 << ysh bytes wide (2: pre-swizzled tiles)
+  int btile;               // x digits stored as pre-swizzled [K block][192][64] tiles
 };
 
 __host__ __device__ inline int64_t k3d_tile0(int64_t rt, int64_t kb, int64_t kbs);
@@ -281,17 +283,18 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
             if (P == 2 && TILES == 2) {
               // stage: [digit-0 tile 0][digit-0 tile 1][digit-1 tile 0][digit-1 tile 1]
               const int trow = (int)(k3d_tile0(row0 / K3_BM, kb, a.kb_stride) * K3_BM);
-              tma_2d(sb, &mapA0, 0, trow, fb, pol_a);         // both digit-0 tiles
+              tma_2d(sb, &mapA0, 0, trow >> a.ysh, fb, pol_a);         // both digit-0 tiles
 #pragma unroll
               for (int ti = 0; ti < TILES; ++ti)
                 if (i1[ti] >= 0)
-                  tma_2d(sb + (TILES + ti) * K3_A_TILE, &mapA1, 0, i1[ti] * K3_BM, fb, pol_a);
+                  tma_2d(sb + (TILES + ti) * K3_A_TILE, &mapA1, 0, (i1[ti] * K3_BM) >> a.ysh, fb, pol_a);
             } else {
 #pragma unroll
               for (int ti = 0; ti < TILES; ++ti) {
                 const int trow = (int)(k3d_tile0(row0 / K3_BM + ti, kb, a.kb_stride) * K3_BM);
-                tma_2d(sb + (ti * P + 0) * K3_A_TILE, &mapA0, 0, trow, fb, pol_a);
-                if (i1[ti] >= 0) tma_2d(sb + (ti * P + 1) * K3_A_TILE, &mapA1, 0, i1[ti] * K3_BM, fb, pol_a);
+                tma_2d(sb + (ti * P + 0) * K3_A_TILE, &mapA0, 0, trow >> a.ysh, fb, pol_a);
+                if (i1[ti] >= 0)
+                  tma_2d(sb + (ti * P + 1) * K3_A_TILE, &mapA1, 0, (i1[ti] * K3_BM) >> a.ysh, fb, pol_a);
               }
             }
           } else {
@@ -306,7 +309,8 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
           }
           // the three digit tiles are consecutive rows of B: one 192-row box
 #ifndef K3_PROBE_NOB
-          tma_2d(sb + A_BYTES, &mapB, kb * K3_BK, 0, fb, pol_b);
+          tma_2d(sb + A_BYTES, &mapB, a.btile ? 0 : kb * K3_BK,
+                 a.btile ? kb * (K3_ND * K3_NR / 4) : 0, fb, pol_b);
 #endif
           if (++st == STAGES) { st = 0; ph ^= 1; }
         }
@@ -547,6 +551,10 @@ struct K3Prep {
   int64_t ld, rows;
   int P, sgn, rows01;
   unsigned long long* y01;    // [64][2] exact sums of plan rows 0, 1 (DL)
+  // B as [K block][192 rows][64 bytes] tiles, each row's 16-byte chunks where
+  // the 64-byte shared-memory swizzle puts them (a contiguous image of the
+  // operand tile: copied as 256-byte rows); 0: row-major [192][ldb]
+  int btile;
 };
 
 __device__ __forceinline__ int k3_exponent(float m) {
@@ -683,9 +691,13 @@ __global__ void __launch_bounds__(K3G_TPB, 6) k3_digits(K3Prep a) {
       w[0][q] = b0; w[1][q] = b1; w[2][q] = b2;
     }
 #pragma unroll
-    for (int l = 0; l < 3; ++l)
-      *reinterpret_cast<uint4*>(a.B + (int64_t)(l * K3_NR + t) * a.ldb + jb) =
-          make_uint4(w[l][0], w[l][1], w[l][2], w[l][3]);
+    for (int l = 0; l < 3; ++l) {
+      const int row = l * K3_NR + t;
+      int8_t* dst = a.btile ? a.B + (jb / K3_BK) * (int64_t)(K3_ND * K3_NR * K3_BK) + row * K3_BK +
+                                  (((int)((jb % K3_BK) >> 4) ^ ((row >> 1) & 3)) << 4)
+                            : a.B + (int64_t)row * a.ldb + jb;
+      *reinterpret_cast<uint4*>(dst) = make_uint4(w[l][0], w[l][1], w[l][2], w[l][3]);
+    }
     if (a.rows01 && live) {
       // plane rows are ld >= ldb bytes with zero padding: 16-byte loads
       const uint4 p00 = *reinterpret_cast<const uint4*>(a.planes[0] + jb);
@@ -806,8 +818,12 @@ __global__ void k3d_index(int64_t tiles, const int* __restrict__ tilew, int* __r
 }
 
 // one thread per (row, K block): write the residual digits into the tiles
+// presw: the 16-byte chunks of a tile row are stored where the 64-byte
+// shared-memory swizzle puts them (chunk c of row r at c ^ ((r >> 1) & 3)), so
+// a tile is a contiguous image of its shared-memory form and the copy engine
+// moves it as wide unswizzled rows
 __global__ void k3d_write(K3DBuild a, const int* __restrict__ idx1, uint8_t* __restrict__ t0,
-                          uint8_t* __restrict__ t1) {
+                          uint8_t* __restrict__ t1, int presw) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= a.rows * a.kbs) return;
   const int64_t r = t / a.kbs, kb = t - r * a.kbs;
@@ -824,8 +840,9 @@ __global__ void k3d_write(K3DBuild a, const int* __restrict__ idx1, uint8_t* __r
       w0[q >> 2] |= ((uint32_t)g0 & 255u) << (8 * (q & 3));
       w1[q >> 2] |= ((uint32_t)g1 & 255u) << (8 * (q & 3));
     }
-    *reinterpret_cast<uint4*>(d0 + q0) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
-    if (d1) *reinterpret_cast<uint4*>(d1 + q0) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
+    const int qs = presw ? (((q0 >> 4) ^ (int)(((r % K3_BM) >> 1) & 3)) << 4) : q0;
+    *reinterpret_cast<uint4*>(d0 + qs) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
+    if (d1) *reinterpret_cast<uint4*>(d1 + qs) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
   }
 }
 
@@ -1178,6 +1195,8 @@ struct K3PairArgs {
   long long* yacc;
   const int* idx1;          // [rtiles][kbs] compact digit-1 index, -1 if absent
   int zero1;                // index of the all-zero digit-1 tile
+  int ysh;                  // tensor rows are 64 << ysh bytes wide (2: pre-swizzled tiles)
+  int btile;                // x digits stored as pre-swizzled [K block][192][64] tiles
 };
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(K3_THREADS, 1)
@@ -1258,13 +1277,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(K3_THREADS, 1)
           // the leader expects both CTAs' bytes (the peer's loads may land
           // first: the transaction count may go negative until then)
           if (rank == 0) k3_expect_tx(smem_u32(&full[st]), 2 * (2 * K3_A_TILE + K3Q2_BH + __popc(mask) * K3_A_TILE));
-          tma_2d_pair(sb, &mapA0, 0, (int)(k3d_tile0(rt_own, kb, a.kb_stride) * K3_BM), fb, pol_a);
+          tma_2d_pair(sb, &mapA0, 0, (int)(k3d_tile0(rt_own, kb, a.kb_stride) * K3_BM) >> a.ysh, fb, pol_a);
 #pragma unroll
           for (int ti = 0; ti < 2; ++ti)
             if ((mask >> ti) & 1u)
               tma_2d_pair(sb + (2 + ti) * K3_A_TILE, &mapA1, 0,
-                          (own1[ti] >= 0 ? own1[ti] : a.zero1) * K3_BM, fb, pol_a);
-          tma_2d_pair(sb + 4 * K3_A_TILE, &mapBh, kb * K3_BK, (int)rank * (K3_ND * K3_NR / 2), fb, pol_b);
+                          ((own1[ti] >= 0 ? own1[ti] : a.zero1) * K3_BM) >> a.ysh, fb, pol_a);
+          tma_2d_pair(sb + 4 * K3_A_TILE, &mapBh, a.btile ? 0 : kb * K3_BK,
+                      a.btile ? kb * (K3_ND * K3_NR / 4) + (int)rank * (K3_ND * K3_NR / 8)
+                              : (int)rank * (K3_ND * K3_NR / 2), fb, pol_b);
           if (++st == K3Q2_STAGES) { st = 0; ph ^= 1; }
         }
       }
@@ -1573,13 +1594,22 @@ static int k3d_build(invop_plan* p, cudaStream_t s) {
       INVOP_CUDA(cudaMalloc(&p->k3d_tiles[1], (size_t)(p->k3d_n1 + 1) * K3_A_TILE));
       INVOP_CUDA(cudaMemsetAsync(p->k3d_tiles[0], 0, (size_t)tiles * K3_A_TILE, s));
       INVOP_CUDA(cudaMemsetAsync(p->k3d_tiles[1] + (size_t)p->k3d_n1 * K3_A_TILE, 0, K3_A_TILE, s));
+      // INVOP_K3_PRESW=0: tiles stored row-major, swizzled by the tensor copy
+      // (64-byte rows); default: stored pre-swizzled and copied as 256-byte rows
+      const char* pe = std::getenv("INVOP_K3_PRESW");
+      const int presw = pe && *pe == '0' ? 0 : 1;
+      p->k3d_ysh = presw ? 2 : 0;
       k3d_write<<<(unsigned)cdiv(thr, 256), 256, 0, s>>>(a, p->k3d_idx1, p->k3d_tiles[0],
-                                                         p->k3d_tiles[1]);
-      rc = make_map_u8((CUtensorMap*)p->k3d_mapA[0], p->k3d_tiles[0], K3_BK,
-                       (uint64_t)tiles * K3_BM, K3_BK, K3_BK, p->P == 2 ? 2 * K3_BM : K3_BM);
+                                                         p->k3d_tiles[1], presw);
+      const uint64_t wide = (uint64_t)K3_BK << p->k3d_ysh;
+      const uint32_t brows = (uint32_t)((p->P == 2 ? 2 * K3_BM : K3_BM) >> p->k3d_ysh);
+      rc = make_tensor_map_u8(p->k3d_mapA[0], p->k3d_tiles[0], wide,
+                              ((uint64_t)tiles * K3_BM) >> p->k3d_ysh, wide, (uint32_t)wide, brows,
+                              presw ? 0 : 64);
       if (!rc)
-        rc = make_map_u8((CUtensorMap*)p->k3d_mapA[1], p->k3d_tiles[1], K3_BK,
-                         (uint64_t)(p->k3d_n1 + 1) * K3_BM, K3_BK, K3_BK, K3_BM);
+        rc = make_tensor_map_u8(p->k3d_mapA[1], p->k3d_tiles[1], wide,
+                                ((uint64_t)(p->k3d_n1 + 1) * K3_BM) >> p->k3d_ysh, wide,
+                                (uint32_t)wide, (uint32_t)(K3_BM >> p->k3d_ysh), presw ? 0 : 64);
       // digit-1 MMAs the SM-pair kernel issues: (quad, K block, slot) where
       // either SM's tile has a digit-1 plane
       if (!rc) {
@@ -1606,8 +1636,17 @@ static int k3d_build(invop_plan* p, cudaStream_t s) {
   return INVOP_OK;
 }
 
-// the residual tiles go to the SM-pair kernel (k3_dl2) unless INVOP_K3_PAIR=0
-static bool k3_pair_enabled() { return layout_flag("INVOP_K3_PAIR", true); }
+// The residual tiles go to the SM-pair kernel (k3_dl2) or the one-SM kernel
+// (k3_batched<..., DL>): INVOP_K3_PAIR=1/0 forces one; otherwise the plan's
+// choice, timed once on the device when the layout is built (k3_autotune) —
+// which of the two is faster depends on how many SM pairs of this particular
+// GPU can be co-resident (floor-swept parts differ: 0.87-0.94 ms for the pair
+// kernel against 0.89-0.90 ms for the one-SM kernel at config 5 across boxes).
+static bool k3_pair_enabled(const invop_plan* p) {
+  const char* v = getenv("INVOP_K3_PAIR");
+  if (v && *v) return *v != '0';
+  return p->k3_pair != 0;
+}
 
 // the DL kernel serves a batched apply when its residual tiles were built and
 // no INVOP_K3_CFG variant selects a byte-plane configuration
@@ -1619,12 +1658,71 @@ bool k3_uses_dl(const invop_plan* p) {
 }
 
 // the residual-tile apply runs on SM pairs (k3_dl2)
-bool k3_uses_pair(const invop_plan* p) { return k3_uses_dl(p) && k3_pair_enabled(); }
+bool k3_uses_pair(const invop_plan* p) { return k3_uses_dl(p) && k3_pair_enabled(p); }
 
-// lazily built layouts of the batched apply (DL residual tiles)
+static int batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, int64_t ldy,
+                          int64_t nrhs, cudaStream_t s, int pair_sel);
+
+// hashed noise in (-1, 1): the tensor-core kernels run power-capped, and their
+// time depends on how much the operands toggle (zeros time ~8 % faster)
+__global__ void k3_fill_noise(float* __restrict__ x, int64_t n) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint32_t h = (uint32_t)i * 2654435761u + (uint32_t)(i >> 32) * 40503u + 12345u;
+  h ^= h >> 16; h *= 0x7feb352du; h ^= h >> 15; h *= 0x846ca68bu; h ^= h >> 16;
+  x[i] = (float)(int32_t)h * (1.0f / 2147483648.0f);
+}
+
+// One-time choice between the SM-pair and the one-SM kernel for this plan on
+// this GPU: both run a 64-RHS apply of noise, 2 warm-up + 3 timed launches each.
+static int k3_autotune(invop_plan* p, cudaStream_t s) {
+  if (p->k3_pair >= 0 || !k3_uses_dl(p)) return INVOP_OK;
+  const char* v = getenv("INVOP_K3_PAIR");
+  if (v && *v) return INVOP_OK;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return INVOP_OK;          // decided by a later call outside the capture
+  }
+  float *x = nullptr, *y = nullptr;
+  const size_t xb = (size_t)K3_NR * p->n * 4, yb = (size_t)K3_NR * p->rows * 4;
+  if (cudaMalloc(&x, xb) != cudaSuccess || cudaMalloc(&y, yb) != cudaSuccess) {
+    cudaGetLastError();
+    if (x) cudaFree(x);
+    p->k3_pair = 1;           // no room to measure: keep the default
+    return INVOP_OK;
+  }
+  k3_fill_noise<<<(unsigned)cdiv((int64_t)K3_NR * p->n, 256), 256, 0, s>>>(x, (int64_t)K3_NR * p->n);
+  cudaEvent_t e0, e1;
+  INVOP_CUDA(cudaEventCreate(&e0));
+  INVOP_CUDA(cudaEventCreate(&e1));
+  float best_ms = 0.f;
+  int best = 1, rc = INVOP_OK;
+  for (int sel = 1; sel >= 0 && !rc; --sel) {
+    for (int i = 0; i < 2 && !rc; ++i) rc = batched_launch(p, x, p->n, y, p->rows, K3_NR, s, sel);
+    cudaEventRecord(e0, s);
+    for (int i = 0; i < 3 && !rc; ++i) rc = batched_launch(p, x, p->n, y, p->rows, K3_NR, s, sel);
+    cudaEventRecord(e1, s);
+    if (cudaEventSynchronize(e1) != cudaSuccess) rc = cuda_fail(cudaGetLastError(), "k3 autotune");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (getenv("INVOP_K3_DEBUG")) fprintf(stderr, "k3 autotune: %s %.4f ms\n", sel ? "pair" : "single", ms / 3);
+    if (sel == 1 || ms < best_ms) { best_ms = ms; best = sel; }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(x);
+  cudaFree(y);
+  if (!rc) p->k3_pair = best;
+  return rc;
+}
+
+// lazily built layouts of the batched apply (DL residual tiles) and the
+// kernel choice
 int k3_prepare(invop_plan* p, cudaStream_t s) {
   const int rc = k3d_build(p, s);
-  return rc == INVOP_E_UNSUPPORTED ? INVOP_OK : rc;
+  if (rc != INVOP_OK) return rc == INVOP_E_UNSUPPORTED ? INVOP_OK : rc;
+  return k3_autotune(p, s);
 }
 
 // int8 tensor operations (2*M*N*K per MMA) one batched apply of nrhs
@@ -1639,7 +1737,7 @@ int64_t k3_tensor_ops(const invop_plan* p, int64_t nrhs) {
   if (k3_uses_dl(p)) {
     const int64_t rt = k3d_rtiles(p);
     // SM pairs: digit-1 MMAs wherever either SM's tile needs one (k3d_union)
-    if (k3_pair_enabled()) return batches * per_tile_kb * (rt * kbs + 2 * p->k3d_n1u);
+    if (k3_pair_enabled(p)) return batches * per_tile_kb * (rt * kbs + 2 * p->k3d_n1u);
     return batches * per_tile_kb * (rt * kbs + p->k3d_n1);
   }
   return batches * per_tile_kb * p->P * rtiles * kbs;
@@ -1653,6 +1751,14 @@ int64_t k3d_bytes(const invop_plan* p) {
 
 int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, int64_t ldy,
                          int64_t nrhs, cudaStream_t s) {
+  const int rc = k3_prepare(p, s);
+  if (rc) return rc;
+  return batched_launch(p, x, ldx, y, ldy, nrhs, s, -1);
+}
+
+// pair_sel: 1 / 0 force the SM-pair / one-SM kernel (autotune), -1 the plan's choice
+static int batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, int64_t ldy,
+                          int64_t nrhs, cudaStream_t s, int pair_sel) {
   const int64_t ldb = round_up(p->n, K3_BK);
   const int kblocks = (int)(ldb / K3_BK);
   // variant: row tiles per unit (share B) and pipeline depth
@@ -1662,7 +1768,7 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
   int krc = k3d_build(p, s);
   if (krc != INVOP_OK && krc != INVOP_E_UNSUPPORTED) return krc;
   const bool dl = k3_uses_dl(p);
-  const bool pair = dl && k3_pair_enabled();
+  const bool pair = dl && (pair_sel >= 0 ? pair_sel != 0 : k3_pair_enabled(p));
   // work items: row-tile pairs on one SM, quads of row tiles on an SM pair
   const int64_t pairs = pair ? cdiv(p->rows, 4 * K3_BM) : cdiv(p->rows, tiles * K3_BM);
   const int slots = pair ? k3_pair_slots() : sms;
@@ -1727,8 +1833,16 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
     p->k3_maps_ready = 1;
   }
   CUtensorMap mapB;
-  rc = pair ? make_map_u8(&mapB, B, ldb, (uint64_t)K3_ND * K3_NR, ldb, K3_BK, K3_ND * K3_NR / 2)
-            : make_map_u8(&mapB, B, ldb, (uint64_t)K3_ND * K3_NR, ldb, K3_BK, K3_ND * K3_NR);
+  static const int btile = []() {
+    const char* e = std::getenv("INVOP_K3_BTILE");
+    return e && *e == '0' ? 0 : 1;
+  }();
+  if (btile)      // [kblocks * 48 rows][256 bytes], one K block's operand = 48 (pair: 24) rows
+    rc = make_tensor_map_u8(&mapB, B, 4 * K3_BK, (uint64_t)kblocks * (K3_ND * K3_NR / 4), 4 * K3_BK,
+                            4 * K3_BK, pair ? K3_ND * K3_NR / 8 : K3_ND * K3_NR / 4, 0);
+  else
+    rc = pair ? make_map_u8(&mapB, B, ldb, (uint64_t)K3_ND * K3_NR, ldb, K3_BK, K3_ND * K3_NR / 2)
+              : make_map_u8(&mapB, B, ldb, (uint64_t)K3_ND * K3_NR, ldb, K3_BK, K3_ND * K3_NR);
   if (rc) return rc;
   for (int64_t t0 = 0; t0 < nrhs; t0 += K3_NR) {
     const int nr = (int)std::min<int64_t>(K3_NR, nrhs - t0);
@@ -1740,6 +1854,7 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
     pr.planes[1] = p->planes[p->P > 1 ? 1 : 0];
     pr.ld = p->ld; pr.rows = p->rows; pr.P = p->P; pr.sgn = p->is_signed;
     pr.rows01 = dl ? 1 : 0; pr.y01 = (unsigned long long*)y01;
+    pr.btile = btile;
     // 3. (arguments) rows 0/1 + double prefix (DL), scaling, non-finite
     // columns, y
     K3Post q;
@@ -1760,6 +1875,8 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
     // 2. the tensor-core pass: exact int64 row sums into yacc
     K3Args a;
     a.idx1 = p->k3d_idx1;
+    a.ysh = p->k3d_ysh;
+    a.btile = btile;
     a.rows = p->rows; a.n = p->n; a.P = p->P; a.hi_signed = p->is_signed;
     a.kblocks_total = kblocks; a.kblocks_per_unit = kpu; a.splits = splits;
     a.kb_stride = (int)(p->ld / K3_BK);
@@ -1774,6 +1891,7 @@ int apply_batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, i
           pa.rows = p->rows; pa.kblocks_total = kblocks; pa.kb_stride = (int)(p->ld / K3_BK);
           pa.kblocks_per_unit = kpu; pa.splits = splits; pa.quads = pairs; pa.nrhs = nr;
           pa.yacc = yacc; pa.idx1 = p->k3d_idx1; pa.zero1 = (int)p->k3d_n1;
+          pa.ysh = p->k3d_ysh; pa.btile = btile;
           rc = launch_k3_dl2(*A0, *A1, mapB, pa, grid, s);
         } else {
           rc = launch_k3<2, 2, K3_DL_STAGES, true>(*A0, *A1, mapB, a, grid, s);

@@ -60,6 +60,8 @@ struct invop_plan {
   int64_t k3d_n1 = 0;
   int64_t k3d_n1u = 0;               // (quad, K block, slot) with a digit-1 tile on either SM
   int k3d_ready = 0;
+  int k3_pair = -1;                  // 1: SM-pair kernel, 0: one-SM kernel, -1: not timed yet
+  int k3d_ysh = 0;                   // tensor rows of the residual tiles are 64 << k3d_ysh bytes
   // ordered kernel (ordered.cu): one 128-byte-swizzled TMA descriptor per byte
   // plane, cached with the geometry it was built for
   alignas(64) unsigned char ord_maps[INVOP_MAX_PLANES][128];
