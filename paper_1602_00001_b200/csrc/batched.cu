@@ -75,6 +75,8 @@ struct K3Args {
   const int* idx1;         // DL: compact index of a tile's digit-1 plane, -1 if absent
   int ysh;                 // DL: tensor rows are 64 << ysh bytes wide (2: pre-swizzled tiles)
   int btile;               // x digits stored as pre-swizzled [K block][192][64] tiles
+  // pre-swizzled tiles are contiguous images: plain bulk copies (no tensor map)
+  const uint8_t* t0; const uint8_t* t1; const int8_t* B; int bulk;
 };
 
 __host__ __device__ inline int64_t k3d_tile0(int64_t rt, int64_t kb, int64_t kbs);
@@ -108,6 +110,14 @@ __device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, int
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
       " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void k3_bulk(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar,
+                                        uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar), "l"(policy)
       : "memory");
 }
 // K-major operand tile, rows of 64 bytes, SWIZZLE_64B (8-row atoms of 512 B)
@@ -283,11 +293,20 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
             if (P == 2 && TILES == 2) {
               // stage: [digit-0 tile 0][digit-0 tile 1][digit-1 tile 0][digit-1 tile 1]
               const int trow = (int)(k3d_tile0(row0 / K3_BM, kb, a.kb_stride) * K3_BM);
+              if (a.bulk) {
+                k3_bulk(sb, a.t0 + (int64_t)trow * K3_BK, 2 * K3_A_TILE, fb, pol_a);
+#pragma unroll
+                for (int ti = 0; ti < TILES; ++ti)
+                  if (i1[ti] >= 0)
+                    k3_bulk(sb + (TILES + ti) * K3_A_TILE, a.t1 + (int64_t)i1[ti] * K3_A_TILE,
+                            K3_A_TILE, fb, pol_a);
+              } else {
               tma_2d(sb, &mapA0, 0, trow >> a.ysh, fb, pol_a);         // both digit-0 tiles
 #pragma unroll
               for (int ti = 0; ti < TILES; ++ti)
                 if (i1[ti] >= 0)
                   tma_2d(sb + (TILES + ti) * K3_A_TILE, &mapA1, 0, (i1[ti] * K3_BM) >> a.ysh, fb, pol_a);
+              }
             } else {
 #pragma unroll
               for (int ti = 0; ti < TILES; ++ti) {
@@ -309,8 +328,11 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
           }
           // the three digit tiles are consecutive rows of B: one 192-row box
 #ifndef K3_PROBE_NOB
-          tma_2d(sb + A_BYTES, &mapB, a.btile ? 0 : kb * K3_BK,
-                 a.btile ? kb * (K3_ND * K3_NR / 4) : 0, fb, pol_b);
+          if (DL && a.bulk)
+            k3_bulk(sb + A_BYTES, a.B + (int64_t)kb * (K3_ND * K3_B_TILE), K3_ND * K3_B_TILE, fb, pol_b);
+          else
+            tma_2d(sb + A_BYTES, &mapB, a.btile ? 0 : kb * K3_BK,
+                   a.btile ? kb * (K3_ND * K3_NR / 4) : 0, fb, pol_b);
 #endif
           if (++st == STAGES) { st = 0; ph ^= 1; }
         }
@@ -1877,6 +1899,14 @@ static int batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, 
     a.idx1 = p->k3d_idx1;
     a.ysh = p->k3d_ysh;
     a.btile = btile;
+    a.t0 = p->k3d_tiles[0]; a.t1 = p->k3d_tiles[1]; a.B = B;
+    {
+      static const int bulk_env = []() {
+        const char* e = std::getenv("INVOP_K3_BULK");
+        return e && *e == '0' ? 0 : 1;
+      }();
+      a.bulk = dl && bulk_env && p->k3d_ysh == 2 && btile ? 1 : 0;
+    }
     a.rows = p->rows; a.n = p->n; a.P = p->P; a.hi_signed = p->is_signed;
     a.kblocks_total = kblocks; a.kblocks_per_unit = kpu; a.splits = splits;
     a.kb_stride = (int)(p->ld / K3_BK);

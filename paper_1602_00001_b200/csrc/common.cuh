@@ -50,6 +50,7 @@ struct invop_plan {
   int dl_ready = 0, dl_grid = 0, dl_nslabs = 0, dl_groups = 1;
   int64_t* dl_rowlo = nullptr;      // [grid + 1] CTA row ranges (byte-balanced)
   int64_t dl_maxrows = 0;
+  int dl_cd = 0;                    // residuals stored as column differences inside each chunk
   alignas(64) unsigned char k3_mapA[2][128];
   int k3_maps_ready = 0;
   // K3 on row residuals (batched.cu): digit-0 tiles for every (row tile, K

@@ -118,7 +118,22 @@ struct DlBuild {
   int64_t rows, n, ld;
   int nch, nslabs, grid, groups;
   const int64_t* rowlo;       // [grid + 1] CTA row ranges
+  int cd;                     // store column differences of the residuals within each chunk
 };
+
+// Column difference inside a 512-column chunk (one warp, 16 columns per lane):
+// f_j = e_j - e_{j-1}, f = e at the chunk's first column. The apply multiplies
+// f by the suffix sums of X within the chunk (sum_j e_j X_j = sum_i f_i S_i,
+// S_i = sum_{j >= i} X_j), so the change costs nothing per row; the residuals
+// of neighbouring columns are close, so f needs fewer bytes (config 4: 1.56 ->
+// 1.32 B/entry, tools/predictor_study.py).
+__device__ __forceinline__ void dl_coldiff16(int32_t* e, int lane) {
+  int32_t prev = __shfl_up_sync(0xffffffffu, e[15], 1);
+  if (lane == 0) prev = 0;
+#pragma unroll
+  for (int q = 15; q > 0; --q) e[q] -= e[q - 1];
+  e[0] -= prev;
+}
 
 __device__ __forceinline__ void dl_residual16(const DlBuild& a, int64_t r, int c, int lane,
                                               int32_t* e) {
@@ -150,6 +165,7 @@ __global__ void k_dl_width(DlBuild a, uint8_t* __restrict__ width) {
   const int c = (int)(gw - r * a.nch);
   int32_t e[16];
   dl_residual16(a, r, c, lane, e);
+  if (a.cd) dl_coldiff16(e, lane);
   uint32_t w = 1;
 #pragma unroll
   for (int q = 0; q < 16; ++q) w = max(w, dl_width(e[q]));
@@ -233,6 +249,7 @@ __global__ void k_dl_write(DlBuild a, const uint4* __restrict__ hdrs,
   if (cl == 0 && lane < 3) reinterpret_cast<uint4*>(unit)[lane] = hdrs[3 * u + lane];
   int32_t e[16];
   dl_residual16(a, r, c, lane, e);
+  if (a.cd) dl_coldiff16(e, lane);
   const int s0 = h[cl], w = h[cl + 1] - s0;
   for (int b = 0; b < w; ++b)
     *reinterpret_cast<uint4*>(unit + DL_HDR + (int64_t)(s0 + b) * 512 + lane * 16) = dl_bytes16(e, b);
@@ -270,35 +287,47 @@ __device__ __forceinline__ uint32_t dl_lds_u8(uint32_t addr) {
   return v;
 }
 
-// plane b of a lane's 16 residual digits times the 3 digit words of X: the
+// plane b of a lane's 16 residual digits times the ND digit words of X: the
 // (b, d) partial lands in S[b + d] (weight 256^(b+d)). Exact in int32: one
 // DP4A adds at most 4 * 128 * 128 = 2^16.
-template <int B>
+template <int B, int ND>
 __device__ __forceinline__ void dl_plane(const uint4& cw, const uint32_t (*xd)[4], int32_t* S) {
 #pragma unroll
   for (int k = 0; k < 4; ++k)
 #pragma unroll
-    for (int d = 0; d < 3; ++d) S[B + d] = dp4a_ss(u4get(cw, k), xd[d][k], S[B + d]);
+    for (int d = 0; d < ND; ++d) S[B + d] = dp4a_ss(u4get(cw, k), xd[d][k], S[B + d]);
 }
 
 // planes 1.. of one chunk (width w >= 2), warp-uniform branches
+template <int ND>
 __device__ __forceinline__ void dl_upper(uint32_t pa, uint32_t w, const uint32_t (*xd)[4], int32_t* S) {
   if (w >= 2) {
-    dl_plane<1>(dl_lds128(pa + 512), xd, S);
+    dl_plane<1, ND>(dl_lds128(pa + 512), xd, S);
     if (w >= 3) {
-      dl_plane<2>(dl_lds128(pa + 1024), xd, S);
-      if (w >= 4) dl_plane<3>(dl_lds128(pa + 1536), xd, S);
+      dl_plane<2, ND>(dl_lds128(pa + 1024), xd, S);
+      if (w >= 4) dl_plane<3, ND>(dl_lds128(pa + 1536), xd, S);
     }
   }
 }
 
+// exact warp sum of the weight classes. ND = 3: |e| < 2^25, |X| <= 2^22, 16
+// codes per lane -> |acc| < 2^54, two 27-bit halves. ND = 4 (column
+// differences against suffix sums): |f| < 2^26, |S| < 2^30 ->
+// |acc| < 2^60, three parts of 26 + 26 + the rest
+template <int ND>
 __device__ __forceinline__ long long dl_warp_sum(const int32_t* S) {
-  const long long acc = (long long)S[0] + ((long long)S[1] << 8) + ((long long)S[2] << 16) +
-                        ((long long)S[3] << 24) + ((long long)S[4] << 32) + ((long long)S[5] << 40);
-  // exact warp sum: |e| < 2^25, |X| <= 2^22, 16 SW codes per lane -> |acc| < 2^54
-  const uint32_t lo = __reduce_add_sync(0xffffffffu, (uint32_t)acc & 0x7FFFFFFu);
-  const int32_t hi = __reduce_add_sync(0xffffffffu, (int32_t)(acc >> 27));
-  return ((long long)hi << 27) + (long long)lo;
+  long long acc = (long long)S[0] + ((long long)S[1] << 8) + ((long long)S[2] << 16) +
+                  ((long long)S[3] << 24) + ((long long)S[4] << 32) + ((long long)S[5] << 40);
+  if (ND == 3) {
+    const uint32_t lo = __reduce_add_sync(0xffffffffu, (uint32_t)acc & 0x7FFFFFFu);
+    const int32_t hi = __reduce_add_sync(0xffffffffu, (int32_t)(acc >> 27));
+    return ((long long)hi << 27) + (long long)lo;
+  }
+  acc += (long long)S[6] << 48;
+  const uint32_t lo = __reduce_add_sync(0xffffffffu, (uint32_t)acc & 0x3FFFFFFu);
+  const uint32_t mid = __reduce_add_sync(0xffffffffu, (uint32_t)(acc >> 26) & 0x3FFFFFFu);
+  const int32_t hi = __reduce_add_sync(0xffffffffu, (int32_t)(acc >> 52));
+  return ((long long)hi << 52) + ((long long)mid << 26) + (long long)lo;
 }
 
 __device__ __forceinline__ void dl_slot(double* sp, bool first, long long Y, double inv2e, int lane) {
@@ -314,10 +343,10 @@ __device__ __forceinline__ float dl_x(const DlArgs& a, int64_t j) {
 // the rows of one consumer iteration: headers of all (row, chunk), then the
 // plane-0 words, then the DP4As of all rows (independent chains); upper planes
 // last (warp-uniform branches on the chunk widths)
-template <int SW, int ROWS, int WPG>
+template <int SW, int ROWS, int WPG, int ND>
 __device__ __forceinline__ void dl_rows_phased(const uint32_t* sb, int q, uint32_t stepv,
-                                               const uint32_t (*xd)[3][4], int lane,
-                                               int32_t (*Sa)[6]) {
+                                               const uint32_t (*xd)[ND][4], int lane,
+                                               int32_t (*Sa)[7]) {
   uint32_t h[ROWS][SW], w[ROWS][SW];
 #pragma unroll
   for (int r = 0; r < ROWS; ++r)
@@ -338,28 +367,28 @@ __device__ __forceinline__ void dl_rows_phased(const uint32_t* sb, int q, uint32
 #pragma unroll
   for (int r = 0; r < ROWS; ++r)
 #pragma unroll
-    for (int k = 0; k < 6; ++k) Sa[r][k] = 0;
+    for (int k = 0; k < 7; ++k) Sa[r][k] = 0;
 #pragma unroll
   for (int t = 0; t < SW; ++t)
 #pragma unroll
-    for (int r = 0; r < ROWS; ++r) dl_plane<0>(cw[r][t], xd[t], Sa[r]);
+    for (int r = 0; r < ROWS; ++r) dl_plane<0, ND>(cw[r][t], xd[t], Sa[r]);
 #pragma unroll
   for (int t = 0; t < SW; ++t) {
     if (!((stepv >> t) & 1u)) continue;                      // warp-uniform
 #pragma unroll
-    for (int r = 0; r < ROWS; ++r) dl_upper(h[r][t], w[r][t], xd[t], Sa[r]);
+    for (int r = 0; r < ROWS; ++r) dl_upper<ND>(h[r][t], w[r][t], xd[t], Sa[r]);
   }
 }
 
 // chunk by chunk (fewer live registers for many chunks per warp)
-template <int SW, int ROWS, int WPG>
+template <int SW, int ROWS, int WPG, int ND>
 __device__ __forceinline__ void dl_rows_lazy(const uint32_t* sb, int q, uint32_t stepv,
-                                             const uint32_t (*xd)[3][4], int lane,
-                                             int32_t (*Sa)[6]) {
+                                             const uint32_t (*xd)[ND][4], int lane,
+                                             int32_t (*Sa)[7]) {
 #pragma unroll
   for (int r = 0; r < ROWS; ++r)
 #pragma unroll
-    for (int k = 0; k < 6; ++k) Sa[r][k] = 0;
+    for (int k = 0; k < 7; ++k) Sa[r][k] = 0;
 #pragma unroll
   for (int t = 0; t < SW; ++t) {
     if (!((stepv >> t) & 1u)) continue;                      // warp-uniform
@@ -374,9 +403,9 @@ __device__ __forceinline__ void dl_rows_lazy(const uint32_t* sb, int q, uint32_t
       cw[r] = dl_lds128(pa[r]);
     }
 #pragma unroll
-    for (int r = 0; r < ROWS; ++r) dl_plane<0>(cw[r], xd[t], Sa[r]);
+    for (int r = 0; r < ROWS; ++r) dl_plane<0, ND>(cw[r], xd[t], Sa[r]);
 #pragma unroll
-    for (int r = 0; r < ROWS; ++r) dl_upper(pa[r], wd[r], xd[t], Sa[r]);
+    for (int r = 0; r < ROWS; ++r) dl_upper<ND>(pa[r], wd[r], xd[t], Sa[r]);
   }
 }
 
@@ -411,8 +440,9 @@ __device__ __forceinline__ void dl_x16(const DlArgs& a, int64_t c0, bool inside,
 // CONS consumer warps in G groups. Group g walks segment g of the CTA's rows
 // (ROWS rows per iteration); warp q of a group owns chunks q + t*(CONS/G) of
 // every slab, its x piece held in registers as balanced digits.
-template <int CONS, int G, int ROWS, bool F64IO>
+template <int CONS, int G, int ROWS, bool F64IO, bool CD = false>
 __global__ void __launch_bounds__((CONS + 1) * 32, 1) k2_dl(DlArgs a) {
+  constexpr int ND = CD ? 4 : 3;        // digit planes of the x-side operand
   constexpr int WPG = CONS / G;
   constexpr int SW = DL_SLAB / (WPG * 512);
   extern __shared__ __align__(128) unsigned char smem[];
@@ -486,7 +516,9 @@ __global__ void __launch_bounds__((CONS + 1) * 32, 1) k2_dl(DlArgs a) {
     const int64_t sbase = nrows / G, srem = nrows % G;
     const int segn = (int)(sbase + (g < srem ? 1 : 0));
     const int seglo = (int)(g * sbase + (g < srem ? g : srem));
-    uint32_t xd[SW][3][4];          // balanced base-256 digits of the fixed-point x piece
+    // balanced base-256 digits of the fixed-point x piece (CD: of its suffix
+    // sums within each chunk)
+    uint32_t xd[SW][ND][4];
     uint32_t stepv = 0;             // bit t: chunk t of this warp lies inside the operator
     for (int slab = 0; slab < a.nslabs; ++slab) {
       stepv = 0;
@@ -524,7 +556,9 @@ __global__ void __launch_bounds__((CONS + 1) * 32, 1) k2_dl(DlArgs a) {
         if (mx > 0.0f && !masked) {
           int ex;
           frexpf(mx, &ex);
-          e = 22 - ex;
+          // |X| <= 2^22; CD: |X| <= 2^21 so that the 512 suffix sums stay
+          // below 2^30 (four balanced digits)
+          e = (CD ? 21 : 22) - ex;
         }
         inv2e = ldexp(1.0, -e);
 #pragma unroll
@@ -532,6 +566,33 @@ __global__ void __launch_bounds__((CONS + 1) * 32, 1) k2_dl(DlArgs a) {
           const int64_t c0 = (int64_t)slab * DL_SLAB + (int64_t)(q + t * WPG) * 512 + lane * 16;
           float* v = xk[SW <= 2 ? t : 0];
           if (SW > 2) dl_x16<F64IO>(a, c0, (stepv >> t) & 1u, v);
+          if (CD) {
+            // S_i = sum of X over columns >= i of the chunk: lane-local suffix,
+            // then the totals of the lanes to the right
+            int32_t sfx[16];
+#pragma unroll
+            for (int k = 15; k >= 0; --k) {
+              const int32_t X = masked ? 0 : __float2int_rn(ldexpf(v[k], e));
+              sfx[k] = k == 15 ? X : X + sfx[k + 1];
+            }
+            int32_t inc = sfx[0];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const int32_t u = __shfl_down_sync(0xffffffffu, inc, o);
+              if (lane + o < 32) inc += u;
+            }
+            const int32_t right = inc - sfx[0];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              int32_t X[4];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) X[i] = sfx[4 * k + i] + right;
+              uint32_t dw[4];
+              x_digits4w(X, dw);
+#pragma unroll
+              for (int d = 0; d < ND; ++d) xd[t][d][k] = dw[d];
+            }
+          } else {
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             int32_t X[4];
@@ -540,6 +601,7 @@ __global__ void __launch_bounds__((CONS + 1) * 32, 1) k2_dl(DlArgs a) {
             uint32_t dw[3];
             x_digits4(X, dw);
             xd[t][0][k] = dw[0]; xd[t][1][k] = dw[1]; xd[t][2][k] = dw[2];
+          }
           }
         }
       }
@@ -561,9 +623,9 @@ __global__ void __launch_bounds__((CONS + 1) * 32, 1) k2_dl(DlArgs a) {
           uint32_t sb[ROWS];
 #pragma unroll
           for (int r = 0; r < ROWS; ++r) sb[r] = ring_s + s_pos[r < nr ? st[r] : st[0]];
-          int32_t Sa[ROWS][6];
-          if (G == 1) dl_rows_phased<SW, ROWS, WPG>(sb, q, stepv, xd, lane, Sa);
-          else dl_rows_lazy<SW, ROWS, WPG>(sb, q, stepv, xd, lane, Sa);
+          int32_t Sa[ROWS][7];
+          if (G == 1) dl_rows_phased<SW, ROWS, WPG, ND>(sb, q, stepv, xd, lane, Sa);
+          else dl_rows_lazy<SW, ROWS, WPG, ND>(sb, q, stepv, xd, lane, Sa);
           __syncwarp();
           if (lane == 0) {
 #pragma unroll
@@ -574,7 +636,7 @@ __global__ void __launch_bounds__((CONS + 1) * 32, 1) k2_dl(DlArgs a) {
           for (int r = 0; r < ROWS; ++r) {
             if (r < nr) {
               const int ir = i + r;
-              const long long Y = dl_warp_sum(Sa[r]) + (ir >= 2 ? 2 * Y1 - Y2 : (ir == 1 ? Y1 : 0));
+              const long long Y = dl_warp_sum<ND>(Sa[r]) + (ir >= 2 ? 2 * Y1 - Y2 : (ir == 1 ? Y1 : 0));
               Y2 = Y1;
               Y1 = Y;
               dl_slot(&slot[(lr + r) * WPG + q], slab == 0, Y, inv2e, lane);
@@ -698,7 +760,22 @@ int dl_build(invop_plan* p, cudaStream_t s) {
   if (!p->dl_rowlo) INVOP_CUDA(cudaMalloc(&p->dl_rowlo, (size_t)(a.grid + 1) * 8));
   INVOP_CUDA(cudaMemcpyAsync(p->dl_rowlo, lo.data(), lo.size() * 8, cudaMemcpyHostToDevice, s));
   a.rowlo = p->dl_rowlo;
+  a.cd = 0;
   k_dl_width<<<(unsigned)cdiv(warps * 32, 256), 256, 0, s>>>(a, width);
+  {
+    // INVOP_DL_CD=1: column differences inside the chunks (the kernel then
+    // multiplies by suffix sums of x). Measured at config 4: 423.9 -> 357.3 MB
+    // per apply but 0.0665 -> 0.0697 ms: the x-side operand grows from 3 to 4
+    // digit planes (+13 % DP4A) and the kernel turns issue-bound, so it is
+    // opt-in. One consumer group only (x digits per chunk live in registers).
+    const char* ce = getenv("INVOP_DL_CD");
+    const bool cd_ok = a.groups == 1 && dl_consumers() == 16 && !getenv("INVOP_DL_ROWS");
+    if (cd_ok && ce && *ce == '1') {
+      a.cd = 1;
+      k_dl_width<<<(unsigned)cdiv(warps * 32, 256), 256, 0, s>>>(a, width);
+    }
+    p->dl_cd = a.cd;
+  }
   if (a.grid > 1 && layout_flag_dl("INVOP_DL_BALANCE", false)) {
     std::vector<uint8_t> w((size_t)p->rows * a.nch);
     INVOP_CUDA(cudaMemcpyAsync(w.data(), width, w.size(), cudaMemcpyDeviceToHost, s));
@@ -759,10 +836,10 @@ int dl_build(invop_plan* p, cudaStream_t s) {
   return INVOP_OK;
 }
 
-template <int CONS, int G, int ROWS, bool F64IO>
+template <int CONS, int G, int ROWS, bool F64IO, bool CD = false>
 static cudaError_t dl_launch(const DlArgs& a, int grid, size_t smem, bool pdl, cudaStream_t s) {
   static size_t smem_set = 0;            // opt-in once per instantiation and size
-  auto kern = k2_dl<CONS, G, ROWS, F64IO>;
+  auto kern = k2_dl<CONS, G, ROWS, F64IO, CD>;
   if (smem_set < smem) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     smem_set = smem;
@@ -803,9 +880,11 @@ int apply_dl_launch(invop_plan* p, const void* x, void* y, bool f64io, cudaStrea
   const size_t smem = (size_t)ring + side;
   int rows = 2;
   if (const char* v = getenv("INVOP_DL_ROWS")) rows = atoi(v) == 1 ? 1 : 2;
-  const int key = cons * 1000 + p->dl_groups * 100 + rows * 10 + (f64io ? 1 : 0);
+  const int key = p->dl_cd * 100000 + cons * 1000 + p->dl_groups * 100 + rows * 10 + (f64io ? 1 : 0);
   cudaError_t e = cudaSuccess;
   switch (key) {
+    case 116120: e = dl_launch<16, 1, 2, false, true>(a, p->dl_grid, smem, dl_pdl_env(), s); break;
+    case 116121: e = dl_launch<16, 1, 2, true, true>(a, p->dl_grid, smem, dl_pdl_env(), s); break;
     case 16120: e = dl_launch<16, 1, 2, false>(a, p->dl_grid, smem, dl_pdl_env(), s); break;
     case 16121: e = dl_launch<16, 1, 2, true>(a, p->dl_grid, smem, dl_pdl_env(), s); break;
     case 16110: e = dl_launch<16, 1, 1, false>(a, p->dl_grid, smem, dl_pdl_env(), s); break;

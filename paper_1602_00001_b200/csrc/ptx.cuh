@@ -87,6 +87,26 @@ __device__ __forceinline__ void x_digits4(const int32_t* X, uint32_t* w) {
   w[0] = p0; w[1] = p1; w[2] = p2;
 }
 
+// balanced base-256 digits of |X| < 2^31 - 2^23: four digits, packed like x_digits4
+__device__ __forceinline__ void x_digits4w(const int32_t* X, uint32_t* w) {
+  uint32_t p0 = 0, p1 = 0, p2 = 0, p3 = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int32_t x = X[i];
+    const int32_t d0 = ((x + 128) & 255) - 128;
+    const int32_t x1 = (x - d0) >> 8;
+    const int32_t d1 = ((x1 + 128) & 255) - 128;
+    const int32_t x2 = (x1 - d1) >> 8;
+    const int32_t d2 = ((x2 + 128) & 255) - 128;
+    const int32_t d3 = (x2 - d2) >> 8;
+    p0 |= (uint32_t)(d0 & 255) << (8 * i);
+    p1 |= (uint32_t)(d1 & 255) << (8 * i);
+    p2 |= (uint32_t)(d2 & 255) << (8 * i);
+    p3 |= (uint32_t)(d3 & 255) << (8 * i);
+  }
+  w[0] = p0; w[1] = p1; w[2] = p2; w[3] = p3;
+}
+
 // PRMT with the full selector nibble (bit 3 = replicate the sign of the
 // selected byte); __byte_perm only honours the low 3 bits of each nibble.
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {

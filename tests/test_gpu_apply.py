@@ -662,6 +662,17 @@ def test_dl_row_residuals(invop, O, amp, signed, N, groups, monkeypatch):
         assert y_dl.tobytes() == y_st.tobytes()
     else:
         assert relerr(y_dl, y_st.astype(np.float64)) <= 2e-6
+    if groups == 1 and dplan.code_bytes > 1:
+        # opt-in variant: column differences inside the chunks against suffix
+        # sums of a 22-bit fixed-point x (fewer bytes; same tolerance)
+        monkeypatch.setenv("INVOP_DL", "1")
+        monkeypatch.setenv("INVOP_DL_CD", "1")
+        dcd = invop._plan.DevicePlan.from_mantissas(mant, 4, row0=0, n=N)
+        y_cd = dcd.apply_device(xt, mode=0).cpu().numpy()
+        assert dcd.apply_kernel(1) == "k2_dl"
+        assert relerr(y_cd, yo) <= F32_TOL
+        monkeypatch.delenv("INVOP_DL_CD")
+        del dcd
     # host fp64 entry: the DL kernel reads fp64 x / writes fp64 y itself
     monkeypatch.setenv("INVOP_DL", "1")
     yh = dplan.apply_host(x, mode=0)
