@@ -11,8 +11,8 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --c
   --log-file $out/launches_cfg5.csv python bench.py --config 5 $B > $out/ncu_bench5.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k2_dl" -c 1 \
   -o $out/k2_dl_cfg4 python tools/profile_apply.py 4 fast 1 > $out/ncu_k2dl.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k3_dl2" -c 1 \
-  -o $out/k3_dl2_cfg5 python tools/profile_apply.py 5 fast 64 > $out/ncu_k3.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k3_dl2|k3_batched" -c 1 \
+  -o $out/k3_cfg5 python tools/profile_apply.py 5 fast 64 > $out/ncu_k3.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k3_xmax|k3_digits|k3_post" -c 3 \
   -o $out/k3_side_cfg5 python tools/profile_apply.py 5 fast 64 > $out/ncu_k3side.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k2_ordered" -c 1 \
