@@ -67,7 +67,7 @@ extern "C" int invop_plan_destroy(invop_plan* p) {
   if (p->dev_x) cudaFree(p->dev_x);
   if (p->dev_y) cudaFree(p->dev_y);
   if (p->k3_ws) cudaFree(p->k3_ws);
-  for (int b = 0; b < 2; ++b)
+  for (int b = 0; b < 3; ++b)
     if (p->k3_tiles[b]) cudaFree(p->k3_tiles[b]);
   if (p->hl_data) cudaFree(p->hl_data);
   if (p->hl_rowptr) cudaFree(p->hl_rowptr);

@@ -204,7 +204,8 @@ __host__ __device__ constexpr uint32_t idesc_i8(int a_signed, int n = K3_NR) {
 template <int P, int TILES, int STAGES, bool DL>
 __global__ void __launch_bounds__(K3_THREADS, 1)
     k3_batched(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapA1,
-               const __grid_constant__ CUtensorMap mapB, K3Args a) {
+               const __grid_constant__ CUtensorMap mapA2, const __grid_constant__ CUtensorMap mapB,
+               K3Args a) {
   constexpr int NACC = P + K3_ND - 1;                      // weights 0 .. P+1
   constexpr int A_BYTES = TILES * P * K3_A_TILE;
   constexpr int STAGE = A_BYTES + K3_ND * K3_B_TILE;
@@ -324,6 +325,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
               const int trow = (int)(((int64_t)(row0 / K3_BM + ti) * a.kb_stride + kb) * K3_BM);
               tma_2d(sb + (ti * P + 0) * K3_A_TILE, &mapA0, 0, trow, fb, pol_a);
               if (P > 1) tma_2d(sb + (ti * P + 1) * K3_A_TILE, &mapA1, 0, trow, fb, pol_a);
+              if (P > 2) tma_2d(sb + (ti * P + 2) * K3_A_TILE, &mapA2, 0, trow, fb, pol_a);
             }
           }
           // the three digit tiles are consecutive rows of B: one 192-row box
@@ -898,7 +900,7 @@ __device__ __forceinline__ int k3q_pad(int k) { return k + (k >> 4); }
 struct K3Post {
   long long* yacc;
   int64_t rows, n, ld;
-  const uint8_t* planes[2];
+  const uint8_t* planes[3];
   int P, sgn;
   const int* e;
   double scale;
@@ -1020,6 +1022,7 @@ __device__ __forceinline__ float k3q_nonfinite(const K3Post& a, int t, int64_t r
     const int64_t off = r * a.ld + j;
     uint32_t u = a.planes[0][off];
     if (a.P > 1) u |= (uint32_t)a.planes[1][off] << 8;
+    if (a.P > 2) u |= (uint32_t)a.planes[2][off] << 16;
     const int sh = 32 - 8 * a.P;
     const int32_t q = a.sgn ? ((int32_t)(u << sh) >> sh) : (int32_t)u;
     if (q == 0) continue;
@@ -1505,17 +1508,17 @@ static int launch_cluster(Kern kern, const Arg& arg, int nr, int threads, int cl
 }
 
 bool batched_supported(const invop_plan* p, int64_t nrhs) {
-  return p->P <= 2 && nrhs >= 8 && p->n >= K3_BK && p->rows >= 1 && encode_fn() != nullptr;
+  return p->P <= 3 && nrhs >= 8 && p->n >= K3_BK && p->rows >= 1 && encode_fn() != nullptr;
 }
 
 template <int P, int TILES, int STAGES, bool DL = false>
-static int launch_k3(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b,
-                     const K3Args& args, int grid, cudaStream_t s) {
+static int launch_k3(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& a2,
+                     const CUtensorMap& b, const K3Args& args, int grid, cudaStream_t s) {
   constexpr int STAGE = TILES * P * K3_A_TILE + K3_ND * K3_B_TILE;
   size_t smem = (size_t)STAGES * STAGE + 1024 + (DL ? (P == 2 ? K3_B_TILE : K3_A_TILE) : 0);
   auto kern = k3_batched<P, TILES, STAGES, DL>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<grid, K3_THREADS, smem, s>>>(a0, a1, b, args);
+  kern<<<grid, K3_THREADS, smem, s>>>(a0, a1, a2, b, args);
   INVOP_CHECK_LAUNCH("k3_batched");
   return INVOP_OK;
 }
@@ -1786,6 +1789,7 @@ static int batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, 
   // variant: row tiles per unit (share B) and pipeline depth
   int tiles = K3_TILES, stages = K3_STAGES;
   if (const char* v = getenv("INVOP_K3_CFG")) sscanf(v, "%d,%d", &tiles, &stages);
+  if (p->P == 3) { tiles = 1; stages = 5; }     // the one 3-plane configuration
   const int sms = num_sms();
   int krc = k3d_build(p, s);
   if (krc != INVOP_OK && krc != INVOP_E_UNSUPPORTED) return krc;
@@ -1796,7 +1800,9 @@ static int batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, 
   const int slots = pair ? k3_pair_slots() : sms;
   // K splits: each unit spans <= 32768 columns; then pick the split count that
   // best fills the SMs (SM pairs) in whole waves
-  int min_split = (int)cdiv(kblocks, K3_KMAX / K3_BK);
+  // int32 class sums: up to min(P, 3) products of at most 255 * 128 per column
+  const int kmax = p->P >= 3 ? K3_KMAX / 2 : K3_KMAX;
+  int min_split = (int)cdiv(kblocks, kmax / K3_BK);
   int best = min_split;
   double best_eff = -1.0;
   for (int sp = min_split; sp <= std::max(min_split, 16); ++sp) {
@@ -1850,6 +1856,8 @@ static int batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, 
     rc = make_map_u8((CUtensorMap*)p->k3_mapA[0], p->k3_tiles[0], K3_BK, trows, K3_BK, K3_BK, K3_BM);
     if (!rc && p->P > 1)
       rc = make_map_u8((CUtensorMap*)p->k3_mapA[1], p->k3_tiles[1], K3_BK, trows, K3_BK, K3_BK, K3_BM);
+    if (!rc && p->P > 2)
+      rc = make_map_u8((CUtensorMap*)p->k3_mapA[2], p->k3_tiles[2], K3_BK, trows, K3_BK, K3_BK, K3_BM);
     if (rc) return rc;
     if (p->P == 1) memcpy(p->k3_mapA[1], p->k3_mapA[0], sizeof(CUtensorMap));
     p->k3_maps_ready = 1;
@@ -1883,6 +1891,7 @@ static int batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, 
     q.yacc = yacc; q.rows = p->rows; q.n = p->n; q.ld = p->ld;
     q.planes[0] = p->planes[0];
     q.planes[1] = p->planes[p->P > 1 ? 1 : 0];
+    q.planes[2] = p->planes[p->P > 2 ? 2 : 0];
     q.P = p->P; q.sgn = p->is_signed;
     q.e = e; q.scale = p->scale;
     q.nf_count = nfc; q.nf_cols = nfl; q.y01 = y01; q.maxbits = maxb;
@@ -1924,15 +1933,17 @@ static int batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, 
           pa.ysh = p->k3d_ysh; pa.btile = btile;
           rc = launch_k3_dl2(*A0, *A1, mapB, pa, grid, s);
         } else {
-          rc = launch_k3<2, 2, K3_DL_STAGES, true>(*A0, *A1, mapB, a, grid, s);
+          rc = launch_k3<2, 2, K3_DL_STAGES, true>(*A0, *A1, *A1, mapB, a, grid, s);
         }
         break;
-      case 124: rc = launch_k3<1, 2, 4>(*A0, *A1, mapB, a, grid, s); break;
-      case 116: rc = launch_k3<1, 1, 6>(*A0, *A1, mapB, a, grid, s); break;
-      case 224: rc = launch_k3<2, 2, 4>(*A0, *A1, mapB, a, grid, s); break;
-      case 216: rc = launch_k3<2, 1, 6>(*A0, *A1, mapB, a, grid, s); break;
-      case 214: rc = launch_k3<2, 1, 4>(*A0, *A1, mapB, a, grid, s); break;
-      case 223: rc = launch_k3<2, 2, 3>(*A0, *A1, mapB, a, grid, s); break;
+      case 124: rc = launch_k3<1, 2, 4>(*A0, *A1, *A1, mapB, a, grid, s); break;
+      case 116: rc = launch_k3<1, 1, 6>(*A0, *A1, *A1, mapB, a, grid, s); break;
+      case 224: rc = launch_k3<2, 2, 4>(*A0, *A1, *A1, mapB, a, grid, s); break;
+      case 216: rc = launch_k3<2, 1, 6>(*A0, *A1, *A1, mapB, a, grid, s); break;
+      case 214: rc = launch_k3<2, 1, 4>(*A0, *A1, *A1, mapB, a, grid, s); break;
+      case 223: rc = launch_k3<2, 2, 3>(*A0, *A1, *A1, mapB, a, grid, s); break;
+      // 3-byte codes: one row tile per unit (5 weight classes x 64 TMEM columns)
+      case 315: rc = launch_k3<3, 1, 5>(*A0, *A1, *(const CUtensorMap*)p->k3_mapA[2], mapB, a, grid, s); break;
       default: return fail(INVOP_E_VALUE, "unsupported INVOP_K3_CFG");
     }
     if (rc) return rc;

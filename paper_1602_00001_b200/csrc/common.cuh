@@ -37,7 +37,7 @@ struct invop_plan {
   void* shard_stage = nullptr; size_t shard_stage_bytes = 0;   // sharded.cu all-gather staging
   // K3 (tensor-core batched apply): workspace and cached TMA descriptors
   void* k3_ws = nullptr; size_t k3_ws_bytes = 0;
-  uint8_t* k3_tiles[2] = {nullptr, nullptr};   // tiled copy of planes 0/1
+  uint8_t* k3_tiles[3] = {nullptr, nullptr, nullptr};   // tiled copy of planes 0..2
   // HL layout (hl.cu): two low byte planes + top plane only where a chunk needs it
   uint8_t* hl_data = nullptr;
   int64_t* hl_rowptr = nullptr;     // [rows+1] byte offsets
@@ -51,7 +51,7 @@ struct invop_plan {
   int64_t* dl_rowlo = nullptr;      // [grid + 1] CTA row ranges (byte-balanced)
   int64_t dl_maxrows = 0;
   int dl_cd = 0;                    // residuals stored as column differences inside each chunk
-  alignas(64) unsigned char k3_mapA[2][128];
+  alignas(64) unsigned char k3_mapA[3][128];
   int k3_maps_ready = 0;
   // K3 on row residuals (batched.cu): digit-0 tiles for every (row tile, K
   // block), digit-1 tiles only where needed (compact, indexed by k3d_idx1)

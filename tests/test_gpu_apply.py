@@ -967,3 +967,37 @@ def test_ordered_many_rhs_and_unaligned_x(invop, O):
         assert xv.data_ptr() % 16 == 8
         y = plan.device_plan.apply_device(xv.reshape(1, n)).cpu().numpy()[0]
         assert y.tobytes() == O.ordered_apply(mant, 4, x).tobytes()
+
+
+@pytest.mark.parametrize("signed", [False, True])
+@pytest.mark.parametrize("rows,N,k", [(300, 4096, 24), (130, 20000, 9), (517, 8192, 64)])
+def test_k3_three_byte_codes(invop, O, signed, rows, N, k):
+    """3-byte codes (config 4's width) with many right-hand sides: the byte-plane
+    tensor-core kernel with three operand planes (five weight classes), exact
+    integer sums, inf/nan columns as the reference loop."""
+    import torch
+
+    rng = np.random.default_rng(rows + N + k + signed)
+    mant = _smooth_rows(rng, rows, N, 3_000_000, signed)
+    if not signed:
+        mant = np.abs(mant)
+    mant[7, ::5] = 0
+    dplan = invop._plan.DevicePlan.from_mantissas(mant, 5, row0=0, n=N)
+    assert dplan.code_bytes == 3
+    X = rng.standard_normal((k, N)).astype(np.float32)
+    X[:, ::13] *= 1e-4
+    Y = dplan.apply_device(torch.tensor(X, device="cuda"), mode=0).cpu().numpy()
+    assert dplan.apply_kernel(k) == "k3_batched"
+    Xr = X.astype(np.float64)
+    for t in sorted({0, 1, k // 2, k - 1}):
+        assert relerr(Y[t], O.ordered_apply(mant, 5, Xr[t])) <= F32_TOL, t
+    # one right-hand side at a time gives the same sums (k2_dl pieces differ: tolerance)
+    y0 = dplan.apply_device(torch.tensor(X[0], device="cuda"), mode=0).cpu().numpy()
+    assert relerr(y0, Y[0].astype(np.float64)) <= 2e-6
+    X[2, 5] = np.inf
+    X[3, 5], X[3, 9] = -np.inf, np.inf
+    X[4, 7] = np.nan
+    Y = dplan.apply_device(torch.tensor(X, device="cuda"), mode=0).cpu().numpy()
+    Xr = X.astype(np.float64)
+    for t in range(2, 6):
+        _nonfinite_match(Y[t], O.ordered_apply(mant, 5, Xr[t]))
