@@ -217,9 +217,9 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
   // DL: an all-zero operand tile after the stages (initialises the
   // accumulator that only digit-1 planes feed when the unit's first K block
   // has none): a B tile (4 KB) for the straight-line issue, an A tile otherwise
-  constexpr int ZERO_BYTES = (P == 2 && K3_ND == 3) ? K3_B_TILE : K3_A_TILE;
+  constexpr int ZERO_BYTES = (P >= 2 && K3_ND == 3) ? K3_B_TILE : K3_A_TILE;
   unsigned char* zero_tile = base + (size_t)STAGES * STAGE;
-  if (DL) {
+  if (DL || P >= 2) {
     for (int i = threadIdx.x; i < ZERO_BYTES / 16; i += blockDim.x)
       reinterpret_cast<uint4*>(zero_tile)[i] = make_uint4(0, 0, 0, 0);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -421,6 +421,36 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
             if (++st == STAGES) { st = 0; ph ^= 1; }
             continue;
 #endif
+          } else if constexpr (!DL && P >= 2 && K3_ND == 3) {
+            // byte planes, straight-line issue with N = 192: plane p x all
+            // three digits is ONE MMA into the contiguous classes p .. p+2; at
+            // a unit's first K step plane 0 starts classes 0-2 and a zero B
+            // tile starts the class each further plane opens (p + 2).
+            if (elect_one()) {
+#pragma unroll
+              for (int kk = 0; kk < K3_BK / 32; ++kk) {
+                const uint32_t cont = (i > 0 || kk > 0) ? 1u : 0u;
+                const uint64_t db = dbase + (uint64_t)((A_BYTES + kk * 32) >> 4);
+#pragma unroll
+                for (int ti = 0; ti < TILES; ++ti) {
+                  const uint32_t t0 = tmem + (uint32_t)(ti * NACC * K3_NR);
+#pragma unroll
+                  for (int p = 0; p < P; ++p) {
+                    const int sg = (p == P - 1) ? a.hi_signed : 0;
+                    const uint64_t ap = dbase + (uint64_t)(((ti * P + p) * K3_A_TILE + kk * 32) >> 4);
+                    if (!cont && p >= 1)
+                      mma_i8(t0 + (uint32_t)((p + 2) * K3_NR), ap, dzero + (uint64_t)((kk * 32) >> 4),
+                             idesc_i8(sg), 0u);
+                    mma_i8(t0 + (uint32_t)(p * K3_NR), ap, db, idesc_i8(sg, K3_ND * K3_NR),
+                           p == 0 ? cont : 1u);
+                  }
+                }
+              }
+              mma_commit(smem_u32(&empty[st]));          // stage free once these MMAs complete
+            }
+            __syncwarp();
+            if (++st == STAGES) { st = 0; ph ^= 1; }
+            continue;
           } else
 #pragma unroll
           for (int kk = 0; kk < K3_BK / 32; ++kk) {
@@ -1515,7 +1545,7 @@ template <int P, int TILES, int STAGES, bool DL = false>
 static int launch_k3(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& a2,
                      const CUtensorMap& b, const K3Args& args, int grid, cudaStream_t s) {
   constexpr int STAGE = TILES * P * K3_A_TILE + K3_ND * K3_B_TILE;
-  size_t smem = (size_t)STAGES * STAGE + 1024 + (DL ? (P == 2 ? K3_B_TILE : K3_A_TILE) : 0);
+  size_t smem = (size_t)STAGES * STAGE + 1024 + (P >= 2 ? K3_B_TILE : (DL ? K3_A_TILE : 0));
   auto kern = k3_batched<P, TILES, STAGES, DL>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   kern<<<grid, K3_THREADS, smem, s>>>(a0, a1, a2, b, args);
