@@ -45,6 +45,25 @@ static bool layout_flag(const char* env, bool dflt) {
   return *v != '0';
 }
 
+// INVOP_K3_BULK=0: operand tiles stored row-major and swizzled by tensor
+// copies (the round-1 form); default: stored pre-swizzled, 1-D bulk copies
+static int k3_bulk_env() {
+  static const int v = []() {
+    const char* e = getenv("INVOP_K3_BULK");
+    return e && *e == '0' ? 0 : 1;
+  }();
+  return v;
+}
+
+// INVOP_K3_BTILE=0: x digits row-major [192][ldb]; default: pre-swizzled tiles
+static int k3_btile_env() {
+  static const int v = []() {
+    const char* e = getenv("INVOP_K3_BTILE");
+    return e && *e == '0' ? 0 : 1;
+  }();
+  return v;
+}
+
 constexpr int K3_BM = 128;            // rows per MMA tile
 constexpr int K3_TILES = 2;           // row tiles per work unit (share B)
 constexpr int K3_BK = 64;             // K bytes per stage (SWIZZLE_64B row)
@@ -76,7 +95,7 @@ struct K3Args {
   int ysh;                 // DL: tensor rows are 64 << ysh bytes wide (2: pre-swizzled tiles)
   int btile;               // x digits stored as pre-swizzled [K block][192][64] tiles
   // pre-swizzled tiles are contiguous images: plain bulk copies (no tensor map)
-  const uint8_t* t0; const uint8_t* t1; const int8_t* B; int bulk;
+  const uint8_t* t0; const uint8_t* t1; const uint8_t* t2; const int8_t* B; int bulk;
 };
 
 __host__ __device__ inline int64_t k3d_tile0(int64_t rt, int64_t kb, int64_t kbs);
@@ -322,7 +341,14 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
 #pragma unroll
             for (int ti = 0; ti < TILES; ++ti) {
               // tiled planes: tile (rt, kb) starts at tensor row (rt*kblocks + kb)*128
-              const int trow = (int)(((int64_t)(row0 / K3_BM + ti) * a.kb_stride + kb) * K3_BM);
+              const int64_t tix = (int64_t)(row0 / K3_BM + ti) * a.kb_stride + kb;
+              const int trow = (int)(tix * K3_BM);
+              if (a.bulk) {
+                k3_bulk(sb + (ti * P + 0) * K3_A_TILE, a.t0 + tix * K3_A_TILE, K3_A_TILE, fb, pol_a);
+                if (P > 1) k3_bulk(sb + (ti * P + 1) * K3_A_TILE, a.t1 + tix * K3_A_TILE, K3_A_TILE, fb, pol_a);
+                if (P > 2) k3_bulk(sb + (ti * P + 2) * K3_A_TILE, a.t2 + tix * K3_A_TILE, K3_A_TILE, fb, pol_a);
+                continue;
+              }
               tma_2d(sb + (ti * P + 0) * K3_A_TILE, &mapA0, 0, trow, fb, pol_a);
               if (P > 1) tma_2d(sb + (ti * P + 1) * K3_A_TILE, &mapA1, 0, trow, fb, pol_a);
               if (P > 2) tma_2d(sb + (ti * P + 2) * K3_A_TILE, &mapA2, 0, trow, fb, pol_a);
@@ -330,7 +356,7 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
           }
           // the three digit tiles are consecutive rows of B: one 192-row box
 #ifndef K3_PROBE_NOB
-          if (DL && a.bulk)
+          if (a.bulk)
             k3_bulk(sb + A_BYTES, a.B + (int64_t)kb * (K3_ND * K3_B_TILE), K3_ND * K3_B_TILE, fb, pol_b);
           else
             tma_2d(sb + A_BYTES, &mapB, a.btile ? 0 : kb * K3_BK,
@@ -554,8 +580,10 @@ __global__ void __launch_bounds__(K3_THREADS, 1)
 // the planes, built once per plan: tile (rt, kb) = rows [128 rt, 128 rt+128) x
 // columns [64 kb, 64 kb+64) stored as one contiguous 8 KB block, tiles of a row
 // tile consecutive along K, so a row tile's whole K range is one contiguous run.
+// presw: 16-byte chunks stored where the 64-byte shared-memory swizzle puts
+// them (the tile is then moved by one 1-D bulk copy).
 __global__ void k3_tile_planes(const uint8_t* __restrict__ in, int64_t rows, int64_t ld,
-                               uint8_t* __restrict__ out, int64_t rtiles) {
+                               uint8_t* __restrict__ out, int64_t rtiles, int presw) {
   const int64_t kbt = ld / K3_BK;
   const int64_t total16 = rtiles * kbt * (K3_A_TILE / 16);
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total16;
@@ -567,7 +595,8 @@ __global__ void k3_tile_planes(const uint8_t* __restrict__ in, int64_t rows, int
     const int64_t row = rt * K3_BM + r;
     uint4 v = make_uint4(0, 0, 0, 0);
     if (row < rows) v = *reinterpret_cast<const uint4*>(in + row * ld + kb * K3_BK + c16 * 16);
-    *reinterpret_cast<uint4*>(out + tile * K3_A_TILE + r * K3_BK + c16 * 16) = v;
+    const int cs = presw ? (c16 ^ ((r >> 1) & 3)) : c16;
+    *reinterpret_cast<uint4*>(out + tile * K3_A_TILE + r * K3_BK + cs * 16) = v;
   }
 }
 
@@ -1878,7 +1907,7 @@ static int batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, 
     for (int b = 0; b < p->P; ++b) {
       if (!p->k3_tiles[b]) INVOP_CUDA(cudaMalloc(&p->k3_tiles[b], tile_bytes));
       k3_tile_planes<<<(unsigned)std::min<int64_t>(cdiv(tile_bytes / 16, 256), sms * 16), 256, 0, s>>>(
-          p->planes[b], p->rows, p->ld, p->k3_tiles[b], rtiles);
+          p->planes[b], p->rows, p->ld, p->k3_tiles[b], rtiles, k3_bulk_env() && k3_btile_env());
       INVOP_LAUNCHED(1);
       INVOP_CHECK_LAUNCH("k3_tile_planes");
     }
@@ -1891,12 +1920,10 @@ static int batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, 
     if (rc) return rc;
     if (p->P == 1) memcpy(p->k3_mapA[1], p->k3_mapA[0], sizeof(CUtensorMap));
     p->k3_maps_ready = 1;
+    p->k3_presw = k3_bulk_env() && k3_btile_env();
   }
   CUtensorMap mapB;
-  static const int btile = []() {
-    const char* e = std::getenv("INVOP_K3_BTILE");
-    return e && *e == '0' ? 0 : 1;
-  }();
+  const int btile = k3_btile_env();
   if (btile)      // [kblocks * 48 rows][256 bytes], one K block's operand = 48 (pair: 24) rows
     rc = make_tensor_map_u8(&mapB, B, 4 * K3_BK, (uint64_t)kblocks * (K3_ND * K3_NR / 4), 4 * K3_BK,
                             4 * K3_BK, pair ? K3_ND * K3_NR / 8 : K3_ND * K3_NR / 4, 0);
@@ -1938,13 +1965,13 @@ static int batched_launch(invop_plan* p, const float* x, int64_t ldx, float* y, 
     a.idx1 = p->k3d_idx1;
     a.ysh = p->k3d_ysh;
     a.btile = btile;
-    a.t0 = p->k3d_tiles[0]; a.t1 = p->k3d_tiles[1]; a.B = B;
-    {
-      static const int bulk_env = []() {
-        const char* e = std::getenv("INVOP_K3_BULK");
-        return e && *e == '0' ? 0 : 1;
-      }();
-      a.bulk = dl && bulk_env && p->k3d_ysh == 2 && btile ? 1 : 0;
+    a.B = B;
+    if (dl) {
+      a.t0 = p->k3d_tiles[0]; a.t1 = p->k3d_tiles[1]; a.t2 = nullptr;
+      a.bulk = k3_bulk_env() && p->k3d_ysh == 2 && btile ? 1 : 0;
+    } else {
+      a.t0 = p->k3_tiles[0]; a.t1 = p->k3_tiles[1]; a.t2 = p->k3_tiles[2];
+      a.bulk = p->k3_presw && btile ? 1 : 0;
     }
     a.rows = p->rows; a.n = p->n; a.P = p->P; a.hi_signed = p->is_signed;
     a.kblocks_total = kblocks; a.kblocks_per_unit = kpu; a.splits = splits;

@@ -53,6 +53,7 @@ struct invop_plan {
   int dl_cd = 0;                    // residuals stored as column differences inside each chunk
   alignas(64) unsigned char k3_mapA[3][128];
   int k3_maps_ready = 0;
+  int k3_presw = 0;                  // tiled planes stored pre-swizzled (bulk copies)
   // K3 on row residuals (batched.cu): digit-0 tiles for every (row tile, K
   // block), digit-1 tiles only where needed (compact, indexed by k3d_idx1)
   alignas(64) unsigned char k3d_mapA[2][128];
