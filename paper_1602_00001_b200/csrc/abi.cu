@@ -98,8 +98,6 @@ extern "C" int invop_plan_info(const invop_plan* p, int64_t* n, int64_t* rows, i
   return INVOP_OK;
 }
 
-static bool aligned16(const void* ptr) { return ((uintptr_t)ptr & 15u) == 0; }
-
 static bool layout_enabled(const char* env, bool dflt) {
   const char* v = getenv(env);
   if (!v || !*v) return dflt;
@@ -110,8 +108,8 @@ static bool layout_enabled(const char* env, bool dflt) {
 // rows: codes of <= 3 bytes take the DL layout (second-order row residuals,
 // default; INVOP_DL=0 disables), 3-byte codes the HL layout when DL is
 // declined (INVOP_HL=0 disables); everything else streams the byte planes
-// (k2_stream / k2_fast). Many right-hand sides of <= 2-byte codes go to the
-// tensor-core kernel (K3; INVOP_NO_TC=1 disables).
+// (k2_stream / k2_fast). Eight or more right-hand sides of <= 3-byte codes go
+// to the tensor-core kernels (K3; INVOP_NO_TC=1 disables).
 enum { ROUTE_PLANES = 0, ROUTE_K3, ROUTE_DL, ROUTE_HL };
 
 static int fast_route(const invop_plan* p, int64_t nrhs) {
@@ -298,6 +296,18 @@ extern "C" int invop_apply_host(invop_plan* p, const double* x, double* y, int64
       return INVOP_OK;
     }
     cudaGetLastError();
+  }
+  if (mode == INVOP_MODE_ORDERED && p->n > 0 && host_alias(y, &ydev)) {
+    // page-locked y: the ordered kernel stores each row's fp64 sum straight
+    // into host memory (one 8-byte store per row; no device-to-host copy). x
+    // is staged in device memory (every block reads all of it).
+    int rc = ensure_scratch(&p->dev_x, &p->dev_x_bytes, xb + 64);
+    if (rc) return rc;
+    INVOP_CUDA(cudaMemcpyAsync(p->dev_x, x, xb, cudaMemcpyHostToDevice, s));
+    rc = apply_ordered_launch(p, (const double*)p->dev_x, p->n, (double*)ydev, p->rows, nrhs, s);
+    if (rc) return rc;
+    INVOP_CUDA(cudaStreamSynchronize(s));
+    return INVOP_OK;
   }
   // fp64 staging + fp32 copies for the fast path
   int rc = ensure_scratch(&p->dev_x, &p->dev_x_bytes, xb + xb / 2 + 64);
