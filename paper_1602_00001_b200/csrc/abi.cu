@@ -267,6 +267,35 @@ extern "C" int invop_apply_host(invop_plan* p, const double* x, double* y, int64
   size_t xb = (size_t)nrhs * p->n * sizeof(double);
   size_t yb = (size_t)nrhs * p->rows * sizeof(double);
   void* ydev = nullptr;
+  {
+    // pageable host buffers (numpy arrays of a reference-style caller): stage
+    // them through plan-owned page-locked memory so that the zero-copy paths
+    // below apply (x copied in, y written by the kernel and copied out);
+    // INVOP_HOST_STAGING=0 keeps the driver's pageable copies
+    static const bool staging = !(getenv("INVOP_HOST_STAGING") && *getenv("INVOP_HOST_STAGING") == '0');
+    void* tmp = nullptr;
+    if (staging && x && y && xb + yb <= ((size_t)64 << 20) && !host_alias(y, &tmp) &&
+        !host_alias(x, &tmp)) {
+      const size_t need = ((xb + 255) & ~(size_t)255) + yb;
+      if (p->host_pinned_bytes < need) {
+        if (p->host_pinned) cudaFreeHost(p->host_pinned);
+        p->host_pinned = nullptr;
+        p->host_pinned_bytes = 0;
+        if (cudaHostAlloc((void**)&p->host_pinned, need, cudaHostAllocDefault) == cudaSuccess)
+          p->host_pinned_bytes = need;
+        else
+          cudaGetLastError();
+      }
+      if (p->host_pinned_bytes >= need) {
+        double* px = p->host_pinned;
+        double* py = (double*)((char*)p->host_pinned + ((xb + 255) & ~(size_t)255));
+        memcpy(px, x, xb);
+        const int rc = invop_apply_host(p, px, py, nrhs, mode, stream);
+        if (rc == INVOP_OK) memcpy(y, py, yb);
+        return rc;
+      }
+    }
+  }
   if (mode == INVOP_MODE_FAST && nrhs == 1 && fast_route(p, 1) == ROUTE_DL &&
       dl_build(p, s) == INVOP_OK && host_alias(y, &ydev)) {
     // page-locked y: the DL kernel writes its fp64 rows straight into host
