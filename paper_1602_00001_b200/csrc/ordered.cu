@@ -10,15 +10,24 @@
 // is fed and how few instructions it spends per element beside the three
 // fp64 operations (coefficient, product, ordered add):
 //
-//  * each warp runs its own TMA pipeline: per 128-column tile one lane issues
-//    ONE 2-D tensor copy per byte plane (box 128 B x 32 rows, 128-byte
-//    swizzle: the row walk of a thread is conflict-free LDS.128) and one bulk
-//    copy of the x tile, completing on a per-stage mbarrier — the copy
-//    engine does the addressing that the per-thread cp.async version spent
-//    ~2 instructions per element on;
+//  * a block is one producer warp plus four consumer warps, one consumer per
+//    SM scheduler (a lone chain is latency-bound: 8 cycles per DADD link, so
+//    what matters is that no two chains share a scheduler while another
+//    idles). Per 128-column tile the producer issues ONE 2-D tensor copy per
+//    byte plane (box 128 B x 128 rows, 128-byte swizzle: a thread's row walk is
+//    conflict-free LDS.128) and one bulk copy of the x tile into a stage ring
+//    shared by the consumers (full / empty mbarriers), and leaves a flag when
+//    the tile's x holds inf/nan (read one tile ahead, off the critical path);
+//  * consumers walk their rows as a software pipeline carried through
+//    registers: the 16 products of chunk c are added while chunk c+1 is decoded
+//    and multiplied — two independent value sets, so ptxas interleaves them
+//    (it schedules a product right before its add otherwise);
 //  * codes are assembled with PRMT (sign-replicate mode supplies the fourth
 //    byte of 3-byte codes whose top bit is clear, so no mask);
-//  * the coefficient is one fp64 operation: fma(2^52 + |v|, s, -2^52 s).
+//  * the coefficient is one fp64 operation: fma(2^52 + |v|, s, -2^52 s);
+//  * more row blocks than SMs: shallower rings, two blocks per SM.
+// INVOP_ORD_PROBE (measurement only): 1 copies without arithmetic, 2 arithmetic
+// without copies, 4 arithmetic without barriers.
 #include "common.cuh"
 #include "ptx.cuh"
 #include <algorithm>
