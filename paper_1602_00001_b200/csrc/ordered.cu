@@ -25,7 +25,9 @@
 //  * codes are assembled with PRMT (sign-replicate mode supplies the fourth
 //    byte of 3-byte codes whose top bit is clear, so no mask);
 //  * the coefficient is one fp64 operation: fma(2^52 + |v|, s, -2^52 s);
-//  * more row blocks than SMs: shallower rings, two blocks per SM.
+//  * more row blocks than SMs: shallower rings, two blocks per SM; more than
+//    two per SM: 224-row blocks of seven consumers reading x from global
+//    memory (all row warps of config 5 in one round).
 // INVOP_ORD_PROBE (measurement only): 1 copies without arithmetic, 2 arithmetic
 // without copies, 4 arithmetic without barriers.
 #include "common.cuh"
@@ -105,8 +107,10 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
 // producer's arrive + the copies' bytes), an empty barrier (one arrive per
 // active consumer warp) and a flag word (tile needs the zero-skip path).
 // NC = 4 puts one consumer on each of the SM's four schedulers.
-template <int P, bool SIGNED, bool SX, int KR, int NC, int S>
-__global__ void __launch_bounds__((NC + 1) * 32, 1)
+// XG: the stages hold the code tiles only and the consumers read x from global
+// memory (L1/L2-resident) — what lets two blocks of seven consumers share an SM.
+template <int P, bool SIGNED, bool SX, int KR, int NC, int S, bool XG = false>
+__global__ void __launch_bounds__((NC + 1) * 32, XG ? 2 : 1)
     k2_ordered(const __grid_constant__ OrdMaps<P> maps, OrdArgs a) {
   extern __shared__ __align__(1024) unsigned char sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -115,7 +119,7 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1)
   constexpr int PLANE_BYTES = NC * 32 * ORD_TILE;           // per plane per stage
   constexpr int CODE_BYTES = PLANE_BYTES;
   constexpr int X_BYTES = ORD_TILE * 8 * KR;                // per stage
-  constexpr int STAGE_BYTES = PLANE_BYTES * P + X_BYTES;
+  constexpr int STAGE_BYTES = PLANE_BYTES * P + (XG ? 0 : X_BYTES);
   const uint32_t sm_s = (uint32_t)__cvta_generic_to_shared(sm);
   const uint32_t ctl_s = sm_s + (uint32_t)S * STAGE_BYTES;  // control words after the stages
   // per stage: full @ +0, empty @ +8, flag @ +16 (padded to 32 bytes)
@@ -159,7 +163,7 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1)
       const int st = (int)(t % ORD_STAGES);
       const uint32_t ph = (uint32_t)((t / ORD_STAGES) & 1);
       const int64_t col0 = t * ORD_TILE;
-      const bool xb = a.xbulk && col0 + ORD_TILE <= a.n;
+      const bool xb = !XG && a.xbulk && col0 + ORD_TILE <= a.n;
       bool fin = true;
 #pragma unroll
       for (int k = 0; k < KR; ++k)
@@ -169,7 +173,7 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1)
       if (t + 1 < ntiles) load_x(t + 1, xn);
       mbar_wait(empty_bar(st), ph ^ 1);      // every consumer released this stage
       const uint32_t sb = sm_s + (uint32_t)st * STAGE_BYTES;
-      if (!xb) {
+      if (!xb && !XG) {
         // tail tile or unaligned x: the lanes copy it (zero past n)
 #pragma unroll
         for (int k = 0; k < KR; ++k)
@@ -283,18 +287,22 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1)
     }
   };
   // products of chunk c against right-hand side k
-  auto chunk_products = [&](uint32_t sb, int c, int k, const double (&d)[16], double (&t2)[16]) {
+  auto chunk_products = [&](uint32_t sb, int64_t t, int c, int k, const double (&d)[16],
+                            double (&t2)[16]) {
     const uint32_t xa = sb + P * CODE_BYTES + (uint32_t)(k * ORD_TILE + c * 16) * 8;
+    // XG: the launcher guarantees 16-byte aligned x rows and n % 128 == 0
+    const double2* xg =
+        reinterpret_cast<const double2*>(a.x + k * a.ldx + t * ORD_TILE + c * 16);
 #pragma unroll
     for (int q2 = 0; q2 < 8; ++q2) {
-      const double2 xv = lds_d2(xa + q2 * 16);
+      const double2 xv = XG ? __ldg(xg + q2) : lds_d2(xa + q2 * 16);
       t2[2 * q2] = __dmul_rn(d[2 * q2], xv.x);
       t2[2 * q2 + 1] = __dmul_rn(d[2 * q2 + 1], xv.y);
     }
   };
   // one tile, straight-line (8 chunks of 16 codes, no guards: rows and columns
   // past the operator are zero-filled by the tensor copy, x past n is zero)
-  auto tile_pass = [&](uint32_t sb, auto masked_tag) {
+  auto tile_pass = [&](uint32_t sb, int64_t t, auto masked_tag) {
     constexpr bool MASKED = decltype(masked_tag)::value;
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
@@ -303,7 +311,7 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1)
 #pragma unroll
       for (int k = 0; k < KR; ++k) {
         double t2[16];
-        chunk_products(sb, c, k, d, t2);
+        chunk_products(sb, t, c, k, d, t2);
         if (MASKED) {
           // the reference's zero skip (_native.pyx:32-46 never sees a zero
           // mantissa): the chain does not advance on a zero code
@@ -331,10 +339,10 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1)
 #pragma unroll
       for (int q = 0; q < 16; ++q) a0 = __dadd_rn(a0, t2[q]);
     };
-    auto products = [&](uint32_t sb, int c, double (&t2)[16]) {
+    auto products = [&](uint32_t sb, int64_t t, int c, double (&t2)[16]) {
       double d[16];
       chunk_coeffs(sb, c, d);
-      chunk_products(sb, c, 0, d, t2);
+      chunk_products(sb, t, c, 0, d, t2);
     };
     bool have = false;         // ttA holds chunk 0 of tile t
     bool waited = false, masked = false;
@@ -349,21 +357,21 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1)
       waited = false;
       if (masked) {
         acc[0] = a0;
-        tile_pass(sb, std::true_type{});
+        tile_pass(sb, t, std::true_type{});
         a0 = acc[0];
         have = false;
         release_tile(t);
         continue;
       }
-      if (!have) products(sb, 0, ttA);
+      if (!have) products(sb, t, 0, ttA);
 #pragma unroll
       for (int c = 0; c < 7; ++c) {
         if ((c & 1) == 0) {
           chain(ttA);
-          products(sb, c + 1, ttB);
+          products(sb, t, c + 1, ttB);
         } else {
           chain(ttB);
-          products(sb, c + 1, ttA);
+          products(sb, t, c + 1, ttA);
         }
       }
       release_tile(t);
@@ -374,7 +382,7 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1)
         waited = true;
         if (!masked) {
           chain(ttB);
-          products(stage_of(t + 1), 0, ttA);
+          products(stage_of(t + 1), t + 1, 0, ttA);
           have = true;
         }
       }
@@ -384,8 +392,8 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1)
   } else {
     for (int64_t t = 0; t < ntiles; ++t) {
       const uint32_t sb = stage_of(t);
-      if (wait_tile(t)) tile_pass(sb, std::true_type{});
-      else tile_pass(sb, std::false_type{});
+      if (wait_tile(t)) tile_pass(sb, t, std::true_type{});
+      else tile_pass(sb, t, std::false_type{});
       release_tile(t);
     }
   }
@@ -404,15 +412,15 @@ constexpr int ord_stages(int P, int KR) {
 }
 
 // the plan's per-plane tensor maps (built once per geometry)
-static int ord_get_maps(const invop_plan* cp, const unsigned char (**out)[128]) {
+static int ord_get_maps(const invop_plan* cp, int box_rows, const unsigned char (**out)[128]) {
   invop_plan* p = const_cast<invop_plan*>(cp);
-  const int64_t geom[4] = {p->rows, p->n, p->ld, p->P};
+  const int64_t geom[4] = {p->rows, p->n, p->ld, p->P * 1000 + box_rows};
   if (p->ord_maps_key != p->planes[0] || memcmp(geom, p->ord_maps_geom, sizeof(geom)) != 0) {
     p->ord_maps_key = nullptr;
     for (int b = 0; b < p->P; ++b) {
       // columns past n and rows past the shard read as zero codes
       int rc = make_tensor_map_u8(p->ord_maps[b], p->planes[b], (uint64_t)p->n, (uint64_t)p->rows,
-                                  (uint64_t)p->ld, ORD_TILE, 32 * ord_nc(p->P), 128);
+                                  (uint64_t)p->ld, ORD_TILE, (uint32_t)box_rows, 128);
       if (rc) return rc;
     }
     memcpy(p->ord_maps_geom, geom, sizeof(geom));
@@ -427,11 +435,13 @@ constexpr int ord_stages2(int P, int KR) {
   return (112 * 1024) / ord_stage_bytes(P, KR) < 4 ? (112 * 1024) / ord_stage_bytes(P, KR) : 4;
 }
 
-template <int P, bool SIGNED, bool SX, int KR, int S>
-static int launch_ord_s(const unsigned char (*maps)[128], OrdArgs a, cudaStream_t s) {
-  constexpr int NC = ord_nc(P);
-  const size_t smem = (size_t)ord_stage_bytes(P, KR) * S + 32 * S;
-  auto kern = k2_ordered<P, SIGNED, SX, KR, NC, S>;
+template <int P, bool SIGNED, bool SX, int KR, int NC, int S, bool XG>
+static int launch_ord_s(const invop_plan* p, OrdArgs a, cudaStream_t s) {
+  const unsigned char (*maps)[128] = nullptr;
+  const int rc = ord_get_maps(p, NC * 32, &maps);
+  if (rc) return rc;
+  const size_t smem = (size_t)(NC * 32 * ORD_TILE * P + (XG ? 0 : ORD_TILE * 8 * KR)) * S + 32 * S;
+  auto kern = k2_ordered<P, SIGNED, SX, KR, NC, S, XG>;
   INVOP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   OrdMaps<P> m;
   memcpy(m.m, maps, sizeof(m.m));
@@ -443,33 +453,48 @@ static int launch_ord_s(const unsigned char (*maps)[128], OrdArgs a, cudaStream_
 }
 
 template <int P, bool SIGNED, bool SX, int KR>
-static int launch_ord_t(const unsigned char (*maps)[128], OrdArgs a, cudaStream_t s) {
+static int launch_ord_t(const invop_plan* p, OrdArgs a, cudaStream_t s) {
+  constexpr int NC = ord_nc(P);
   constexpr int S = ord_stages(P, KR), S2 = ord_stages2(P, KR);
   static_assert(S >= 2, "ordered kernel needs two stages");
   // More row blocks than SMs: shallower rings so that two blocks are resident
   // per SM (the second consumer on each scheduler fills the issue slots the
   // first leaves open; a single consumer is latency-bound on its DADD chain).
   if constexpr (KR == 1 && S2 >= 2 && S2 < S) {
-    static const int force = std::getenv("INVOP_ORD_DEEP") ? atoi(std::getenv("INVOP_ORD_DEEP")) : -1;
-    const bool two = force >= 0 ? force == 0 : cdiv(a.rows, ord_nc(P) * 32) > num_sms();
-    if (two) return launch_ord_s<P, SIGNED, SX, KR, S2>(maps, a, s);
+    // INVOP_ORD_DEEP: 1 one block per SM, 0 two blocks, 2 seven-consumer blocks
+    const char* fe = std::getenv("INVOP_ORD_DEEP");
+    const int force = fe && *fe ? atoi(fe) : -1;
+    const int64_t blocks = cdiv(a.rows, NC * 32);
+    if constexpr (P <= 2) {
+      // Still more than two blocks per SM: blocks of seven consumers (224
+      // rows; two-stage rings of code tiles only, x read from global memory)
+      // when that saves whole rounds of blocks — config 5: 512 blocks in two
+      // rounds become 293 blocks in one.
+      const int64_t slots = 2 * (int64_t)num_sms();
+      const bool wide = a.xbulk && a.n % ORD_TILE == 0 && !a.accumulate &&
+                        cdiv(cdiv(a.rows, 7 * 32), slots) < cdiv(blocks, slots);
+      if (force == 2 || (force < 0 && wide)) {
+        if (a.xbulk && a.n % ORD_TILE == 0)
+          return launch_ord_s<P, SIGNED, SX, KR, 7, 2, true>(p, a, s);
+      }
+    }
+    const bool two = force >= 0 ? force == 0 : blocks > num_sms();
+    if (two) return launch_ord_s<P, SIGNED, SX, KR, NC, S2, false>(p, a, s);
   }
-  return launch_ord_s<P, SIGNED, SX, KR, S>(maps, a, s);
+  return launch_ord_s<P, SIGNED, SX, KR, NC, S, false>(p, a, s);
 }
 
 template <int P, bool SIGNED, bool SX>
-static int launch_ord_p(const unsigned char (*maps)[128], OrdArgs a, int KR, cudaStream_t s) {
-  if (KR >= 4 && P <= 4) return launch_ord_t<P, SIGNED, SX, 4>(maps, a, s);
-  if (KR >= 2) return launch_ord_t<P, SIGNED, SX, 2>(maps, a, s);
-  return launch_ord_t<P, SIGNED, SX, 1>(maps, a, s);
+static int launch_ord_p(const invop_plan* p, OrdArgs a, int KR, cudaStream_t s) {
+  if (KR >= 4 && P <= 4) return launch_ord_t<P, SIGNED, SX, 4>(p, a, s);
+  if (KR >= 2) return launch_ord_t<P, SIGNED, SX, 2>(p, a, s);
+  return launch_ord_t<P, SIGNED, SX, 1>(p, a, s);
 }
 
 int apply_ordered_launch(const invop_plan* p, const double* x, int64_t ldx, double* y,
                          int64_t ldy, int64_t nrhs, cudaStream_t s, bool accumulate) {
   if (p->rows == 0 || nrhs == 0) return INVOP_OK;
-  const unsigned char (*maps)[128] = nullptr;
-  int rc = ord_get_maps(p, &maps);
-  if (rc) return rc;
+  int rc = INVOP_OK;
   // non-negative codes in signed planes decode identically as unsigned (the
   // cheaper coefficient path)
   const int sgn = p->is_signed && p->min_val < 0 ? 1 : 0;
@@ -488,23 +513,23 @@ int apply_ordered_launch(const invop_plan* p, const double* x, int64_t ldx, doub
     static const int probe = std::getenv("INVOP_ORD_PROBE") ? atoi(std::getenv("INVOP_ORD_PROBE")) : 0;
     a.probe = probe;
     switch (p->P * 2 + sgn) {
-      case 2: rc = launch_ord_p<1, false, false>(maps, a, KR, s); break;
-      case 3: rc = launch_ord_p<1, true, false>(maps, a, KR, s); break;
-      case 4: rc = launch_ord_p<2, false, false>(maps, a, KR, s); break;
-      case 5: rc = launch_ord_p<2, true, false>(maps, a, KR, s); break;
-      case 6: rc = sx3 ? launch_ord_p<3, false, true>(maps, a, KR, s)
-                       : launch_ord_p<3, false, false>(maps, a, KR, s); break;
-      case 7: rc = launch_ord_p<3, true, false>(maps, a, KR, s); break;
-      case 8: rc = launch_ord_p<4, false, false>(maps, a, KR, s); break;
-      case 9: rc = launch_ord_p<4, true, false>(maps, a, KR, s); break;
-      case 10: rc = launch_ord_p<5, false, false>(maps, a, KR, s); break;
-      case 11: rc = launch_ord_p<5, true, false>(maps, a, KR, s); break;
-      case 12: rc = launch_ord_p<6, false, false>(maps, a, KR, s); break;
-      case 13: rc = launch_ord_p<6, true, false>(maps, a, KR, s); break;
-      case 14: rc = launch_ord_p<7, false, false>(maps, a, KR, s); break;
-      case 15: rc = launch_ord_p<7, true, false>(maps, a, KR, s); break;
-      case 16: rc = launch_ord_p<8, false, false>(maps, a, KR, s); break;
-      default: rc = launch_ord_p<8, true, false>(maps, a, KR, s); break;
+      case 2: rc = launch_ord_p<1, false, false>(p, a, KR, s); break;
+      case 3: rc = launch_ord_p<1, true, false>(p, a, KR, s); break;
+      case 4: rc = launch_ord_p<2, false, false>(p, a, KR, s); break;
+      case 5: rc = launch_ord_p<2, true, false>(p, a, KR, s); break;
+      case 6: rc = sx3 ? launch_ord_p<3, false, true>(p, a, KR, s)
+                       : launch_ord_p<3, false, false>(p, a, KR, s); break;
+      case 7: rc = launch_ord_p<3, true, false>(p, a, KR, s); break;
+      case 8: rc = launch_ord_p<4, false, false>(p, a, KR, s); break;
+      case 9: rc = launch_ord_p<4, true, false>(p, a, KR, s); break;
+      case 10: rc = launch_ord_p<5, false, false>(p, a, KR, s); break;
+      case 11: rc = launch_ord_p<5, true, false>(p, a, KR, s); break;
+      case 12: rc = launch_ord_p<6, false, false>(p, a, KR, s); break;
+      case 13: rc = launch_ord_p<6, true, false>(p, a, KR, s); break;
+      case 14: rc = launch_ord_p<7, false, false>(p, a, KR, s); break;
+      case 15: rc = launch_ord_p<7, true, false>(p, a, KR, s); break;
+      case 16: rc = launch_ord_p<8, false, false>(p, a, KR, s); break;
+      default: rc = launch_ord_p<8, true, false>(p, a, KR, s); break;
     }
     if (rc) return rc;
     k0 += KR;
