@@ -108,8 +108,9 @@ static bool layout_enabled(const char* env, bool dflt) {
 // rows: codes of <= 3 bytes take the DL layout (second-order row residuals,
 // default; INVOP_DL=0 disables), 3-byte codes the HL layout when DL is
 // declined (INVOP_HL=0 disables); everything else streams the byte planes
-// (k2_stream / k2_fast). Eight or more right-hand sides of <= 3-byte codes go
-// to the tensor-core kernels (K3; INVOP_NO_TC=1 disables).
+// (k2_stream / k2_fast). Two or more right-hand sides of <= 3-byte codes go
+// to the tensor-core kernels (K3; INVOP_NO_TC=1 disables; tiny operators with
+// fewer than eight right-hand sides stay on k2_fast).
 enum { ROUTE_PLANES = 0, ROUTE_K3, ROUTE_DL, ROUTE_HL };
 
 static int fast_route(const invop_plan* p, int64_t nrhs) {

@@ -1567,7 +1567,18 @@ static int launch_cluster(Kern kern, const Arg& arg, int nr, int threads, int cl
 }
 
 bool batched_supported(const invop_plan* p, int64_t nrhs) {
-  return p->P <= 3 && nrhs >= 8 && p->n >= K3_BK && p->rows >= 1 && encode_fn() != nullptr;
+  // Two or more right-hand sides: one pass of the tensor-core kernel over the
+  // operator (HBM-bound) beats per-RHS / 4-RHS passes of the CUDA-core kernels
+  // (config 4: 7 RHS 0.716 -> 0.125 ms; config 5: 8.04 -> 0.763 ms).
+  // INVOP_K3_MIN_RHS restores a higher threshold (round 1: 8).
+  static const int min_rhs = []() {
+    const char* e = getenv("INVOP_K3_MIN_RHS");
+    return e && *e ? std::max(2, atoi(e)) : 2;
+  }();
+  // small batches on tiny operators stay on the single-launch kernel (config 1:
+  // 7-10 us against ~19 us for the four-kernel chain)
+  if (nrhs < 8 && p->rows * p->n < ((int64_t)1 << 20)) return false;
+  return p->P <= 3 && nrhs >= min_rhs && p->n >= K3_BK && p->rows >= 1 && encode_fn() != nullptr;
 }
 
 template <int P, int TILES, int STAGES, bool DL = false>
