@@ -460,12 +460,12 @@ static int launch_ord_t(const invop_plan* p, OrdArgs a, cudaStream_t s) {
   // More row blocks than SMs: shallower rings so that two blocks are resident
   // per SM (the second consumer on each scheduler fills the issue slots the
   // first leaves open; a single consumer is latency-bound on its DADD chain).
-  if constexpr (KR == 1 && S2 >= 2 && S2 < S) {
+  if constexpr (S2 >= 2 && S2 < S) {
     // INVOP_ORD_DEEP: 1 one block per SM, 0 two blocks, 2 seven-consumer blocks
     const char* fe = std::getenv("INVOP_ORD_DEEP");
     const int force = fe && *fe ? atoi(fe) : -1;
     const int64_t blocks = cdiv(a.rows, NC * 32);
-    if constexpr (P <= 2) {
+    if constexpr (P <= 2 && KR == 1) {
       // Still more than two blocks per SM: blocks of seven consumers (224
       // rows; two-stage rings of code tiles only, x read from global memory)
       // when that saves whole rounds of blocks — config 5: 512 blocks in two
